@@ -1,0 +1,17 @@
+"""CPU fp64 oracle for Hybrid Tree Attention -- TEST INFRASTRUCTURE ONLY.
+
+Only `tests/`, `__graft_entry__.smoke()` and bench.py's `cpu_baseline` / `--impl reference`
+legs may import this package.  The product library (`paper_2502_17421_b200`) never imports
+it and shares no code with it; see DESIGN.md "Oracle".
+
+Contents
+  attention(...)     explicit-mask fp64 attention (C, hta_oracle.c), steps O1-O7 of
+                     SURVEY.md §8(c) / PAPER.md:195-201, 603-656.
+  merge(parts)       the LSE aggregation of PAPER.md:203-219 (max-shifted, reading Z11).
+  tree_mask(...)     ancestor mask by recursive set walk (oracle/tree.py).
+  accept_greedy(...) longest accepted root path by brute-force enumeration (oracle/tree.py).
+
+Parity status of each function is recorded in DESIGN.md "Oracle pins".
+"""
+from .attention import attention, merge, load_library, build_library  # noqa: F401
+from .tree import tree_mask, accept_greedy  # noqa: F401
