@@ -1,0 +1,405 @@
+"""Benchmark of one verification-attention step (Hybrid Tree Attention, LongSpec arXiv 2502.17421).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl hta|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (sequence-parallel, NCCL)
+
+A step is one pass of the whole hot path for one layer, on seeded synthetic
+inputs shaped like BASELINE.json's workload: a0 tree mask from the parent array (device), a1-a4
+prefix pass + tree pass + LSE merge (hta_forward; hta_forward_seqpar for N > 1, which adds a5,
+the NCCL exchange of head-sliced partials), a6 greedy accepted path (device).  Inputs live in
+HBM; the L2 is flushed (a 512 MiB write) before every timed step and the flush is not timed.
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from workloads import CONFIGS, accept_tokens  # noqa: E402
+from workloads.generators import config_workload  # noqa: E402
+
+DEFAULT_WORKLOAD = "llama8b_64k"   # BASELINE.json configs[2]: "1/2/4/8 x B200"
+METRIC = "verification_attention_tokens_per_s"
+L2_FLUSH_BYTES = 512 << 20
+
+
+def peaks():
+    p = {"hbm_gbs": 6551.0, "bf16_tflops": 1665.4, "bf16_tflops_sustained": 1385.9, "source": "measured"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update({k: float(m[k]) for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in m})
+    except (OSError, ValueError, KeyError):
+        p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+    return p
+
+
+def algorithmic_work(cfg, n_keys):
+    """Per-step algorithmic bytes and FLOPs of the prefix pass: the KV cache
+    is read once; 4*B*T*H*N*d FLOPs (QK^T and PV)."""
+    B, T, H, Hkv, d = cfg["B"], cfg["T"], cfg["H"], cfg["H_kv"], cfg["d"]
+    e = 2 if cfg["dtype"] == "bf16" else 4
+    kv_bytes = 2 * B * n_keys * Hkv * d * e
+    qo_bytes = 2 * B * T * H * d * e
+    flops = 4 * B * T * H * n_keys * d
+    return kv_bytes + qo_bytes, flops
+
+
+class ClockSampler:
+    """nvidia-smi clock / throttle sampling during the timed region (B200_PROFILING.md)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out = ""
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (getattr(self, "out", "") or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle timing
+
+def time_oracle(w, mask_np, budget_s=12.0):
+    """The fp64 oracle as it stands, on a bounded sample of rows of the same workload; returns
+    (tokens/s extrapolated to the whole step, seconds, rows, cores)."""
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    rows_all = [(b, t, h) for b in range(w.B) for t in range(w.T) for h in range(w.H)]
+    R = min(len(rows_all), max(cores, 8))
+    t0 = time.perf_counter()
+    oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask_np, seqlens=w.seqlens,
+                     rows=rows_all[:R], threads=cores)
+    t_cal = time.perf_counter() - t0
+    R2 = min(len(rows_all), max(R, int(R * budget_s / max(t_cal, 1e-3))))
+    step = max(1, len(rows_all) // R2)
+    sample = rows_all[::step][:R2]
+    t0 = time.perf_counter()
+    oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask_np, seqlens=w.seqlens,
+                     rows=sample, threads=cores)
+    dt = time.perf_counter() - t0
+    t_step = dt * len(rows_all) / len(sample)
+    return w.B * w.T / t_step, dt, len(sample), len(rows_all), cores
+
+
+# ----------------------------------------------------------------------------- main
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args, cfg, ws, rank):
+    """--impl reference: the fp64 CPU oracle (this tier's reference arm) on a bounded sample."""
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    w = config_workload(args.workload, seed=0)
+    mask = np.stack([oracle.tree_mask(w.parents[b]) for b in range(w.B)])
+    per = []
+    for _ in range(args.warmup):
+        time_oracle(w, mask, budget_s=args.ref_budget / max(1, args.steps + args.warmup))
+    for _ in range(args.steps):
+        tps, dt, n, tot, cores = time_oracle(w, mask, budget_s=args.ref_budget / max(1, args.steps + args.warmup))
+        per.append(w.B * w.T / tps)
+    t = statistics.mean(per)
+    val = w.B * w.T / t
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, **{k: cfg[k] for k in ("B", "T", "H", "H_kv", "d", "N")}},
+            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{n} of {tot} query rows per step, extrapolated linearly"},
+            "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="hta", choices=["hta", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-all-configs", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=60.0, help="seconds of oracle work for --impl reference")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+    cfg = dict(CONFIGS[args.workload])
+    cfg.pop("desc")
+    if args.impl == "reference":
+        run_reference(args, cfg, ws, rank)
+        return
+
+    import numpy as np
+    from paper_2502_17421_b200 import hta
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    comm = hta.HtaComm(rank, ws) if ws > 1 else None
+
+    # ---- inputs (seeded, synthetic, BASELINE.json workload shape); KV cache resident in HBM
+    w = config_workload(args.workload, seed=0)
+    lo, hi = hta.shard_bounds(w.N, ws, rank)
+    kc = w.k_cache[:, lo:hi].contiguous().to(dev)
+    vc = w.v_cache[:, lo:hi].contiguous().to(dev)
+    sl = torch.clamp(w.seqlens - lo, 0, hi - lo).to(torch.int32).to(dev)
+    parents_h = w.parents[0].contiguous()
+    draft_h, tgt_h, ctx = accept_tokens(parents_h, seed=0, vocab=32000, p_match=0.8)
+    host = {"q": w.q.pin_memory(), "kt": w.k_tree.pin_memory(), "vt": w.v_tree.pin_memory(),
+            "parents": parents_h.pin_memory(), "draft": draft_h.pin_memory(), "tgt": tgt_h.pin_memory()}
+    d_in = {k: v.to(dev) for k, v in host.items()}
+    T = w.T
+    mask = torch.empty(T, T, dtype=torch.uint8, device=dev)
+    Hx = w.H // ws
+    o = torch.empty(w.B, T, Hx, w.d, dtype=w.torch_dtype, device=dev)
+    lse = torch.empty(w.B, Hx, T, dtype=torch.float32, device=dev)
+    path = torch.empty(T, dtype=torch.int32, device=dev)
+    plen = torch.empty(1, dtype=torch.int32, device=dev)
+    bonus = torch.empty(1, dtype=torch.int32, device=dev)
+    shape = hta.make_shape(d_in["q"], k_cache=kc, k_tree=d_in["kt"])
+    if ws > 1:
+        wsb = torch.empty(comm.workspace_size(shape), dtype=torch.uint8, device=dev)
+    else:
+        wsb = torch.empty(hta.workspace_size(shape, torch.cuda.get_device_properties(dev).multi_processor_count),
+                          dtype=torch.uint8, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    o_host = torch.empty(o.shape, dtype=o.dtype).pin_memory()
+    res_host = torch.empty(T + 2, dtype=torch.int32).pin_memory()
+
+    def step(x, events=None):
+        hta.hta_build_tree_mask(x["parents"], mask)                                         # a0
+        if ws > 1:                                                                          # a1-a5
+            comm.forward(x["q"], kc, vc, x["kt"], x["vt"], mask, cache_seqlens_local=sl, o=o, lse_out=lse, ws=wsb)
+        else:                                                                               # a1-a4
+            hta.hta_forward(x["q"], kc, vc, x["kt"], x["vt"], mask, cache_seqlens=sl, o=o, lse_out=lse, ws=wsb,
+                            events=events)
+        hta.hta_accept_greedy(x["parents"], x["draft"], x["tgt"], root=0, context_argmax=ctx,
+                              path=path, path_len=plen, bonus=bonus)                        # a6
+
+    launches_per_step = 4 if ws == 1 else 5
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        step(d_in)
+    torch.cuda.synchronize()
+
+    def timed(fn, K):
+        """Per-step CUDA-event times (ms) of K steps; L2 flushed (untimed) before each."""
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(K):
+            flush.fill_(i & 0xFF)
+            evs[i][0].record()
+            fn(i)
+            evs[i][1].record()
+        torch.cuda.synchronize()
+        barrier()
+        return [a.elapsed_time(b) for a, b in evs]
+
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    with ClockSampler(local) as clk:
+        # (1) device-resident step
+        times = timed(lambda i: step(d_in), args.steps)
+        # (2) dominant kernel (prefix pass) timed on its own launch stream with CUDA events
+        if ws == 1:
+            pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            timed(lambda i: step(d_in, events=pev[i]), args.steps)
+            prefix_ms = statistics.mean(a.elapsed_time(b) for a, b in pev)
+        else:
+            prefix_ms = None
+
+        # (3) end to end through the public API: per-step inputs H2D from pinned host memory,
+        # result (O + accepted path) D2H; the KV cache is resident model state.
+        def e2e_step(i):
+            x = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
+            step(x)
+            o_host.copy_(o, non_blocking=True)
+            res_host[:T].copy_(path, non_blocking=True)
+            res_host[T:T + 1].copy_(plen, non_blocking=True)
+            res_host[T + 1:].copy_(bonus, non_blocking=True)
+        e2e_times = timed(e2e_step, args.steps)
+    clocks = clk.summary()
+
+    t_ms = max_over_ranks(statistics.mean(times))
+    e2e_ms = max_over_ranks(statistics.mean(e2e_times))
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    d2h = o_host.numel() * o_host.element_size() + res_host.numel() * 4
+
+    # roofline of the dominant kernel (per launch = per step, this rank's KV slice)
+    n_keys = hi - lo
+    alg_bytes, alg_flops = algorithmic_work(cfg, n_keys)
+    pk = peaks()
+    roof = None
+    if prefix_ms is not None:
+        t_s = prefix_ms * 1e-3
+        t_mem = alg_bytes / (pk["hbm_gbs"] * 1e9)
+        t_tc = alg_flops / (pk["bf16_tflops"] * 1e12)
+        if t_tc >= t_mem:
+            ach = alg_flops / t_s / 1e12
+            roof = {"bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                    "frac": ach / pk["bf16_tflops"], "traffic": None}
+        else:
+            ach = alg_bytes / t_s / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": ach / pk["hbm_gbs"], "traffic": None}
+        roof.update({"kernel": "prefix_tc_kernel", "kernel_us": prefix_ms * 1e3,
+                     "roofline_us": max(t_mem, t_tc) * 1e6, "frac_of_max_roof": max(t_mem, t_tc) / t_s,
+                     "alg_bytes": alg_bytes, "alg_flops": alg_flops,
+                     "hbm_gbs_achieved": alg_bytes / t_s / 1e9, "tflops_achieved": alg_flops / t_s / 1e12,
+                     "peaks": pk["source"] + " MEASURED_PEAKS.json (burst)"})
+        prof = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+        if os.path.exists(prof):
+            try:
+                roof["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
+            except (OSError, ValueError):
+                pass
+
+    tokens = w.B * T
+    value = tokens / (t_ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms, "us_per_step": t_ms * 1e3, "higher_is_better": True,
+        "scaling": "strong" if ws > 1 else "strong", "vs_baseline": None, "dtype": cfg["dtype"],
+        "data": "synthetic (seeded; value distribution V1 sink+local; beam-search tree)",
+        "config": {"workload": args.workload, "B": w.B, "T": T, "H": w.H, "H_kv": w.H_kv, "d": w.d, "N": w.N,
+                   "parallelism": f"seq{ws}", "l2": "flushed (512 MiB write) before every timed step",
+                   "step": "a0 mask + hta_forward (a1-a4) + accept (a6)" + (" + NCCL exchange (a5)" if ws > 1 else "")},
+        "clocks": clocks,
+        "gpu_launches": launches_per_step * args.steps,
+        "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "note": "per-step inputs (q, tree K/V, parents, draft/target tokens) H2D; KV cache resident"},
+        "roofline": roof,
+    }
+
+    # ---- cpu baseline (rank 0, N = 1 only): the oracle as it stands, bounded sample
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        import oracle
+        mask_np = np.stack([oracle.tree_mask(w.parents[b]) for b in range(w.B)])
+        tps, dt, n, tot, cores = time_oracle(w, mask_np)
+        line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                                "sample": f"{n} of {tot} query rows ({dt:.1f} s), extrapolated linearly"}
+
+    # ---- the other BASELINE configs (N = 1): µs/step, device-resident, L2 flushed
+    if rank == 0 and ws == 1 and not args.no_all_configs:
+        others = {}
+        for name in CONFIGS:
+            if name == args.workload:
+                continue
+            others[name] = bench_config(name, dev, flush, k=max(5, args.steps // 5))
+        line["all_configs_us_per_step"] = others
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+        torch.distributed.destroy_process_group()
+
+
+def bench_config(name, dev, flush, k=10):
+    from paper_2502_17421_b200 import hta
+    w = config_workload(name, seed=0)
+    x = {"q": w.q.to(dev), "kc": w.k_cache.to(dev), "vc": w.v_cache.to(dev), "kt": w.k_tree.to(dev),
+         "vt": w.v_tree.to(dev), "parents": w.parents[0].to(dev)}
+    mask = hta.hta_build_tree_mask(x["parents"])
+    o, lse = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask)
+    shape = hta.make_shape(x["q"], k_cache=x["kc"], k_tree=x["kt"])
+    wsb = torch.empty(hta.workspace_size(shape, torch.cuda.get_device_properties(dev).multi_processor_count),
+                      dtype=torch.uint8, device=dev)
+    ts, tp = [], []
+    for i in range(k + 3):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        flush.fill_(i & 0xFF)
+        e[0].record()
+        hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask, o=o, lse_out=lse, ws=wsb)
+        e[1].record()
+        flush.fill_(i & 0xFF)
+        hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask, o=o, lse_out=lse, ws=wsb,
+                        events=(e[2], e[3]))
+        torch.cuda.synchronize()
+        if i >= 3:
+            ts.append(e[0].elapsed_time(e[1]))
+            tp.append(e[2].elapsed_time(e[3]))
+    cfg = dict(CONFIGS[name])
+    b, f = algorithmic_work(cfg, w.N)
+    pk = peaks()
+    t_roof = max(b / (pk["hbm_gbs"] * 1e9), f / (pk["bf16_tflops"] * 1e12))
+    t_pre = statistics.mean(tp) * 1e-3
+    res = {"us_per_step": statistics.mean(ts) * 1e3, "prefix_us": t_pre * 1e6, "roofline_us": t_roof * 1e6,
+           "prefix_frac_of_roofline": t_roof / t_pre, "tokens_per_s": w.B * w.T / (statistics.mean(ts) * 1e-3)}
+    del x, o, lse, wsb
+    torch.cuda.empty_cache()
+    return res
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,537 @@
+// hta_api.cu -- host side of the C ABI declared in include/hta.h: argument validation,
+// work planning (split-KV schedule), TMA descriptor encoding and kernel launches.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "hta_internal.h"
+
+using namespace hta;
+
+namespace {
+
+constexpr int kDefaultSms = 148;
+
+bool is_aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+// Normalised copy of a shape with default strides filled in.
+struct Shape {
+    hta_shape_t s;
+    int G;
+    int64_t esize;
+};
+
+hta_status_t check_shape(const hta_shape_t *in, Shape *out) {
+    if (in == nullptr) return HTA_ERR_INVALID_ARGUMENT;
+    hta_shape_t s = *in;
+    if (s.B < 1 || s.T < 1 || s.T > 256 || s.H < 1 || s.H_kv < 1 || s.H % s.H_kv != 0) return HTA_ERR_INVALID_ARGUMENT;
+    if (s.N_max < 0 || s.N_max > (int64_t(1) << 31) - 1024) return HTA_ERR_INVALID_ARGUMENT;
+    if (!(s.softmax_scale > 0.f) || !std::isfinite(s.softmax_scale)) return HTA_ERR_INVALID_ARGUMENT;
+    if (s.dtype != HTA_BF16 && s.dtype != HTA_FP32) return HTA_ERR_INVALID_ARGUMENT;
+    if (s.num_splits < 0 || s.reserved != 0) return HTA_ERR_INVALID_ARGUMENT;
+    if (s.d != 64 && s.d != 128) return HTA_ERR_UNSUPPORTED;
+    const int64_t d = s.d;
+    auto fill = [](int64_t *st, int64_t a, int64_t b, int64_t c) {
+        if (st[0] == 0 && st[1] == 0 && st[2] == 0) {
+            st[0] = a;
+            st[1] = b;
+            st[2] = c;
+        }
+    };
+    fill(s.q_strides, int64_t(s.T) * s.H * d, int64_t(s.H) * d, d);
+    fill(s.kv_strides, std::max<int64_t>(s.N_max, 1) * s.H_kv * d, int64_t(s.H_kv) * d, d);
+    fill(s.tkv_strides, int64_t(s.T) * s.H_kv * d, int64_t(s.H_kv) * d, d);
+    const int64_t esize = s.dtype == HTA_BF16 ? 2 : 4;
+    const int64_t vec = 16 / esize;  // every row must start 16-byte aligned
+    for (int i = 0; i < 3; ++i) {
+        if (s.q_strides[i] <= 0 || s.kv_strides[i] <= 0 || s.tkv_strides[i] <= 0) return HTA_ERR_INVALID_ARGUMENT;
+        if (s.q_strides[i] % vec || s.kv_strides[i] % vec || s.tkv_strides[i] % vec) return HTA_ERR_INVALID_ARGUMENT;
+    }
+    out->s = s;
+    out->G = s.H / s.H_kv;
+    out->esize = esize;
+    return HTA_OK;
+}
+
+hta_status_t check_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return HTA_ERR_UNSUPPORTED;
+    static std::atomic<int> cached_major[64];
+    static std::atomic<int> cached_sms[64];
+    if (dev < 0 || dev >= 64) return HTA_ERR_UNSUPPORTED;
+    int major = cached_major[dev].load();
+    if (major == 0) {
+        int sms = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess)
+            return HTA_ERR_UNSUPPORTED;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cached_sms[dev].store(sms);
+        cached_major[dev].store(major);
+    }
+    return major == 10 ? HTA_OK : HTA_ERR_UNSUPPORTED;
+}
+
+int device_sms() {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return kDefaultSms;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+        return kDefaultSms;
+    return sms;
+}
+
+// Split-KV work plan.
+PrefixPlan make_plan(const Shape &sh, int num_sms) {
+    const hta_shape_t &s = sh.s;
+    PrefixPlan pl{};
+    pl.G = sh.G;
+    pl.M = s.T * sh.G;
+    if (s.dtype == HTA_BF16) {
+        // Two 128-row tiles per CTA when the rows fill them well, else one.
+        const int rem = pl.M % 256;
+        pl.nt = (pl.M > 128 && (rem == 0 || rem > 128)) ? 2 : 1;
+        pl.n_mgroups = (pl.M + 128 * pl.nt - 1) / (128 * pl.nt);
+        pl.units = s.B * s.H_kv * pl.n_mgroups;
+    } else {
+        pl.nt = 1;
+        pl.n_mgroups = 1;
+        pl.units = (s.B * s.T * s.H + 3) / 4;  // SIMT: 4 rows per block
+    }
+    pl.n_tiles = static_cast<int>((s.N_max + kBlockN - 1) / kBlockN);
+    int S;
+    if (s.num_splits > 0) {
+        S = s.num_splits;
+    } else if (s.dtype == HTA_BF16) {
+        // Fewest waves per unit of work: minimise waves(S) / S with a 1%-per-split penalty
+        // for the partials each split adds (wave quantisation over the SMs, 1 CTA per SM).
+        const int smax = std::max(1, std::min(pl.n_tiles, 4 * num_sms / pl.units + 1));
+        double best = 1e30;
+        S = 1;
+        for (int c = 1; c <= smax; ++c) {
+            const int waves = (pl.units * c + num_sms - 1) / num_sms;
+            const double cost = double(waves) / c * (1.0 + 0.01 * c);
+            if (cost < best - 1e-12) {
+                best = cost;
+                S = c;
+            }
+        }
+    } else {
+        S = (4 * num_sms + pl.units - 1) / pl.units;
+    }
+    if (S < 1) S = 1;
+    if (pl.n_tiles > 0 && S > pl.n_tiles) S = pl.n_tiles;
+    if (pl.n_tiles == 0) S = 1;
+    pl.tiles_per_split = pl.n_tiles > 0 ? (pl.n_tiles + S - 1) / S : 1;
+    pl.splits = pl.n_tiles > 0 ? (pl.n_tiles + pl.tiles_per_split - 1) / pl.tiles_per_split : 1;
+    return pl;
+}
+
+size_t part_floats(const hta_shape_t &s) {
+    return size_t(s.B) * s.T * s.H * s.d + size_t(s.B) * s.H * s.T;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    });
+    return fn;
+}
+
+// 4-D map over a [B, N, H_kv, d] (strided) bf16 cache: box = 64 x 1 x 128 x 1, 128B swizzle.
+hta_status_t make_kv_map(CUtensorMap *map, const void *base, const hta_shape_t &s) {
+    EncodeTiledFn enc = encode_fn();
+    if (enc == nullptr) return HTA_ERR_CUDA;
+    cuuint64_t dims[4] = {cuuint64_t(s.d), cuuint64_t(s.H_kv), cuuint64_t(std::max<int64_t>(s.N_max, 1)),
+                          cuuint64_t(s.B)};
+    cuuint64_t strides[3] = {cuuint64_t(s.kv_strides[2] * 2), cuuint64_t(s.kv_strides[1] * 2),
+                             cuuint64_t(s.kv_strides[0] * 2)};
+    cuuint32_t box[4] = {64, 1, cuuint32_t(kBlockN), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? HTA_OK : HTA_ERR_INVALID_ARGUMENT;
+}
+
+// Enqueue the prefix pass writing `splits` partials at (o_out, lse_out) with the given strides.
+hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, const void *k, const void *v,
+                        const int32_t *seqlens, float *o_out, float *lse_out, int64_t o_split_stride,
+                        int64_t lse_split_stride, cudaStream_t st) {
+    const hta_shape_t &s = sh.s;
+    PrefixParams p{};
+    p.q = q;
+    p.qs0 = s.q_strides[0];
+    p.qs1 = s.q_strides[1];
+    p.qs2 = s.q_strides[2];
+    p.k = k;
+    p.v = v;
+    p.ks0 = s.kv_strides[0];
+    p.ks1 = s.kv_strides[1];
+    p.ks2 = s.kv_strides[2];
+    p.seqlens = seqlens;
+    p.B = s.B;
+    p.T = s.T;
+    p.H = s.H;
+    p.H_kv = s.H_kv;
+    p.d = s.d;
+    p.G = sh.G;
+    p.M = pl.M;
+    p.N_max = s.N_max;
+    p.scale = s.softmax_scale;
+    p.scale_log2 = s.softmax_scale * 1.4426950408889634f;
+    p.nt = pl.nt;
+    p.n_mgroups = pl.n_mgroups;
+    p.splits = pl.splits;
+    p.tiles_per_split = pl.tiles_per_split;
+    p.o_out = o_out;
+    p.lse_out = lse_out;
+    p.o_split_stride = o_split_stride;
+    p.lse_split_stride = lse_split_stride;
+    cudaError_t e;
+    if (s.dtype == HTA_BF16) {
+        CUtensorMap tk, tv;
+        hta_status_t r = make_kv_map(&tk, k, s);
+        if (r != HTA_OK) return r;
+        r = make_kv_map(&tv, v, s);
+        if (r != HTA_OK) return r;
+        e = launch_prefix_tc(p, tk, tv, prefix_tc_smem_bytes(s.d, pl.nt), st);
+    } else {
+        e = launch_prefix_simt(p, st);
+    }
+    return e == cudaSuccess ? HTA_OK : HTA_ERR_CUDA;
+}
+
+TreeMergeParams base_tm(const Shape &sh) {
+    const hta_shape_t &s = sh.s;
+    TreeMergeParams p{};
+    p.B = s.B;
+    p.T = s.T;
+    p.H = s.H;
+    p.H_kv = s.H_kv;
+    p.G = sh.G;
+    p.Hr = s.H;
+    p.h0 = 0;
+    p.qs0 = s.q_strides[0];
+    p.qs1 = s.q_strides[1];
+    p.qs2 = s.q_strides[2];
+    p.ts0 = s.tkv_strides[0];
+    p.ts1 = s.tkv_strides[1];
+    p.ts2 = s.tkv_strides[2];
+    p.scale = s.softmax_scale;
+    p.out_hb = s.H;
+    return p;
+}
+
+void set_out_contig_f32(TreeMergeParams &p, const hta_shape_t &s, float *o, float *lse) {
+    p.o = o;
+    p.os0 = int64_t(s.T) * s.H * s.d;
+    p.os1 = int64_t(s.H) * s.d;
+    p.os2 = s.d;
+    p.lse = lse;
+}
+
+}  // namespace
+
+// =============================================================================== ABI
+
+extern "C" {
+
+const char *hta_status_string(hta_status_t st) {
+    switch (st) {
+        case HTA_OK: return "HTA_OK";
+        case HTA_ERR_INVALID_ARGUMENT: return "HTA_ERR_INVALID_ARGUMENT";
+        case HTA_ERR_UNSUPPORTED: return "HTA_ERR_UNSUPPORTED";
+        case HTA_ERR_INVALID_MASK: return "HTA_ERR_INVALID_MASK";
+        case HTA_ERR_WORKSPACE: return "HTA_ERR_WORKSPACE";
+        case HTA_ERR_CUDA: return "HTA_ERR_CUDA";
+        case HTA_ERR_NCCL: return "HTA_ERR_NCCL";
+    }
+    return "HTA_ERR_UNKNOWN";
+}
+
+int32_t hta_version(void) { return 100; }
+
+size_t hta_workspace_size(const hta_shape_t *shape, int32_t num_sms) {
+    Shape sh;
+    if (check_shape(shape, &sh) != HTA_OK) return size_t(-1);
+    const PrefixPlan pl = make_plan(sh, num_sms > 0 ? num_sms : kDefaultSms);
+    return size_t(pl.splits) * part_floats(sh.s) * sizeof(float);
+}
+
+hta_status_t hta_prefix_attn(const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,
+                             const int32_t *cache_seqlens, float *o_part, float *lse_part, void *ws, size_t ws_bytes,
+                             hta_stream_t stream) {
+    Shape sh;
+    hta_status_t r = check_shape(shape, &sh);
+    if (r != HTA_OK) return r;
+    if (!q || !k_cache || !v_cache || !o_part || !lse_part) return HTA_ERR_INVALID_ARGUMENT;
+    if (!is_aligned(q, 16) || !is_aligned(k_cache, 16) || !is_aligned(v_cache, 16) || !is_aligned(o_part, 16))
+        return HTA_ERR_INVALID_ARGUMENT;
+    if ((r = check_device()) != HTA_OK) return r;
+    const hta_shape_t &s = sh.s;
+    const PrefixPlan pl = make_plan(sh, device_sms());
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (pl.splits == 1)
+        return run_prefix(sh, pl, q, k_cache, v_cache, cache_seqlens, o_part, lse_part, 0, 0, st);
+    const size_t need = size_t(pl.splits) * part_floats(s) * sizeof(float);
+    if (ws == nullptr || ws_bytes < need || !is_aligned(ws, 16)) return HTA_ERR_WORKSPACE;
+    float *o_ws = static_cast<float *>(ws);
+    const int64_t ostride = int64_t(s.B) * s.T * s.H * s.d;
+    float *lse_ws = o_ws + size_t(pl.splits) * ostride;
+    const int64_t lstride = int64_t(s.B) * s.H * s.T;
+    r = run_prefix(sh, pl, q, k_cache, v_cache, cache_seqlens, o_ws, lse_ws, ostride, lstride, st);
+    if (r != HTA_OK) return r;
+    TreeMergeParams p = base_tm(sh);
+    p.do_tree = 0;
+    p.n_parts = pl.splits;
+    p.o_parts = o_ws;
+    p.lse_parts = lse_ws;
+    p.o_part_stride = ostride;
+    p.lse_part_stride = lstride;
+    set_out_contig_f32(p, s, o_part, lse_part);
+    return launch_tree_merge(p, s.d, s.dtype, HTA_FP32, true, st) == cudaSuccess ? HTA_OK : HTA_ERR_CUDA;
+}
+
+hta_status_t hta_tree_attn(const hta_shape_t *shape, const void *q, const void *k_tree, const void *v_tree,
+                           const uint8_t *mask, int64_t mask_batch_stride, float *o_part, float *lse_part,
+                           hta_stream_t stream) {
+    Shape sh;
+    hta_status_t r = check_shape(shape, &sh);
+    if (r != HTA_OK) return r;
+    const hta_shape_t &s = sh.s;
+    if (!q || !k_tree || !v_tree || !mask || !o_part || !lse_part) return HTA_ERR_INVALID_ARGUMENT;
+    if (mask_batch_stride != 0 && mask_batch_stride < int64_t(s.T) * s.T) return HTA_ERR_INVALID_ARGUMENT;
+    if (!is_aligned(q, 16) || !is_aligned(k_tree, 16) || !is_aligned(v_tree, 16) || !is_aligned(o_part, 16))
+        return HTA_ERR_INVALID_ARGUMENT;
+    if ((r = check_device()) != HTA_OK) return r;
+    TreeMergeParams p = base_tm(sh);
+    p.q = q;
+    p.kt = k_tree;
+    p.vt = v_tree;
+    p.mask = mask;
+    p.mask_bs = mask_batch_stride;
+    p.do_tree = 1;
+    p.n_parts = 0;
+    set_out_contig_f32(p, s, o_part, lse_part);
+    return launch_tree_merge(p, s.d, s.dtype, HTA_FP32, false, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? HTA_OK
+               : HTA_ERR_CUDA;
+}
+
+hta_status_t hta_merge_lse(const hta_shape_t *shape, int32_t n_parts, const float *o_parts, const float *lse_parts,
+                           void *o, float *lse_out, hta_stream_t stream) {
+    Shape sh;
+    hta_status_t r = check_shape(shape, &sh);
+    if (r != HTA_OK) return r;
+    const hta_shape_t &s = sh.s;
+    if (n_parts < 1 || !o_parts || !lse_parts || !o) return HTA_ERR_INVALID_ARGUMENT;
+    if (!is_aligned(o_parts, 16) || !is_aligned(o, 16)) return HTA_ERR_INVALID_ARGUMENT;
+    if ((r = check_device()) != HTA_OK) return r;
+    TreeMergeParams p = base_tm(sh);
+    p.do_tree = 0;
+    p.n_parts = n_parts;
+    p.o_parts = o_parts;
+    p.lse_parts = lse_parts;
+    p.o_part_stride = int64_t(s.B) * s.T * s.H * s.d;
+    p.lse_part_stride = int64_t(s.B) * s.H * s.T;
+    p.o = o;
+    p.os0 = s.q_strides[0];
+    p.os1 = s.q_strides[1];
+    p.os2 = s.q_strides[2];
+    p.lse = lse_out;
+    return launch_tree_merge(p, s.d, s.dtype, s.dtype, false, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? HTA_OK
+               : HTA_ERR_CUDA;
+}
+
+hta_status_t hta_forward_timed(const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,
+                               const int32_t *cache_seqlens, const void *k_tree, const void *v_tree,
+                               const uint8_t *mask, int64_t mask_batch_stride, void *o, float *lse_out, void *ws,
+                               size_t ws_bytes, hta_stream_t stream, void *ev_begin, void *ev_end) {
+    Shape sh;
+    hta_status_t r = check_shape(shape, &sh);
+    if (r != HTA_OK) return r;
+    const hta_shape_t &s = sh.s;
+    if (!q || !k_cache || !v_cache || !k_tree || !v_tree || !mask || !o) return HTA_ERR_INVALID_ARGUMENT;
+    if (mask_batch_stride != 0 && mask_batch_stride < int64_t(s.T) * s.T) return HTA_ERR_INVALID_ARGUMENT;
+    if (!is_aligned(q, 16) || !is_aligned(k_cache, 16) || !is_aligned(v_cache, 16) || !is_aligned(k_tree, 16) ||
+        !is_aligned(v_tree, 16) || !is_aligned(o, 16))
+        return HTA_ERR_INVALID_ARGUMENT;
+    if ((r = check_device()) != HTA_OK) return r;
+    const PrefixPlan pl = make_plan(sh, device_sms());
+    const size_t need = size_t(pl.splits) * part_floats(s) * sizeof(float);
+    if (ws == nullptr || ws_bytes < need || !is_aligned(ws, 16)) return HTA_ERR_WORKSPACE;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    float *o_ws = static_cast<float *>(ws);
+    const int64_t ostride = int64_t(s.B) * s.T * s.H * s.d;
+    float *lse_ws = o_ws + size_t(pl.splits) * ostride;
+    const int64_t lstride = int64_t(s.B) * s.H * s.T;
+    if (ev_begin != nullptr && cudaEventRecord(static_cast<cudaEvent_t>(ev_begin), st) != cudaSuccess)
+        return HTA_ERR_CUDA;
+    r = run_prefix(sh, pl, q, k_cache, v_cache, cache_seqlens, o_ws, lse_ws, ostride, lstride, st);
+    if (r != HTA_OK) return r;
+    if (ev_end != nullptr && cudaEventRecord(static_cast<cudaEvent_t>(ev_end), st) != cudaSuccess)
+        return HTA_ERR_CUDA;
+    TreeMergeParams p = base_tm(sh);
+    p.q = q;
+    p.kt = k_tree;
+    p.vt = v_tree;
+    p.mask = mask;
+    p.mask_bs = mask_batch_stride;
+    p.do_tree = 1;
+    p.n_parts = pl.splits;
+    p.o_parts = o_ws;
+    p.lse_parts = lse_ws;
+    p.o_part_stride = ostride;
+    p.lse_part_stride = lstride;
+    p.o = o;
+    p.os0 = s.q_strides[0];
+    p.os1 = s.q_strides[1];
+    p.os2 = s.q_strides[2];
+    p.lse = lse_out;
+    return launch_tree_merge(p, s.d, s.dtype, s.dtype, ev_end == nullptr, st) == cudaSuccess ? HTA_OK
+                                                                                              : HTA_ERR_CUDA;
+}
+
+hta_status_t hta_forward(const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,
+                         const int32_t *cache_seqlens, const void *k_tree, const void *v_tree, const uint8_t *mask,
+                         int64_t mask_batch_stride, void *o, float *lse_out, void *ws, size_t ws_bytes,
+                         hta_stream_t stream) {
+    return hta_forward_timed(shape, q, k_cache, v_cache, cache_seqlens, k_tree, v_tree, mask, mask_batch_stride, o,
+                             lse_out, ws, ws_bytes, stream, nullptr, nullptr);
+}
+
+hta_status_t hta_build_tree_mask(const int32_t *parents, int32_t T, uint8_t *mask, int32_t on_device,
+                                 hta_stream_t stream) {
+    if (T < 1 || T > 256 || parents == nullptr || mask == nullptr) return HTA_ERR_INVALID_ARGUMENT;
+    if (!on_device) return host_build_mask(parents, T, mask) == 0 ? HTA_OK : HTA_ERR_INVALID_MASK;
+    hta_status_t r = check_device();
+    if (r != HTA_OK) return r;
+    return launch_build_mask(parents, T, mask, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? HTA_OK
+                                                                                                    : HTA_ERR_CUDA;
+}
+
+hta_status_t hta_validate_tree_mask(const uint8_t *mask, int32_t T) {
+    if (mask == nullptr || T < 1 || T > 256) return HTA_ERR_INVALID_ARGUMENT;
+    for (int i = 0; i < T; ++i) {
+        const uint8_t *row = mask + int64_t(i) * T;
+        if (row[i] != 1) return HTA_ERR_INVALID_MASK;
+        int par = -1;
+        for (int j = 0; j < T; ++j) {
+            if (row[j] > 1) return HTA_ERR_INVALID_MASK;
+            if (j > i && row[j]) return HTA_ERR_INVALID_MASK;
+            if (j < i && row[j]) par = j;
+        }
+        // row i must equal row(par) + {i} (or {i} alone for a root)
+        for (int j = 0; j < T; ++j) {
+            const uint8_t want = (j == i) ? 1 : (par >= 0 ? mask[int64_t(par) * T + j] : 0);
+            if (row[j] != want) return HTA_ERR_INVALID_MASK;
+        }
+    }
+    return HTA_OK;
+}
+
+hta_status_t hta_accept_greedy(const int32_t *parents, const int32_t *draft_tokens, const int32_t *target_argmax,
+                               int32_t T, int32_t root, int32_t context_argmax, int32_t *path, int32_t *path_len,
+                               int32_t *bonus, int32_t on_device, hta_stream_t stream) {
+    if (T < 1 || T > 256 || root < -1 || root >= T) return HTA_ERR_INVALID_ARGUMENT;
+    if (!parents || !draft_tokens || !target_argmax || !path || !path_len || !bonus) return HTA_ERR_INVALID_ARGUMENT;
+    if (!on_device)
+        return host_accept(parents, draft_tokens, target_argmax, T, root, context_argmax, path, path_len, bonus) == 0
+                   ? HTA_OK
+                   : HTA_ERR_INVALID_MASK;
+    hta_status_t r = check_device();
+    if (r != HTA_OK) return r;
+    return launch_accept(parents, draft_tokens, target_argmax, T, root, context_argmax, path, path_len, bonus,
+                         reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? HTA_OK
+               : HTA_ERR_CUDA;
+}
+
+}  // extern "C"
+
+// ======================================================================= seqpar helpers
+
+namespace hta {
+
+hta_status_t seqpar_local_parts(const hta_shape_t *shape, const void *q, const void *k, const void *v,
+                                const int32_t *seqlens, float *parts_ws, size_t parts_bytes, float *sendb, int P,
+                                cudaStream_t st) {
+    Shape sh;
+    hta_status_t r = check_shape(shape, &sh);
+    if (r != HTA_OK) return r;
+    if ((r = check_device()) != HTA_OK) return r;
+    const hta_shape_t &s = sh.s;
+    const PrefixPlan pl = make_plan(sh, device_sms());
+    const int64_t ostride = int64_t(s.B) * s.T * s.H * s.d;
+    const int64_t lstride = int64_t(s.B) * s.H * s.T;
+    if (size_t(pl.splits) * part_floats(s) * sizeof(float) > parts_bytes) return HTA_ERR_WORKSPACE;
+    float *lse_ws = parts_ws + size_t(pl.splits) * ostride;
+    r = run_prefix(sh, pl, q, k, v, seqlens, parts_ws, lse_ws, ostride, lstride, st);
+    if (r != HTA_OK) return r;
+    const int Hp = s.H / P;
+    const int64_t blk = int64_t(s.B) * s.T * Hp * s.d + int64_t(s.B) * Hp * s.T;
+    TreeMergeParams p = base_tm(sh);
+    p.do_tree = 0;
+    p.n_parts = pl.splits;
+    p.o_parts = parts_ws;
+    p.lse_parts = lse_ws;
+    p.o_part_stride = ostride;
+    p.lse_part_stride = lstride;
+    p.o = sendb;
+    p.os0 = int64_t(s.T) * Hp * s.d;
+    p.os1 = int64_t(Hp) * s.d;
+    p.os2 = s.d;
+    p.o_block_stride = blk;
+    p.lse = sendb + int64_t(s.B) * s.T * Hp * s.d;
+    p.lse_block_stride = blk;
+    p.out_hb = Hp;
+    return launch_tree_merge(p, s.d, s.dtype, HTA_FP32, true, st) == cudaSuccess ? HTA_OK : HTA_ERR_CUDA;
+}
+
+hta_status_t seqpar_final_merge(const hta_shape_t *shape, int P, int rank, const void *q, const void *kt,
+                                const void *vt, const uint8_t *mask, int64_t mask_bs, const float *recvb,
+                                size_t blk_floats, void *o, float *lse, cudaStream_t st) {
+    Shape sh;
+    hta_status_t r = check_shape(shape, &sh);
+    if (r != HTA_OK) return r;
+    const hta_shape_t &s = sh.s;
+    if (mask_bs != 0 && mask_bs < int64_t(s.T) * s.T) return HTA_ERR_INVALID_ARGUMENT;
+    const int Hp = s.H / P;
+    TreeMergeParams p = base_tm(sh);
+    p.Hr = Hp;
+    p.h0 = rank * Hp;
+    p.q = q;
+    p.kt = kt;
+    p.vt = vt;
+    p.mask = mask;
+    p.mask_bs = mask_bs;
+    p.do_tree = 1;
+    p.n_parts = P;
+    p.o_parts = recvb;
+    p.lse_parts = recvb + int64_t(s.B) * s.T * Hp * s.d;
+    p.o_part_stride = int64_t(blk_floats);
+    p.lse_part_stride = int64_t(blk_floats);
+    p.o = o;
+    p.os0 = int64_t(s.T) * Hp * s.d;
+    p.os1 = int64_t(Hp) * s.d;
+    p.os2 = s.d;
+    p.lse = lse;
+    p.out_hb = Hp;
+    return launch_tree_merge(p, s.d, s.dtype, s.dtype, false, st) == cudaSuccess ? HTA_OK : HTA_ERR_CUDA;
+}
+
+}  // namespace hta

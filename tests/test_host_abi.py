@@ -1,0 +1,159 @@
+"""CPU tests of the C ABI: the library loads, exports every symbol include/hta.h declares, and
+its host-side logic (workspace sizing, argument validation, host tree utilities) is right.
+No compute call is made (no GPU here)."""
+import ctypes
+import itertools
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from workloads import accept_tokens, tree_parents
+from paper_2502_17421_b200 import hta
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2502_17421_b200 import build
+    build.build()
+    return hta.lib()
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "hta.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(hta_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_exports_every_header_symbol(L):
+    syms = header_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(hta._SIG), "binding and header disagree"
+
+
+def test_status_strings_and_version(L):
+    for code, name in hta.STATUS.items():
+        assert L.hta_status_string(code).decode() == name
+    assert L.hta_version() >= 100
+
+
+def _shape(B=1, T=64, H=32, H_kv=8, d=128, N=65536, dtype=hta.HTA_BF16, splits=0):
+    s = hta.hta_shape_t()
+    s.B, s.T, s.H, s.H_kv, s.d, s.N_max = B, T, H, H_kv, d, N
+    s.softmax_scale = 1.0 / d ** 0.5
+    s.dtype = dtype
+    s.num_splits = splits
+    return s
+
+
+def test_workspace_size_matches_split_plan(L):
+    part = lambda s: (s.B * s.T * s.H * s.d + s.B * s.H * s.T) * 4
+    # Llama-8B-64k: M = 256 rows per kv head -> 2 row tiles per CTA, 8 units, 148 // 8 = 18 splits
+    s = _shape()
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == 18 * part(s)
+    # forced splits are capped by the number of 128-key tiles
+    s = _shape(N=300, splits=7)
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == 3 * part(s)
+    s = _shape(N=0)
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == 1 * part(s)
+    # QwQ-like: M = 320 -> one tile per CTA, 3 row groups x 8 kv heads x B=4 = 96 units;
+    # 3 splits = 288 CTAs = 1.95 waves (vs 96 CTAs = 0.65 wave for 1 split)
+    s = _shape(B=4, H=40, N=32768)
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == 3 * part(s)
+
+
+@pytest.mark.parametrize("field,value", [("T", 0), ("T", 257), ("H", 30), ("d", 96), ("N_max", -1),
+                                         ("softmax_scale", 0.0), ("softmax_scale", float("nan")),
+                                         ("reserved", 1), ("num_splits", -2), ("dtype", 7)])
+def test_invalid_shapes_rejected_on_host(L, field, value):
+    s = _shape()
+    setattr(s, field, value)
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == ctypes.c_size_t(-1).value
+    # the compute entry points reject it before touching the device
+    rc = L.hta_forward(ctypes.byref(s), *([ctypes.c_void_p(16)] * 7), 0, ctypes.c_void_p(16), None,
+                       ctypes.c_void_p(16), 1 << 30, None)
+    assert rc in (1, 2)
+
+
+def test_misaligned_strides_rejected(L):
+    s = _shape()
+    s.q_strides = (ctypes.c_int64 * 3)(64 * 32 * 128, 32 * 128, 127)
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == ctypes.c_size_t(-1).value
+
+
+def test_null_pointers_rejected(L):
+    s = _shape(N=256)
+    rc = L.hta_forward(ctypes.byref(s), None, *([ctypes.c_void_p(16)] * 6), 0, ctypes.c_void_p(16), None,
+                       ctypes.c_void_p(16), 1 << 30, None)
+    assert rc == 1
+
+
+def test_host_mask_builder_bit_exact_vs_oracle(L):
+    for seed in range(40):
+        T = [1, 2, 8, 17, 64, 128, 200, 256][seed % 8]
+        kind = ["random", "random_forest", "beam", "chain", "star", "heap_binary", "roots"][seed % 7]
+        par = tree_parents(kind, T, seed=seed)
+        m = hta.hta_build_tree_mask(par)
+        np.testing.assert_array_equal(m.numpy(), oracle.tree_mask(par))
+        assert hta.hta_validate_tree_mask(m)
+
+
+def test_host_mask_builder_rejects_bad_parents(L):
+    for bad in ([0], [-1, 1], [-1, 0, 3], [-3, -1]):
+        with pytest.raises(hta.HtaError):
+            hta.hta_build_tree_mask(torch.tensor(bad, dtype=torch.int32))
+
+
+def test_validator_rejects_non_tree_masks(L):
+    good = oracle.tree_mask(tree_parents("heap_binary", 8))
+    assert hta.hta_validate_tree_mask(torch.from_numpy(good))
+    bad = good.copy()
+    bad[3, 3] = 0                       # not reflexive
+    assert not hta.hta_validate_tree_mask(torch.from_numpy(bad))
+    bad = good.copy()
+    bad[1, 5] = 1                       # sees a later node
+    assert not hta.hta_validate_tree_mask(torch.from_numpy(bad))
+    bad = good.copy()
+    bad[7, 0] = 0                       # not ancestor-closed (misses the root)
+    assert not hta.hta_validate_tree_mask(torch.from_numpy(bad))
+
+
+def test_host_accept_bit_exact_vs_oracle(L):
+    for seed in range(400):
+        T = [1, 3, 8, 17, 64, 128, 256][seed % 7]
+        kind = ["random", "random_forest", "beam", "chain", "star"][seed % 5]
+        par = tree_parents(kind, T, seed=seed)
+        draft, tgt, ctx = accept_tokens(par, seed, vocab=4, p_match=0.8, distinct_siblings=(seed % 2 == 0))
+        for root in (0, -1) if kind != "random_forest" else (-1,):
+            got = hta.hta_accept_greedy(par, draft, tgt, root=root, context_argmax=ctx)
+            want = oracle.accept_greedy(par, draft, tgt, root=root, context_argmax=ctx)
+            assert got == (want[0], want[1]), (seed, root)
+
+
+def test_host_accept_exhaustive_small(L):
+    for T in range(1, 5):
+        for par in itertools.product(*[range(-1, i) for i in range(T)]):
+            p = torch.tensor(par, dtype=torch.int32)
+            for bits in range(1 << T):
+                draft = torch.tensor([(bits >> i) & 1 for i in range(T)], dtype=torch.int32)
+                tgt = torch.tensor([(bits >> ((i + 1) % T)) & 1 for i in range(T)], dtype=torch.int32)
+                for root in range(-1, T):
+                    got = hta.hta_accept_greedy(p, draft, tgt, root=root, context_argmax=1)
+                    want = oracle.accept_greedy(par, draft, tgt, root=root, context_argmax=1)
+                    assert got == (want[0], want[1])
+
+
+def test_shard_bounds_cover_sequence():
+    for N in (0, 1, 7, 65536, 131071):
+        for P in (1, 2, 3, 4, 8):
+            b = [hta.shard_bounds(N, P, r) for r in range(P)]
+            assert b[0][0] == 0 and b[-1][1] == N
+            assert all(b[i][1] == b[i + 1][0] for i in range(P - 1))
+            assert max(hi - lo for lo, hi in b) - min(hi - lo for lo, hi in b) <= 1
