@@ -107,6 +107,16 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def created_events(n):
+    """CUDA events that exist on the device (torch creates them lazily at the first record;
+    hta_forward_timed records them from C, so create them up front)."""
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    for e in evs:
+        e.record()
+    torch.cuda.synchronize()
+    return evs
+
+
 # ----------------------------------------------------------------------------- oracle timing
 
 def time_oracle(w, mask_np, budget_s=12.0):
@@ -270,8 +280,8 @@ def main():
         times = timed(lambda i: step(d_in), args.steps)
         # (2) dominant kernel (prefix pass) timed on its own launch stream with CUDA events
         if ws == 1:
-            pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in range(args.steps)]
+            ev = created_events(2 * args.steps)
+            pev = [(ev[2 * i], ev[2 * i + 1]) for i in range(args.steps)]
             timed(lambda i: step(d_in, events=pev[i]), args.steps)
             prefix_ms = statistics.mean(a.elapsed_time(b) for a, b in pev)
         else:
@@ -377,7 +387,7 @@ def bench_config(name, dev, flush, k=10):
                       dtype=torch.uint8, device=dev)
     ts, tp = [], []
     for i in range(k + 3):
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e = created_events(4)
         flush.fill_(i & 0xFF)
         e[0].record()
         hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask, o=o, lse_out=lse, ws=wsb)

@@ -17,6 +17,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhta.so")
+TRACE_LIB = os.path.join(PKG, "libhta_trace.so")   # diagnostics only (-DHTA_TRACE)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",
@@ -39,13 +40,14 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in deps())
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    if not force and not needs_build():
+def build(verbose: bool = False, force: bool = False, trace: bool = False) -> str:
+    lib = TRACE_LIB if trace else LIB
+    if not trace and not force and not needs_build():
         return LIB
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build_trace" if trace else "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
-    extra = ["-Xptxas", "-v"] if verbose else []
+    extra = (["-Xptxas", "-v"] if verbose else []) + (["-DHTA_TRACE"] if trace else [])
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
@@ -62,12 +64,11 @@ def build(verbose: bool = False, force: bool = False) -> str:
             failed = True
     if failed:
         raise RuntimeError("libhta build failed")
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-ldl", "-lpthread"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose="--verbose" in sys.argv, force=True)
-    print(LIB)
+    print(build(verbose="--verbose" in sys.argv, force=True, trace="--trace" in sys.argv))

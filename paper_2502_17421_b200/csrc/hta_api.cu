@@ -90,9 +90,8 @@ PrefixPlan make_plan(const Shape &sh, int num_sms) {
     pl.G = sh.G;
     pl.M = s.T * sh.G;
     if (s.dtype == HTA_BF16) {
-        // Two 128-row tiles per CTA when the rows fill them well, else one.
-        const int rem = pl.M % 256;
-        pl.nt = (pl.M > 128 && (rem == 0 || rem > 128)) ? 2 : 1;
+        // More than 128 rows per KV head: CTA pairs (cta_group::2, 256 rows per pair).
+        pl.nt = (pl.M > 128 && s.d == 128) ? 2 : 1;
         pl.n_mgroups = (pl.M + 128 * pl.nt - 1) / (128 * pl.nt);
         pl.units = s.B * s.H_kv * pl.n_mgroups;
     } else {
@@ -107,11 +106,12 @@ PrefixPlan make_plan(const Shape &sh, int num_sms) {
     } else if (s.dtype == HTA_BF16) {
         // Fewest waves per unit of work: minimise waves(S) / S with a 1%-per-split penalty
         // for the partials each split adds (wave quantisation over the SMs, 1 CTA per SM).
-        const int smax = std::max(1, std::min(pl.n_tiles, 4 * num_sms / pl.units + 1));
+        const int ctas = pl.units * pl.nt;  // CTAs per split (a pair is two CTAs, two SMs)
+        const int smax = std::max(1, std::min(pl.n_tiles, 4 * num_sms / ctas + 1));
         double best = 1e30;
         S = 1;
         for (int c = 1; c <= smax; ++c) {
-            const int waves = (pl.units * c + num_sms - 1) / num_sms;
+            const int waves = (ctas * c + num_sms - 1) / num_sms;
             const double cost = double(waves) / c * (1.0 + 0.01 * c);
             if (cost < best - 1e-12) {
                 best = cost;
@@ -150,15 +150,15 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// 4-D map over a [B, N, H_kv, d] (strided) bf16 cache: box = 64 x 1 x 128 x 1, 128B swizzle.
-hta_status_t make_kv_map(CUtensorMap *map, const void *base, const hta_shape_t &s) {
+// 4-D map over a [B, N, H_kv, d] (strided) bf16 cache: box = 64 x 1 x box_rows x 1, 128B swizzle.
+hta_status_t make_kv_map(CUtensorMap *map, const void *base, const hta_shape_t &s, int box_rows) {
     EncodeTiledFn enc = encode_fn();
     if (enc == nullptr) return HTA_ERR_CUDA;
     cuuint64_t dims[4] = {cuuint64_t(s.d), cuuint64_t(s.H_kv), cuuint64_t(std::max<int64_t>(s.N_max, 1)),
                           cuuint64_t(s.B)};
     cuuint64_t strides[3] = {cuuint64_t(s.kv_strides[2] * 2), cuuint64_t(s.kv_strides[1] * 2),
                              cuuint64_t(s.kv_strides[0] * 2)};
-    cuuint32_t box[4] = {64, 1, cuuint32_t(kBlockN), 1};
+    cuuint32_t box[4] = {64, 1, cuuint32_t(box_rows), 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -203,9 +203,10 @@ hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, co
     cudaError_t e;
     if (s.dtype == HTA_BF16) {
         CUtensorMap tk, tv;
-        hta_status_t r = make_kv_map(&tk, k, s);
+        // a CTA of a pair loads half of each K tile (64 keys) and half of each V tile (64 columns)
+        hta_status_t r = make_kv_map(&tk, k, s, pl.nt == 2 ? kBlockN / 2 : kBlockN);
         if (r != HTA_OK) return r;
-        r = make_kv_map(&tv, v, s);
+        r = make_kv_map(&tv, v, s, kBlockN);
         if (r != HTA_OK) return r;
         e = launch_prefix_tc(p, tk, tv, prefix_tc_smem_bytes(s.d, pl.nt), st);
     } else {

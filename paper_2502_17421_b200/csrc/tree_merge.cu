@@ -186,28 +186,26 @@ __global__ void __launch_bounds__(128) tree_merge_kernel(const TreeMergeParams p
                 const int s = s0 + lane;
                 const float ws = s < p.n_parts ? expf(p.lse_parts[s * p.lse_part_stride + lrow] - mx) : 0.f;
                 const int cnt = min(32, p.n_parts - s0);
-                int u = 0;
-                for (; u + 4 <= cnt; u += 4) {
-                    float w4[4], v4[4][E];
+                // eight partial rows in flight per lane (the partials are L2-resident)
+                for (int u = 0; u < cnt; u += 8) {
+                    float w8[8], v8[8][E];
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        w4[k] = __shfl_sync(0xffffffffu, ws, u + k);
-                        VecIO<float, E>::load(p.o_parts + (s0 + u + k) * p.o_part_stride + orow, v4[k]);
+                    for (int k = 0; k < 8; ++k) {
+                        w8[k] = __shfl_sync(0xffffffffu, ws, (u + k) & 31);
+                        if (u + k < cnt) {
+                            VecIO<float, E>::load(p.o_parts + (s0 + u + k) * p.o_part_stride + orow, v8[k]);
+                        } else {
+                            w8[k] = 0.f;
+#pragma unroll
+                            for (int e = 0; e < E; ++e) v8[k][e] = 0.f;
+                        }
                     }
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        W += w4[k];
+                    for (int k = 0; k < 8; ++k) {
+                        W += w8[k];
 #pragma unroll
-                        for (int e = 0; e < E; ++e) acc[e] = fmaf(w4[k], v4[k][e], acc[e]);
+                        for (int e = 0; e < E; ++e) acc[e] = fmaf(w8[k], v8[k][e], acc[e]);
                     }
-                }
-                for (; u < cnt; ++u) {
-                    const float w = __shfl_sync(0xffffffffu, ws, u);
-                    float v[E];
-                    VecIO<float, E>::load(p.o_parts + (s0 + u) * p.o_part_stride + orow, v);
-                    W += w;
-#pragma unroll
-                    for (int e = 0; e < E; ++e) acc[e] = fmaf(w, v[e], acc[e]);
                 }
             }
             const float inv = 1.0f / W;

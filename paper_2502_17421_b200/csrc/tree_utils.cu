@@ -3,11 +3,12 @@
 // Mask (reading Z4): mask[i][j] = 1 iff j == i or j is an ancestor of i.
 //   Host: bit-parallel rows, row(i) = row(parent(i)) | bit(i) in index order (parents[i] < i).
 //   Device: one thread per node walks its parent chain (depth <= T <= 256).
-// Accepted path (reading Z12): forward pass marks accepted nodes
+// Accepted path (reading Z12).  Host: forward pass marks accepted nodes
 //   (acc[v] = acc[parent] && draft[v] == target_argmax[parent]), a reverse pass computes the
 //   longest accepted continuation below every node, and the walk from the root takes, at
-//   each level, the smallest-index child that still reaches the maximal length.  That is the
-//   lexicographically smallest among the longest accepted paths.
+//   each level, the smallest-index child that still reaches the maximal length -- the
+//   lexicographically smallest among the longest accepted paths.  Device: the same result
+//   computed by a block of T threads (see accept_kernel).
 #include <cstring>
 
 #include "hta_internal.h"
@@ -30,29 +31,42 @@ int host_build_mask(const int32_t *parents, int T, uint8_t *mask) {
     return 0;
 }
 
-__global__ void build_mask_kernel(const int32_t *__restrict__ parents, int T, uint8_t *__restrict__ mask) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) build_mask_kernel(const int32_t *__restrict__ parents, int T,
+                                                         uint8_t *__restrict__ mask) {
+    __shared__ int32_t par[256];
+    const int i = threadIdx.x;
+    if (i < T) par[i] = parents[i];  // one coalesced load; the chain walks below hit smem
+    __syncthreads();
     if (i >= T) return;
-    uint8_t *row = mask + static_cast<int64_t>(i) * T;
-    for (int j = 0; j < T; ++j) row[j] = 0;
+    uint32_t bits[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
     bool ok = true;
     int a = i;
     while (a >= 0) {  // parent indices strictly decrease, so this terminates
-        row[a] = 1;
-        const int pa = parents[a];
+        bits[a >> 5] |= 1u << (a & 31);
+        const int pa = par[a];
         if (pa < -1 || pa >= a) {
             ok = false;
             break;
         }
         a = pa;
     }
+    uint8_t *row = mask + static_cast<int64_t>(i) * T;
     if (!ok)
-        for (int j = 0; j < T; ++j) row[j] = 0;
+        for (int w = 0; w < 8; ++w) bits[w] = 0u;
+    if ((T & 3) == 0) {  // rows are 4-byte aligned: store 4 mask bytes at a time
+        for (int j = 0; j < T; j += 4) {
+            const uint32_t nib = (bits[j >> 5] >> (j & 31)) & 0xFu;
+            const uint32_t word = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+            *reinterpret_cast<uint32_t *>(row + j) = word;
+        }
+    } else {
+        for (int j = 0; j < T; ++j) row[j] = static_cast<uint8_t>((bits[j >> 5] >> (j & 31)) & 1u);
+    }
 }
 
 cudaError_t launch_build_mask(const int32_t *parents, int T, uint8_t *mask, cudaStream_t s) {
-    if (T <= 0) return cudaSuccess;
-    build_mask_kernel<<<(T + 127) / 128, 128, 0, s>>>(parents, T, mask);
+    if (T <= 0 || T > 256) return cudaErrorInvalidValue;
+    build_mask_kernel<<<1, 256, 0, s>>>(parents, T, mask);
     return cudaGetLastError();
 }
 
@@ -120,20 +134,128 @@ int host_accept(const int32_t *parents, const int32_t *draft, const int32_t *tgt
     return accept_impl(parents, draft, tgt, T, root, ctx, path, path_len, bonus, acc, height);
 }
 
-__global__ void accept_kernel(const int32_t *parents, const int32_t *draft, const int32_t *tgt, int T, int root,
-                              int ctx, int32_t *path, int32_t *path_len, int32_t *bonus) {
-    __shared__ uint8_t acc[256];
-    __shared__ int16_t height[256];
-    if (threadIdx.x != 0) return;
-    if (accept_impl(parents, draft, tgt, T, root, ctx, path, path_len, bonus, acc, height) != 0) {
-        *path_len = -1;
-        *bonus = -1;
+// Device version: one block, thread v = node v.  Pointer jumping over the parent chains gives,
+// for every node, whether its whole root path matches (AND of the per-node match bits) and its
+// depth, in ceil(log2 T) rounds; the maximal accepted depth is a block max; the nodes on some
+// maximal accepted path are marked by walking up from the maximal endpoints; the walk from
+// the root then takes the smallest marked child at each level (lexicographically smallest).
+__global__ void __launch_bounds__(256) accept_kernel(const int32_t *parents, const int32_t *draft,
+                                                     const int32_t *tgt, int T, int root, int ctx, int32_t *path,
+                                                     int32_t *path_len, int32_t *bonus) {
+    __shared__ int32_t par[256], tg[256], anc[256], dep[256];
+    __shared__ uint8_t ok[256], good[256];
+    __shared__ int s_err, s_L, s_next;
+    const int v = threadIdx.x;
+    const bool in = v < T;
+    if (v == 0) {
+        s_err = 0;
+        s_L = 0;
+    }
+    int pa = -1, dr = 0;
+    if (in) {
+        pa = parents[v];
+        dr = draft[v];
+        tg[v] = tgt[v];
+        par[v] = pa;
+    }
+    __syncthreads();
+    if (in && (pa < -1 || pa >= v)) atomicOr(&s_err, 1);
+    if (v == 0 && (root < -1 || root >= T)) atomicOr(&s_err, 1);
+    // match bit and first jump target of every node
+    int my_anc = -1, my_dep = 0;
+    uint8_t my_ok = 0;
+    if (in) {
+        my_dep = 1;
+        pa = (pa >= -1 && pa < v) ? pa : -1;  // invalid input is reported below; never index with it
+        if (root >= 0) {
+            my_ok = (v == root) ? 1 : (pa >= 0 && dr == tg[pa]);
+            my_anc = (v == root) ? -1 : pa;
+        } else {
+            my_ok = pa < 0 ? (dr == ctx) : (dr == tg[pa]);
+            my_anc = pa;
+        }
+        anc[v] = my_anc;
+        dep[v] = my_dep;
+        ok[v] = my_ok;
+    }
+    __syncthreads();
+    if (s_err) {
+        if (v == 0) {
+            *path_len = -1;
+            *bonus = -1;
+        }
+        return;
+    }
+    for (int round = 0; round < 8; ++round) {  // 2^8 = 256 >= any depth
+        int a2 = my_anc, d2 = my_dep;
+        uint8_t o2 = my_ok;
+        if (in && my_anc >= 0) {
+            o2 = my_ok & ok[my_anc];
+            d2 = my_dep + dep[my_anc];
+            a2 = anc[my_anc];
+        }
+        __syncthreads();
+        if (in) {
+            my_anc = a2;
+            my_dep = d2;
+            my_ok = o2;
+            anc[v] = a2;
+            dep[v] = d2;
+            ok[v] = o2;
+        }
+        __syncthreads();
+    }
+    // in root mode only root's subtree counts: every other chain ends at a top node with ok = 0
+    if (in && my_ok) atomicMax(&s_L, my_dep);
+    if (in) good[v] = 0;
+    __syncthreads();
+    const int L = s_L;
+    if (L == 0) {  // forest mode with no accepted depth-1 node
+        if (v == 0) {
+            *path_len = 0;
+            *bonus = ctx;
+        }
+        return;
+    }
+    if (in && my_ok && my_dep == L) {  // mark the nodes of every maximal accepted path
+        int a = v;
+        while (a >= 0 && (root < 0 || a != root)) {
+            good[a] = 1;
+            a = par[a];
+        }
+        if (root >= 0) good[root] = 1;
+    }
+    __syncthreads();
+    int cur;
+    if (root >= 0) {
+        cur = root;
+    } else {
+        if (v == 0) s_next = 0x7fffffff;
+        __syncthreads();
+        if (in && par[v] < 0 && good[v]) atomicMin(&s_next, v);
+        __syncthreads();
+        cur = s_next;
+    }
+    if (v == 0) path[0] = cur;
+    for (int len = 1; len < L; ++len) {
+        __syncthreads();
+        if (v == 0) s_next = 0x7fffffff;
+        __syncthreads();
+        if (in && par[v] == cur && good[v]) atomicMin(&s_next, v);
+        __syncthreads();
+        cur = s_next;
+        if (v == 0) path[len] = cur;
+    }
+    if (v == 0) {
+        *path_len = L;
+        *bonus = tg[cur];
     }
 }
 
 cudaError_t launch_accept(const int32_t *parents, const int32_t *draft, const int32_t *tgt, int T, int root, int ctx,
                           int32_t *path, int32_t *path_len, int32_t *bonus, cudaStream_t s) {
-    accept_kernel<<<1, 32, 0, s>>>(parents, draft, tgt, T, root, ctx, path, path_len, bonus);
+    if (T < 1 || T > 256) return cudaErrorInvalidValue;
+    accept_kernel<<<1, 256, 0, s>>>(parents, draft, tgt, T, root, ctx, path, path_len, bonus);
     return cudaGetLastError();
 }
 

@@ -14,7 +14,7 @@ from typing import Optional, Tuple
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libhta.so")
+LIB_PATH = os.environ.get("HTA_LIB", os.path.join(_PKG, "libhta.so"))
 
 HTA_BF16, HTA_FP32 = 0, 1
 STATUS = {0: "HTA_OK", 1: "HTA_ERR_INVALID_ARGUMENT", 2: "HTA_ERR_UNSUPPORTED", 3: "HTA_ERR_INVALID_MASK",
