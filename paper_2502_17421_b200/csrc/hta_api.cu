@@ -104,15 +104,18 @@ PrefixPlan make_plan(const Shape &sh, int num_sms) {
     if (s.num_splits > 0) {
         S = s.num_splits;
     } else if (s.dtype == HTA_BF16) {
-        // Fewest waves per unit of work: minimise waves(S) / S with a 1%-per-split penalty
-        // for the partials each split adds (wave quantisation over the SMs, 1 CTA per SM).
+        // Shortest makespan: waves(S) x (tiles per split + a fixed per-CTA cost of ~3 tiles for
+        // prologue and epilogue), with a 1%-per-split penalty for the partials each split adds
+        // (wave quantisation over the SMs, 1 CTA per SM).  Measured on B200: LongChat-16k is
+        // faster as one wave of 4 splits than as two waves of 9 (tools/split_sweep.py).
         const int ctas = pl.units * pl.nt;  // CTAs per split (a pair is two CTAs, two SMs)
         const int smax = std::max(1, std::min(pl.n_tiles, 4 * num_sms / ctas + 1));
         double best = 1e30;
         S = 1;
         for (int c = 1; c <= smax; ++c) {
             const int waves = (ctas * c + num_sms - 1) / num_sms;
-            const double cost = double(waves) / c * (1.0 + 0.01 * c);
+            const int per = (pl.n_tiles + c - 1) / c;
+            const double cost = double(waves) * (per + 3) * (1.0 + 0.01 * c);
             if (cost < best - 1e-12) {
                 best = cost;
                 S = c;
@@ -166,6 +169,26 @@ hta_status_t make_kv_map(CUtensorMap *map, const void *base, const hta_shape_t &
     return r == CUDA_SUCCESS ? HTA_OK : HTA_ERR_INVALID_ARGUMENT;
 }
 
+// Q [B, T, H, d] viewed as 4-D (d, H, T, B): a box (64, G, 128/G, 1) at (kb*64, g*G, t0, b) is
+// exactly 128 rows r = (t - t0)*G + (h - g*G) of a row tile, 128 B each, in the K-major
+// SWIZZLE_128B layout the MMA reads; rows past M (t >= T) are zero-filled.  Needs G | 128 and
+// 16-byte row strides; otherwise the kernel stages Q with plain loads.
+bool make_q_map(CUtensorMap *map, const void *q, const hta_shape_t &s, int G) {
+    if (128 % G != 0) return false;
+    for (int i = 0; i < 3; ++i)
+        if ((s.q_strides[i] * 2) % 16 != 0) return false;
+    EncodeTiledFn enc = encode_fn();
+    if (enc == nullptr) return false;
+    cuuint64_t dims[4] = {cuuint64_t(s.d), cuuint64_t(s.H), cuuint64_t(s.T), cuuint64_t(s.B)};
+    cuuint64_t strides[3] = {cuuint64_t(s.q_strides[2] * 2), cuuint64_t(s.q_strides[1] * 2),
+                             cuuint64_t(s.q_strides[0] * 2)};
+    cuuint32_t box[4] = {64, cuuint32_t(G), cuuint32_t(128 / G), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(q), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Enqueue the prefix pass writing `splits` partials at (o_out, lse_out) with the given strides.
 hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, const void *k, const void *v,
                         const int32_t *seqlens, float *o_out, float *lse_out, int64_t o_split_stride,
@@ -208,7 +231,10 @@ hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, co
         if (r != HTA_OK) return r;
         r = make_kv_map(&tv, v, s, kBlockN);
         if (r != HTA_OK) return r;
-        e = launch_prefix_tc(p, tk, tv, prefix_tc_smem_bytes(s.d, pl.nt), st);
+        CUtensorMap tq;
+        std::memset(&tq, 0, sizeof(tq));
+        p.q_tma = make_q_map(&tq, q, s, sh.G) ? 1 : 0;
+        e = launch_prefix_tc(p, tq, tk, tv, prefix_tc_smem_bytes(s.d, pl.nt), st);
     } else {
         e = launch_prefix_simt(p, st);
     }

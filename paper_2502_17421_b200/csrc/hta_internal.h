@@ -35,6 +35,7 @@ struct PrefixParams {
     float scale;                      // softmax scale
     float scale_log2;                 // scale * log2(e)
     int nt, n_mgroups, splits, tiles_per_split;
+    int q_tma;                                  // Q rows of a tile come from tmap_q (G divides 128)
     float *o_out;                     // [S][B][T][H][d] fp32, normalised partials
     float *lse_out;                   // [S][B][H][T] natural-log LSE
     int64_t o_split_stride, lse_split_stride;  // elements between splits
@@ -66,8 +67,8 @@ struct TreeMergeParams {
 };
 
 // Launchers (return cudaGetLastError() of the launch).
-cudaError_t launch_prefix_tc(const PrefixParams &p, const CUtensorMap &tmap_k, const CUtensorMap &tmap_v,
-                             int smem_bytes, cudaStream_t s);
+cudaError_t launch_prefix_tc(const PrefixParams &p, const CUtensorMap &tmap_q, const CUtensorMap &tmap_k,
+                             const CUtensorMap &tmap_v, int smem_bytes, cudaStream_t s);
 int prefix_tc_smem_bytes(int d, int nt);
 cudaError_t launch_prefix_simt(const PrefixParams &p, cudaStream_t s);
 cudaError_t launch_tree_merge(const TreeMergeParams &p, int d, hta_dtype_t in_dtype, hta_dtype_t out_dtype,

@@ -17,18 +17,16 @@
 //    swizzle, the canonical UMMA layout) so K tiles can run ahead of V tiles; in a pair both
 //    CTAs' bytes are counted on the leader's barriers.
 //  * warp 1 of the leader CTA issues the MMAs from a non-blocking, warp-converged loop
-//    (elect.sync per instruction, descriptors advanced by constants): S = Q K^T into one of two
-//    TMEM buffers (fp32) as soon as a K tile and a buffer are free, and O_h += P_h V_h for each
-//    half h of the tile's keys (A = P read from TMEM, the "TS" form; B = V from smem, MN-major)
-//    as soon as that half's P and the V tile are ready.
-//  * warps 2-9: two independent softmax warpgroups; warpgroup h owns key columns
-//    [64h, 64h + 64) of every tile with its own running max / sum and its own accumulator O_h
-//    in TMEM, so the two never wait on each other and overlap each other's latency.  Per tile:
-//    tcgen05.ld of its 64 S values, row max, exp2 (3/8 of the pairs on the FMA pipe by
-//    polynomial, the rest on MUFU), row sum, P -> bf16 -> tcgen05.st over S.  O_h is rescaled in
-//    TMEM only when its running max grows by more than 2^8 (exact: the final normalisation
-//    uses the same, possibly stale, max).  The epilogue merges the two halves exactly (the
-//    log-sum-exp merge of PAPER.md:207-218 applied inside the row).
+//    (elect.sync per instruction, descriptors advanced by constants): S = Q K^T into one of three
+//    TMEM buffers (fp32) as soon as a K tile and a buffer are free, and O += P V with A = P read
+//    from TMEM (the "TS" form) and B = V from smem (MN-major) as soon as P and the V tile are ready.
+//  * warps 2-9 (softmax): the two warps that share a TMEM lane quarter own disjoint 16-row halves
+//    of it, and each row is shared by a pair of threads (lanes t and t+16) that each hold 64 of
+//    its 128 S values (tcgen05.ld .16x32bx2).  Per tile: row max (one shuffle between the pair),
+//    exp2 (3/8 of the pairs on the FMA pipe by polynomial, the rest on MUFU), row sum, P -> bf16
+//    -> tcgen05.st over S.  No two warps ever exchange data, so they drift freely and overlap
+//    each other's latency.  O is rescaled in TMEM only when the running max grows by more than
+//    2^8 (exact: the final normalisation uses the same, possibly stale, max).
 //  * the epilogue divides O by the row sum and writes fp32 partials + natural-log LSE.
 // A split with no visible key writes the sentinel (O = 0, LSE = -inf).
 #include <cuda_bf16.h>
@@ -44,25 +42,56 @@ namespace hta {
 #ifdef HTA_TRACE
 __device__ unsigned long long *g_trace = nullptr;
 __device__ int g_trace_cta = 0;
+__device__ unsigned long long g_cta_times[1024][4];  // per CTA: entry ns, loop start ns/clk, exit ns, exit clk
+constexpr int kTraceRecs = 200;  // per warp, in shared memory (flushed to g_trace at the end)
 #define HTA_TR(ev, tag, jj)                                                                              \
     do {                                                                                                 \
-        if (g_trace != nullptr && blockIdx.x == g_trace_cta && lane == 0 && tr_n < 2048)                \
-            g_trace[warp * 2048 + tr_n++] = (static_cast<unsigned long long>(ev) << 56) |                \
-                                            (static_cast<unsigned long long>(tag) << 52) |               \
-                                            (static_cast<unsigned long long>((jj) & 0xFFFFF) << 32) |    \
-                                            static_cast<unsigned long long>(static_cast<uint32_t>(clock64())); \
+        if (lane == 0 && tr_n < kTraceRecs)                                                              \
+            tr_buf[warp * kTraceRecs + tr_n++] = (static_cast<unsigned long long>(ev) << 56) |            \
+                                                 (static_cast<unsigned long long>(tag) << 52) |           \
+                                                 (static_cast<unsigned long long>((jj) & 0xFFFFF) << 32) |\
+                                                 static_cast<unsigned long long>(static_cast<uint32_t>(clock64())); \
+    } while (0)
+__device__ __forceinline__ uint64_t trace_globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// clock and wall time (ns) side by side: the SM clock the kernel actually ran at
+#define HTA_TR_CLK(ev)                                                                                   \
+    do {                                                                                                 \
+        const uint32_t c_ = static_cast<uint32_t>(clock64());                                            \
+        const uint32_t t_ = static_cast<uint32_t>(trace_globaltimer());                                  \
+        if (lane == 0 && tr_n + 1 < kTraceRecs) {                                                        \
+            tr_buf[warp * kTraceRecs + tr_n++] = (static_cast<unsigned long long>(ev) << 56) | c_;       \
+            tr_buf[warp * kTraceRecs + tr_n++] = (static_cast<unsigned long long>(ev + 1) << 56) | t_;   \
+        }                                                                                                \
     } while (0)
 #else
 #define HTA_TR(ev, tag, jj) do { } while (0)
+#define HTA_TR_CLK(ev) do { } while (0)
 #endif
 
 // Diagnostics only (tools/): HTA_SKIP=1 skips the softmax math, HTA_SKIP=2 also the MMAs,
 // leaving the TMA stream and the barrier protocol; HTA_SKIP=3 runs the MMAs with no TMA traffic
 // (operands are whatever sits in smem) and no softmax; HTA_SKIP=4 = 3 with the softmax.
 // Product builds use 0.
+// Ping-pong of the two softmax warps sharing an SM sub-partition (see the softmax loop).
+#ifndef HTA_PINGPONG
+#define HTA_PINGPONG 0
+#endif
+// Publish P_j only after the load of S_{j+1} is issued (see the softmax loop).
+#ifndef HTA_DEFER
+#define HTA_DEFER 1
+#endif
 #ifndef HTA_SKIP
 #define HTA_SKIP 0
 #endif
+
+#ifndef HTA_KV_POLICY
+#define HTA_KV_POLICY kPolicyEvictFirst
+#endif
+constexpr uint64_t kKvPolicy = HTA_KV_POLICY;  // L2 policy of the streamed K/V tiles (read once)
 
 template <int D, bool PAIR>
 struct TcCfg {
@@ -74,49 +103,66 @@ struct TcCfg {
     static constexpr int kVCols = PAIR ? D / 2 : D;             // head-dim columns of a V tile held here
     static constexpr int kKBytes = kKRows * D * 2;
     static constexpr int kVBytes = kBlockN * kVCols * 2;
+#ifdef HTA_TRACE
+    static constexpr int kRingBytes = 176 * 1024;  // 16 KiB of smem hold the trace records
+#else
     static constexpr int kRingBytes = 192 * 1024;
+#endif
+#ifdef HTA_KRING_PCT  // diagnostics: share of the ring given to K tiles (percent)
+    static constexpr int kSlotsK = (kRingBytes * HTA_KRING_PCT / 100) / kKBytes;
+    static constexpr int kSlotsV = (kRingBytes - kSlotsK * kKBytes) / kVBytes;
+#else
     static constexpr int kSlotsK = (kRingBytes / 2) / kKBytes;
     static constexpr int kSlotsV = (kRingBytes / 2) / kVBytes;
-    static constexpr int kSBufs = 2;                            // S/P buffers in TMEM
+#endif
+    static constexpr int kSBufs = 3;                            // S/P buffers in TMEM
     static constexpr int kSoftmaxWarps = 8;                     // two warpgroups
     static constexpr int kThreads = 64 + 32 * kSoftmaxWarps;    // warp 0 TMA, warp 1 MMA + TMEM
     static constexpr int kVOff = kQBytes + kSlotsK * kKBytes;   // start of the V ring
-    static constexpr int kRedOff = kVOff + kSlotsV * kVBytes;   // row-max / row-sum exchange
-    static constexpr int kBarOff = kRedOff + 4 * kRowsPerTile * 4;  // (m, l) of both halves
+    static constexpr int kBarOff = kVOff + kSlotsV * kVBytes;
+#ifdef HTA_TRACE
+    static constexpr int kTraceOff = kBarOff + 512;
+    static constexpr int kSmemBytes = kTraceOff + 10 * 200 * 8;
+#else
     static constexpr int kSmemBytes = kBarOff + 512;  // base is 1024-aligned (__align__ below)
-    static_assert(kSlotsK >= 3 && kSlotsV >= 3, "need at least 3 slots per ring");
+#endif
+    static_assert(kSlotsK >= 2 && kSlotsV >= 2, "need at least 2 slots per ring");
     static_assert(kSmemBytes <= 232448, "shared memory budget");
 };
 
-// TMEM column map: S/P buffer b at 128*b (b = 0, 1), O_h (accumulator of key half h) at 256 + 128*h.
+// TMEM column map: S/P buffer b at 128*b (b = 0, 1, 2), O at 384.
 __device__ __forceinline__ uint32_t s_col(int buf) { return 128u * static_cast<uint32_t>(buf); }
-__device__ __forceinline__ uint32_t o_col(int half) { return 256u + 128u * static_cast<uint32_t>(half); }
+constexpr uint32_t kOCol = 384u;
 
 template <int D, bool PAIR>
 __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
-    prefix_tc_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
-                     const PrefixParams p) {
+    prefix_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
+                     const __grid_constant__ CUtensorMap tmap_v, const PrefixParams p) {
     using C = TcCfg<D, PAIR>;
     extern __shared__ __align__(1024) uint8_t smem[];  // 128B-swizzled tiles need 1024B alignment
     uint8_t *sQ = smem;
     uint8_t *sK = smem + C::kQBytes;
     uint8_t *sV = smem + C::kVOff;
-    float *red = reinterpret_cast<float *>(smem + C::kRedOff);   // epilogue (m, l) exchange [4][128]
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::kBarOff);
     uint64_t *k_full = bars;                       // [kSlotsK]  (the leader's copy is the one used)
     uint64_t *k_empty = k_full + C::kSlotsK;       // [kSlotsK]
     uint64_t *v_full = k_empty + C::kSlotsK;       // [kSlotsV]  (the leader's copy is the one used)
     uint64_t *v_empty = v_full + C::kSlotsV;       // [kSlotsV]
-    uint64_t *s_full = v_empty + C::kSlotsV;       // [2 bufs]
-    uint64_t *p_full = s_full + 2;                 // [2 halves][2 bufs] (the leader's copy is used)
-    uint64_t *pv_done = p_full + 4;                // [2 halves][2 bufs]: PV_h(j) -> pv_done[2h + j%2]
-    uint64_t *o_final = pv_done + 4;               // [1]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_final + 1);
+    uint64_t *s_full = v_empty + C::kSlotsV;       // [kSBufs]
+    uint64_t *p_full = s_full + C::kSBufs;         // [kSBufs]   (the leader's copy is the one used)
+    uint64_t *pv_done = p_full + C::kSBufs;        // [kSBufs]   PV_j arrives on pv_done[j % 3]
+    uint64_t *o_final = pv_done + C::kSBufs;       // [1]
+    uint64_t *q_full = o_final + 1;                // [1]       Q staged (the leader's copy is the one used)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_full + 1);
 
     const int warp = threadIdx.x >> 5;
+#ifdef HTA_TRACE
+    if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_times[blockIdx.x][0] = trace_globaltimer();
+#endif
     const int lane = threadIdx.x & 31;
 #ifdef HTA_TRACE
     int tr_n = 0;
+    unsigned long long *tr_buf = reinterpret_cast<unsigned long long *>(smem + C::kTraceOff);
 #endif
     const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
@@ -162,6 +208,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     // ---- one-time setup
     if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0u) __trap();  // swizzle atoms need 1 KiB alignment
     if (warp == 0 && lane == 0) {
+        if (p.q_tma) tma_prefetch_desc(&tmap_q);
         tma_prefetch_desc(&tmap_k);
         tma_prefetch_desc(&tmap_v);
     }
@@ -174,12 +221,13 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             mbar_init(&v_full[i], 1);
             mbar_init(&v_empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
-        for (int i = 0; i < 4; ++i) {
-            mbar_init(&p_full[i], (C::kSoftmaxWarps / 2) * (PAIR ? 2 : 1));
+        for (int i = 0; i < C::kSBufs; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], C::kSoftmaxWarps * (PAIR ? 2 : 1));
             mbar_init(&pv_done[i], 1);
         }
         mbar_init(o_final, 1);
+        mbar_init(q_full, p.q_tma ? 1 : C::kSoftmaxWarps * (PAIR ? 2 : 1));
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -191,83 +239,79 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             tmem_relinquish();
         }
     }
-    {   // this CTA's 128 Q rows -> smem in the canonical K-major SWIZZLE_128B layout
-        const __nv_bfloat16 *q = static_cast<const __nv_bfloat16 *>(p.q);
-        constexpr int kChunks = D / 8;  // 16-byte chunks per row
-        for (int idx = threadIdx.x; idx < kRowsPerTile * kChunks; idx += blockDim.x) {
-            const int r = idx / kChunks, ch = idx % kChunks;
-            const int grow = row0 + r;
-            uint4 val = make_uint4(0u, 0u, 0u, 0u);
-            if (grow < p.M) {
-                const int t = grow / p.G, h = g * p.G + grow % p.G;
-                val = *reinterpret_cast<const uint4 *>(q + b * p.qs0 + t * p.qs1 + h * p.qs2 + ch * 8);
-            }
-            uint8_t *dst = sQ + (ch / 8) * C::kRegionBytes + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
-            *reinterpret_cast<uint4 *>(dst) = val;
-        }
-    }
-    fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
     if (PAIR) cluster_sync();  // barrier inits and TMEM allocation visible to the peer
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    if (warp == 0) HTA_TR_CLK(50);
+#ifdef HTA_TRACE
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {
+        g_cta_times[blockIdx.x][1] = trace_globaltimer();
+        g_cta_times[blockIdx.x][2] = clock64();
+    }
+#endif
     if (warp == 0) {
-        // ================= TMA producer: K and V rings filled independently (K runs ahead)
+        // ================= TMA producer: K and V rings (K_j is consumed by S_j, V_j by PV_j)
+        if (lane == 0 && p.q_tma) {  // Q first: it gates S_0 and must not queue behind K/V
+            const int t0 = row0 / p.G;
+            if (PAIR) {
+                if (leader) mbar_arrive_expect_tx(q_full, 2u * C::kQBytes);
+                const uint32_t qfull0 = mapa_shared(smem_u32(q_full), 0);
+#pragma unroll
+                for (int kb = 0; kb < C::kKB; ++kb)
+                    tma_load_4d_pair(sQ + kb * C::kRegionBytes, &tmap_q, qfull0, kb * 64, g * p.G, t0, b,
+                                     kPolicyEvictNormal);  // re-read by every split
+            } else {
+                mbar_arrive_expect_tx(q_full, C::kQBytes);
+#pragma unroll
+                for (int kb = 0; kb < C::kKB; ++kb)
+                    tma_load_4d(sQ + kb * C::kRegionBytes, &tmap_q, q_full, kb * 64, g * p.G, t0, b,
+                                kPolicyEvictNormal);
+            }
+        }
         if (lane == 0 && HTA_SKIP < 3) {
             const uint32_t kfull0 = PAIR ? mapa_shared(smem_u32(&k_full[0]), 0) : 0u;
             const uint32_t vfull0 = PAIR ? mapa_shared(smem_u32(&v_full[0]), 0) : 0u;
-            int kj = 0, vj = 0;
-            uint32_t idle = 0;
-            while (kj < n_tiles || vj < n_tiles) {
-                bool did = false;
-                if (kj < n_tiles && mbar_test(&k_empty[kj % C::kSlotsK], ((kj / C::kSlotsK) & 1) ^ 1u)) {
-                    const int slot = kj % C::kSlotsK;
-                    const int n0 = static_cast<int>(key_lo) + kj * kBlockN;
+            // fixed order K_j, V_j with hardware-suspended waits for free slots (no polling)
+            for (int j = 0; j < n_tiles; ++j) {
+                const int n0 = static_cast<int>(key_lo) + j * kBlockN;
+                {
+                    const int slot = j % C::kSlotsK;
+                    mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);
                     uint8_t *dst = sK + slot * C::kKBytes;
-                    HTA_TR(30, 0, kj);
+                    HTA_TR(30, 0, j);
                     if (PAIR) {
                         if (leader) mbar_arrive_expect_tx(&k_full[slot], 2u * C::kKBytes);
 #pragma unroll
                         for (int kb = 0; kb < C::kKB; ++kb)
                             tma_load_4d_pair(dst + kb * (C::kKRows * 128), &tmap_k, kfull0 + 8u * slot, kb * 64, g,
-                                             n0 + static_cast<int>(rank) * C::kKRows, b, kPolicyEvictFirst);
+                                             n0 + static_cast<int>(rank) * C::kKRows, b, kKvPolicy);
                     } else {
                         mbar_arrive_expect_tx(&k_full[slot], C::kKBytes);
 #pragma unroll
                         for (int kb = 0; kb < C::kKB; ++kb)
                             tma_load_4d(dst + kb * (kBlockN * 128), &tmap_k, &k_full[slot], kb * 64, g, n0, b,
-                                        kPolicyEvictFirst);
+                                        kKvPolicy);
                     }
-                    ++kj;
-                    did = true;
                 }
-                if (vj < kj && mbar_test(&v_empty[vj % C::kSlotsV], ((vj / C::kSlotsV) & 1) ^ 1u)) {
-                    const int slot = vj % C::kSlotsV;
-                    const int n0 = static_cast<int>(key_lo) + vj * kBlockN;
+                {
+                    const int slot = j % C::kSlotsV;
+                    mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
                     uint8_t *dst = sV + slot * C::kVBytes;
-                    HTA_TR(31, 0, vj);
+                    HTA_TR(31, 0, j);
                     if (PAIR) {
                         if (leader) mbar_arrive_expect_tx(&v_full[slot], 2u * C::kVBytes);
                         tma_load_4d_pair(dst, &tmap_v, vfull0 + 8u * slot, static_cast<int>(rank) * 64, g, n0, b,
-                                         kPolicyEvictFirst);
+                                         kKvPolicy);
                     } else {
                         mbar_arrive_expect_tx(&v_full[slot], C::kVBytes);
 #pragma unroll
                         for (int kb = 0; kb < C::kKB; ++kb)
                             tma_load_4d(dst + kb * (kBlockN * 128), &tmap_v, &v_full[slot], kb * 64, g, n0, b,
-                                        kPolicyEvictFirst);
+                                        kKvPolicy);
                     }
-                    ++vj;
-                    did = true;
-                }
-                if (!did) {
-                    if (++idle > (1u << 26)) {
-                        printf("hta: producer stalled (block %d)\n", blockIdx.x);
-                        __trap();
-                    }
-                    __nanosleep(20);
                 }
             }
         }
@@ -284,11 +328,15 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             const uint64_t qd0 = sdesc_sw128(smem_u32(sQ), 16, 1024);
             const uint64_t kd0 = sdesc_sw128(smem_u32(sK), 16, 1024);
             const uint64_t vd0 = sdesc_sw128(smem_u32(sV), kBlockN * 128, 1024);
+            // One elected lane issues each group of MMAs; the descriptors are warp-uniform values
+            // computed outside the elected branch, so ptxas keeps them in uniform registers and
+            // each tcgen05.mma costs a few instructions (issue must stay well under 64 cycles per
+            // N=128 MMA, and this warp shares its sub-partition with two softmax warps).
             auto commit = [](uint64_t *bar) {
                 if (PAIR)
-                    tc_commit2_mc_elect(bar);
+                    tc_commit2_mc(bar);
                 else
-                    tc_commit_elect(bar);
+                    tc_commit(bar);
             };
             auto issue_S = [&](int buf, int slot) {
                 if (HTA_SKIP == 1 || HTA_SKIP == 2) return;
@@ -300,108 +348,190 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     const uint32_t qo = ((k / 4) * C::kRegionBytes + (k % 4) * 32) >> 4;
                     const uint32_t ko = ((k / 4) * (C::kKRows * 128) + (k % 4) * 32) >> 4;
                     if (PAIR)
-                        mma2_bf16_ss_elect(d_t, qd0 + qo, kd + ko, idesc_qk, k > 0 ? 1u : 0u);
+                        mma2_bf16_ss(d_t, qd0 + qo, kd + ko, idesc_qk, k > 0 ? 1u : 0u);
                     else
-                        mma_bf16_ss_elect(d_t, qd0 + qo, kd + ko, idesc_qk, k > 0 ? 1u : 0u);
+                        mma_bf16_ss(d_t, qd0 + qo, kd + ko, idesc_qk, k > 0 ? 1u : 0u);
                 }
             };
-            // O_h += P_h V_h over the 64 keys [64h, 64h + 64) of the tile (K steps 4h .. 4h+3);
-            // P_h sits packed in TMEM columns [64h, 64h + 32) of the S buffer
-            auto issue_PV = [&](int half, int buf, int slot, bool acc) {
+            auto issue_PV = [&](int buf, int slot, bool acc) {
                 if (HTA_SKIP == 1 || HTA_SKIP == 2) return;
-                const uint32_t a_t = tmem + s_col(buf) + 64u * half;
+                const uint32_t a_t = tmem + s_col(buf);
                 const uint64_t vd = vd0 + static_cast<uint32_t>((slot * C::kVBytes) >> 4);
 #pragma unroll
-                for (int kk = 0; kk < kBlockN / 32; ++kk) {
-                    const int k = half * (kBlockN / 32) + kk;
+                for (int k = 0; k < kBlockN / 16; ++k) {
                     // MN-major SW128: 16 keys = two 8-row groups = +2048 B per K step
                     if (PAIR)
-                        mma2_bf16_ts_elect(tmem + o_col(half), a_t + kk * 8, vd + static_cast<uint32_t>(k * 128),
-                                           idesc_pv, (acc || kk > 0) ? 1u : 0u);
+                        mma2_bf16_ts(tmem + kOCol, a_t + k * 8, vd + static_cast<uint32_t>(k * 128), idesc_pv,
+                                     (acc || k > 0) ? 1u : 0u);
                     else
-                        mma_bf16_ts_elect(tmem + o_col(half), a_t + kk * 8, vd + static_cast<uint32_t>(k * 128),
-                                          idesc_pv, (acc || kk > 0) ? 1u : 0u);
+                        mma_bf16_ts(tmem + kOCol, a_t + k * 8, vd + static_cast<uint32_t>(k * 128), idesc_pv,
+                                    (acc || k > 0) ? 1u : 0u);
                 }
             };
-            // warp-uniform probe (lane 0's view is broadcast)
-            auto ready = [](uint64_t *bar, uint32_t parity) {
-                return __shfl_sync(0xffffffffu, mbar_test(bar, parity) ? 1 : 0, 0) != 0;
-            };
+            const bool issuer = elect_one() != 0;
+            // Fixed order with hardware-suspended waits (no polling: a spinning issuer would take
+            // issue slots from the softmax warps sharing its SM sub-partition):
+            //   S_0, S_1, S_2, then for every j: PV_j (needs V_j and P_j), S_{j+3} (needs K_{j+3};
+            //   its buffer was last read by PV_j, issued just before).
             constexpr bool kNoMem = HTA_SKIP >= 3;
-            int ns = 0, np[2] = {0, 0};  // next S, next PV per key half
-            uint32_t idle = 0;
-            while (np[0] < n_tiles || np[1] < n_tiles) {
-                bool did = false;
-                // S_ns into buffer ns % 2 once its K tile landed and both PV halves of tile ns-2
-                // (the last readers of that buffer) have been issued.  The tail tile the softmax
-                // warps sanitise also needs its V tile in smem before they see S.
-                if (ns < n_tiles && ns < min(np[0], np[1]) + 2 &&
-                    (kNoMem || ready(&k_full[ns % C::kSlotsK], (ns / C::kSlotsK) & 1)) &&
-                    (kNoMem || !(tail_zero && ns == n_tiles - 1) ||
-                     ready(&v_full[ns % C::kSlotsV], (ns / C::kSlotsV) & 1))) {
-                    tc_fence_after();
-                    issue_S(ns & 1, ns % C::kSlotsK);
-                    commit(&s_full[ns & 1]);
-                    commit(&k_empty[ns % C::kSlotsK]);
-                    HTA_TR(21, 0, ns);
-                    ++ns;
-                    did = true;
+            auto wait_all = [](uint64_t *bar, uint32_t parity) {
+                mbar_wait(bar, parity);
+                __syncwarp();
+            };
+            auto start_S = [&](int jj) {
+                if (!kNoMem) {
+                    wait_all(&k_full[jj % C::kSlotsK], (jj / C::kSlotsK) & 1);
+                    if (tail_zero && jj == n_tiles - 1)  // the softmax warps sanitise V of this tile
+                        wait_all(&v_full[jj % C::kSlotsV], (jj / C::kSlotsV) & 1);
                 }
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int j = np[h];
-                    if (j < ns && (kNoMem || ready(&v_full[j % C::kSlotsV], (j / C::kSlotsV) & 1)) &&
-                        ready(&p_full[2 * h + (j & 1)], (j >> 1) & 1)) {
-                        HTA_TR(1, h, j);
-                        tc_fence_after();
-                        issue_PV(h, j & 1, j % C::kSlotsV, j > 0);
-                        commit(&pv_done[2 * h + (j & 1)]);
-                        if (np[1 - h] > j) commit(&v_empty[j % C::kSlotsV]);  // both halves read V_j
-                        ++np[h];
-                        did = true;
-                    }
+                tc_fence_after();
+                if (issuer) {
+                    issue_S(jj % C::kSBufs, jj % C::kSlotsK);
+                    commit(&s_full[jj % C::kSBufs]);
+                    commit(&k_empty[jj % C::kSlotsK]);
                 }
-                if (did) {
-                    idle = 0;
-                } else if (++idle > (1u << 26)) {
-                    if (lane == 0) printf("hta: MMA issuer stalled (block %d)\n", blockIdx.x);
-                    __trap();
+                __syncwarp();
+                HTA_TR(21, 0, jj);
+            };
+            if (PAIR && !p.q_tma)
+                mbar_wait_cluster(q_full, 0);  // staged by both CTAs' threads (generic proxy)
+            else
+                mbar_wait(q_full, 0);
+            __syncwarp();
+            HTA_TR(22, 0, 0);
+            for (int jj = 0; jj < C::kSBufs && jj < n_tiles; ++jj) start_S(jj);
+            for (int j = 0; j < n_tiles; ++j) {
+                if (!kNoMem) wait_all(&v_full[j % C::kSlotsV], (j / C::kSlotsV) & 1);
+                wait_all(&p_full[j % C::kSBufs], (j / C::kSBufs) & 1);
+                HTA_TR(1, 0, j);
+                tc_fence_after();
+                if (issuer) {
+                    issue_PV(j % C::kSBufs, j % C::kSlotsV, j > 0);
+                    commit(&pv_done[j % C::kSBufs]);
+                    commit(&v_empty[j % C::kSlotsV]);
                 }
+                __syncwarp();
+                if (j + C::kSBufs < n_tiles) start_S(j + C::kSBufs);
             }
-            commit(o_final);
+            if (issuer) commit(o_final);
         }
         __syncwarp();
     } else {
-        // ================= softmax warpgroup `half`: key columns [64*half, 64*half + 64) of every
-        // tile, its own running max / sum and its own accumulator O_half
-        const int half = (warp - 2) >> 2;
+        // ================= softmax: warp w owns rows 32*(w%4) + 16*rh .. +15 of the tile (rh =
+        // (w-2)/4); lane t holds row (t & 15) of them, key columns [64*(t>>4), 64*(t>>4) + 64)
+        if (!p.q_tma) {  // this CTA's 128 Q rows -> smem in the canonical K-major SWIZZLE_128B
+            // layout (G does not divide 128: no TMA box), staged by the softmax warps
+            const __nv_bfloat16 *q = static_cast<const __nv_bfloat16 *>(p.q);
+            constexpr int kQThreads = 32 * C::kSoftmaxWarps;
+            constexpr int kChunks = D / 8;  // 16-byte chunks per row
+            constexpr int kPer = (kRowsPerTile * kChunks + kQThreads - 1) / kQThreads;
+            const int qt = threadIdx.x - 64;
+            // all loads of a thread in flight at once (a load/store loop would serialise kPer cold
+            // HBM latencies)
+            uint4 val[kPer];
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+                const int idx = qt + i * kQThreads;
+                const int r = idx / kChunks, ch = idx % kChunks;
+                const int grow = row0 + r;
+                val[i] = make_uint4(0u, 0u, 0u, 0u);
+                if (idx < kRowsPerTile * kChunks && grow < p.M) {
+                    const int t = grow / p.G, h = g * p.G + grow % p.G;
+                    val[i] = __ldg(reinterpret_cast<const uint4 *>(q + b * p.qs0 + t * p.qs1 + h * p.qs2 + ch * 8));
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+                const int idx = qt + i * kQThreads;
+                const int r = idx / kChunks, ch = idx % kChunks;
+                if (idx < kRowsPerTile * kChunks)
+                    *reinterpret_cast<uint4 *>(sQ + (ch / 8) * C::kRegionBytes + r * 128 + (((ch & 7) ^ (r & 7)) << 4)) =
+                        val[i];
+            }
+            fence_proxy_async_smem();  // generic-proxy stores -> read by the tensor core
+            __syncwarp();
+            HTA_TR(14, warp - 2, 0);
+            if (lane == 0) {
+                if (PAIR)
+                    mbar_arrive_remote_release_cluster(mapa_shared(smem_u32(q_full), 0));
+                else
+                    mbar_arrive(q_full);
+            }
+        }
         const int quarter = warp & 3;
-        const int r = quarter * 32 + lane;
+        const int rh = (warp - 2) >> 2;
+        const int chalf = lane >> 4;
+        const int r = quarter * 32 + rh * 16 + (lane & 15);
         const int grow = row0 + r;
-        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32 + rh * 16) << 16;
         const float c = p.scale_log2;
         const uint32_t pfull0 = PAIR ? mapa_shared(smem_u32(&p_full[0]), 0) : 0u;
         constexpr int kHalfCols = kBlockN / 2;
-        float m_run = -INFINITY, l_run = 0.f;
+        float m_run = -INFINITY, l_run = 0.f;  // l_run: this thread's 64 columns only
+        // Ping-pong: warps w and w+4 share a sub-partition (same TMEM lane quarter) and would
+        // otherwise run every tile in phase -- both in the issue-bound exponential loop at once,
+        // both idle in the latency-bound TMEM load / store / barrier phases.  Named barriers
+        // make their exponential loops alternate (rh 0 on tile j, rh 1 on tile j, rh 0 on j+1,
+        // ...), so each warp's latency phases overlap its partner's arithmetic.
+        constexpr bool kPingPong = HTA_PINGPONG != 0 && (HTA_SKIP < 1 || HTA_SKIP == 4);
+        const uint32_t bar_mine = 1u + static_cast<uint32_t>(quarter + 4 * rh);
+        const uint32_t bar_partner = 1u + static_cast<uint32_t>(quarter + 4 * (1 - rh));
+        if (kPingPong && rh == 1) named_bar_arrive(bar_partner, 64);  // rh 0 goes first
+        // Publish P_jp (stored to TMEM without waiting): wait for the stores (and any O rescale
+        // of that tile), sanitise the garbage V rows of the last tile, signal the MMA warp.
+        auto publish = [&](int jp) {
+            tmem_st_wait();
+            if (jp == n_tiles - 1 && tail_zero) {
+                // V rows (keys) past the sequence end: zero this CTA's part of key row r (may be
+                // NaN); the thread pair of row r splits the row's 16-byte chunks
+                if (r >= tail_valid) {
+                    uint8_t *vrow = sV + ((n_tiles - 1) % C::kSlotsV) * C::kVBytes + r * 128;
+                    constexpr int kChunks16 = C::kVCols * 2 / 16;  // 16-byte chunks in this CTA's row
+#pragma unroll
+                    for (int cch = chalf * (kChunks16 / 2); cch < (chalf + 1) * (kChunks16 / 2); ++cch)
+                        *reinterpret_cast<uint4 *>(vrow + (cch / 8) * (kBlockN * 128) + (cch % 8) * 16) =
+                            make_uint4(0u, 0u, 0u, 0u);
+                }
+                fence_proxy_async_smem();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                const int pb = jp % C::kSBufs;
+                if (!PAIR)
+                    mbar_arrive(&p_full[pb]);
+                else if (jp == n_tiles - 1 && tail_zero)
+                    mbar_arrive_remote_release_cluster(pfull0 + 8u * pb);  // publishes zeroed V rows
+                else
+                    mbar_arrive_remote(pfull0 + 8u * pb);
+            }
+            HTA_TR(13, warp - 2, jp);
+        };
+        // Deferred publication: P_{j-1} is published after the load of S_j is issued, so the
+        // store-completion wait overlaps the load latency instead of adding to each tile's
+        // critical path (the MMA warp has slack: 3 S buffers).
+        constexpr bool kDefer = HTA_DEFER != 0;
         for (int j = 0; j < n_tiles; ++j) {
-            const int buf = j & 1;
-            mbar_wait(&s_full[buf], static_cast<uint32_t>((j >> 1) & 1));
-            if (quarter == 0) HTA_TR(10, half, j);
+            const int buf = j % C::kSBufs;
+            mbar_wait(&s_full[buf], static_cast<uint32_t>((j / C::kSBufs) & 1));
+            if (warp == 2) HTA_TR(10, 0, j);
             tc_fence_after();
             const bool last = j == n_tiles - 1;
             float mt = 0.f, lsum = 0.f;
-            uint32_t pk[kHalfCols / 2];
             if (HTA_SKIP < 1 || HTA_SKIP == 4) {
                 float s[kHalfCols];
-                tmem_ld64(tmem + lane_off + s_col(buf) + half * kHalfCols, s);
+                tmem_ld_16x64_split64_nowait(tmem + lane_off + s_col(buf), s);
+                if (kDefer && j > 0) publish(j - 1);
+                tmem_ld_wait64(s);
                 if (last && tail_valid < kBlockN) {
                     // keys past the split end -> -inf (last tile only; the empty asm keeps this a
                     // real branch instead of per-element selects on every tile)
                     asm volatile("" ::: "memory");
 #pragma unroll
                     for (int cc = 0; cc < kHalfCols; ++cc)
-                        if (half * kHalfCols + cc >= tail_valid) s[cc] = -INFINITY;
+                        if (chalf * kHalfCols + cc >= tail_valid) s[cc] = -INFINITY;
                 }
+                if (kPingPong) named_bar_sync(bar_mine, 64);
                 float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
 #pragma unroll
                 for (int cc = 4; cc < kHalfCols; cc += 8) {
@@ -410,16 +540,21 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     mx2 = fmaxf(mx2, fmaxf(s[cc + 2], s[cc + 6]));
                     mx3 = fmaxf(mx3, fmaxf(s[cc + 3], s[cc + 7]));
                 }
-                mt = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * c;
-                if (quarter == 0) HTA_TR(11, half, j);
-                // a half with every key masked (tail) keeps its state: P = 0 below
+                float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));  // the other half of the row
+                mt = mx * c;
+                if (warp == 2) HTA_TR(11, 0, j);
                 const float m_new = (mt > m_run + 8.0f) ? mt : m_run;
-                const float m_use = m_new == -INFINITY ? 0.f : m_new;
                 // P = exp2(S*c - m) -> bf16 over S in TMEM.  3 of every 8 column pairs use the
                 // FMA-pipe polynomial, the rest MUFU ex2 (MUFU alone would co-limit the MMAs).
-                const float2 c2 = make_float2(c, c), neg2 = make_float2(-m_use, -m_use);
+                const float2 c2 = make_float2(c, c), neg2 = make_float2(-m_new, -m_new);
                 float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
                 const float2 *s2 = reinterpret_cast<const float2 *>(s);
+                uint32_t pk[kHalfCols / 2];
+                // P packed (2 bf16 per column): keys [64h, 64h+64) -> columns [32h, 32h+32).  Both
+                // halves of a row live in the same warp, whose S loads above already completed.
+                // Stored in two 16-column halves without waiting, so the first store overlaps the
+                // second half's exponentials; one wait::st before P is published.
 #pragma unroll
                 for (int i = 0; i < kHalfCols / 2; ++i) {
                     const float2 x = __ffma2_rn(s2[i], c2, neg2);
@@ -435,103 +570,78 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     else
                         acc0 = __fadd2_rn(acc0, pp);
                     pk[i] = pack_bf16x2(pp.x, pp.y);
+                    if (i == 15) tmem_st_16x16_split_nowait<32>(tmem + lane_off + s_col(buf), pk);
                 }
-                // P_half packed (bf16 x 2 per column) into the first 32 of this half's own 64 S
-                // columns: it never overwrites S values the other half may still be reading
-                tmem_st32(tmem + lane_off + s_col(buf) + half * kHalfCols, pk);
+                tmem_st_16x16_split_nowait<32>(tmem + lane_off + s_col(buf) + 16, pk + 16);
+                if (kPingPong && (rh == 0 || !last)) named_bar_arrive(bar_partner, 64);
                 lsum = (acc0.x + acc1.x) + (acc0.y + acc1.y);
                 mt = m_new;
             } else {
+                if (kDefer && j > 0) publish(j - 1);
                 mt = 0.f;
                 lsum = 1.f;
             }
-            if (quarter == 0) HTA_TR(12, half, j);
-            // Rescale O_half only when this half's running max moved.  O_half must then hold
-            // P_{j-1} V_{j-1} first: wait for PV_half(j-1) on pv_done[2*half + (j-1)%2].  That
-            // barrier cannot run two phases ahead (PV_half(j+1) needs P_half(j+1), not yet
-            // published), so the parity wait is exact although most tiles never wait.
-            const bool need = (j > 0) && (mt != m_run) && (m_run != -INFINITY);
+            if (warp == 2) HTA_TR(12, 0, j);
+            // Rescale O only when the running max moved.  O must then hold P_{j-1} V_{j-1} first:
+            // wait for PV_{j-1} on its own barrier pv_done[(j-1) % 3].  That barrier cannot run two
+            // phases ahead (PV_{j+2} needs P_{j+2}, not yet published), so the parity wait is exact
+            // although most tiles never wait.
+            const bool need = (j > 0) && (mt != m_run);
             const float f = need ? fast_exp2(m_run - mt) : 1.0f;
             l_run = l_run * f + lsum;
             if (__any_sync(0xffffffffu, need)) {
-                mbar_wait(&pv_done[2 * half + ((j - 1) & 1)], static_cast<uint32_t>(((j - 1) >> 1) & 1));
+                mbar_wait(&pv_done[(j - 1) % C::kSBufs], static_cast<uint32_t>(((j - 1) / C::kSBufs) & 1));
                 tc_fence_after();
-                if (quarter == 0) HTA_TR(14, half, j);
 #pragma unroll 1
-                for (int ch = 0; ch < D / 32; ++ch) {
+                for (int ch = 0; ch < D / 2; ch += 32) {  // this thread's D/2 columns of the O row
                     float o[32];
-                    tmem_ld32(tmem + lane_off + o_col(half) + ch * 32, o);
+                    tmem_ld_16x32_split<D / 2>(tmem + lane_off + kOCol + ch, o);
 #pragma unroll
                     for (int e = 0; e < 32; ++e) o[e] *= f;
-                    tmem_st32(tmem + lane_off + o_col(half) + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(o));
+                    tmem_st_16x32_split<D / 2>(tmem + lane_off + kOCol + ch, *reinterpret_cast<uint32_t(*)[32]>(o));
                 }
             }
             m_run = mt;
-            if (last && tail_zero) {
-                if (r >= tail_valid) {
-                    // V rows past the sequence end: zero this half of this CTA's row (may be NaN)
-                    uint8_t *vrow = sV + ((n_tiles - 1) % C::kSlotsV) * C::kVBytes + r * 128;
-                    constexpr int kChunks16 = C::kVCols * 2 / 16;  // 16-byte chunks in this CTA's row
-#pragma unroll
-                    for (int cch = half * (kChunks16 / 2); cch < (half + 1) * (kChunks16 / 2); ++cch)
-                        *reinterpret_cast<uint4 *>(vrow + (cch / 8) * (kBlockN * 128) + (cch % 8) * 16) =
-                            make_uint4(0u, 0u, 0u, 0u);
-                }
-                fence_proxy_async_smem();
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                const int pi = 2 * half + buf;
-                if (!PAIR)
-                    mbar_arrive(&p_full[pi]);
-                else if (last && tail_zero)
-                    mbar_arrive_remote_release_cluster(pfull0 + 8u * pi);  // publishes zeroed V rows
-                else
-                    mbar_arrive_remote(pfull0 + 8u * pi);
-            }
-            if (quarter == 0) HTA_TR(13, half, j);
+            if (!kDefer) publish(j);
         }
-        // ---- epilogue: merge the two halves' (m, O_h, l) exactly; warpgroup h writes output
-        // columns [D/2 * h, D/2 * h + D/2)
-        red[half * kRowsPerTile + r] = m_run;
-        red[(2 + half) * kRowsPerTile + r] = l_run;
+        if (kDefer && n_tiles > 0) publish(n_tiles - 1);
+        // ---- epilogue: the thread pair of a row adds its two partial row sums
         mbar_wait(o_final, 0);
-        named_bar_sync(1, 32 * C::kSoftmaxWarps);
         tc_fence_after();
         pdl_launch_dependents();
-        const float m0 = red[r], m1 = red[kRowsPerTile + r];
-        const float l0 = red[2 * kRowsPerTile + r], l1 = red[3 * kRowsPerTile + r];
-        const float mm = fmaxf(m0, m1);
-        const float w0 = m0 == -INFINITY ? 0.f : fast_exp2(m0 - mm);
-        const float w1 = m1 == -INFINITY ? 0.f : fast_exp2(m1 - mm);
-        const float l_tot = l0 * w0 + l1 * w1;
+        const float l_tot = l_run + __shfl_xor_sync(0xffffffffu, l_run, 16);
         const float inv = 1.0f / l_tot;
-        const float a0 = w0 * inv, a1 = w1 * inv;
         const bool row_ok = grow < p.M;
         int t = 0, h = 0;
         if (row_ok) {
             t = grow / p.G;
             h = g * p.G + grow % p.G;
         }
-        float4 *dst = reinterpret_cast<float4 *>(o_base + ((static_cast<int64_t>(b) * p.T + t) * p.H + h) * D);
+        float *dst = o_base + ((static_cast<int64_t>(b) * p.T + t) * p.H + h) * D + chalf * (D / 2);
 #pragma unroll
-        for (int ch = half * (D / 64); ch < (half + 1) * (D / 64); ++ch) {
-            float x0[32], x1[32];
-            tmem_ld32(tmem + lane_off + o_col(0) + ch * 32, x0);
-            tmem_ld32(tmem + lane_off + o_col(1) + ch * 32, x1);
+        for (int ch = 0; ch < D / 2; ch += 32) {
+            float o[32];
+            tmem_ld_16x32_split<D / 2>(tmem + lane_off + kOCol + ch, o);
             if (row_ok) {
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
-                    dst[ch * 8 + e] = make_float4(x0[4 * e] * a0 + x1[4 * e] * a1, x0[4 * e + 1] * a0 + x1[4 * e + 1] * a1,
-                                                  x0[4 * e + 2] * a0 + x1[4 * e + 2] * a1,
-                                                  x0[4 * e + 3] * a0 + x1[4 * e + 3] * a1);
+                    reinterpret_cast<float4 *>(dst + ch)[e] =
+                        make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
             }
         }
-        if (row_ok && half == 0)
-            lse_base[(static_cast<int64_t>(b) * p.H + h) * p.T + t] = (mm + log2f(l_tot)) * 0.69314718055994530942f;
+        if (row_ok && chalf == 0)
+            lse_base[(static_cast<int64_t>(b) * p.H + h) * p.T + t] = (m_run + log2f(l_tot)) * 0.69314718055994530942f;
     }
 
+#ifdef HTA_TRACE
+    if (warp == 3) HTA_TR_CLK(52);
+    if (threadIdx.x == 96 && blockIdx.x < 1024) {
+        g_cta_times[blockIdx.x][3] = trace_globaltimer();
+        g_cta_times[blockIdx.x][2] = clock64() - g_cta_times[blockIdx.x][2];
+    }
+    if (g_trace != nullptr && blockIdx.x == g_trace_cta && lane == 0)
+        for (int i = 0; i < tr_n; ++i) g_trace[warp * 2048 + i] = tr_buf[warp * kTraceRecs + i];
+#endif
     tc_fence_before();
     __syncthreads();
     if (PAIR) cluster_sync();  // no CTA of the pair leaves while the peer may still signal it
@@ -549,10 +659,14 @@ extern "C" __attribute__((visibility("default"))) int hta_debug_set_trace(void *
     if (cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf)) != cudaSuccess) return -1;
     return cudaMemcpyToSymbol(g_trace_cta, &cta, sizeof(cta)) == cudaSuccess ? 0 : -1;
 }
+extern "C" __attribute__((visibility("default"))) int hta_debug_cta_times(void *host_out) {
+    return cudaMemcpyFromSymbol(host_out, g_cta_times, sizeof(g_cta_times)) == cudaSuccess ? 0 : -1;
+}
 #endif
 
 template <int D, bool PAIR>
-static cudaError_t launch_tc(const PrefixParams &p, const CUtensorMap &tk, const CUtensorMap &tv, cudaStream_t s) {
+static cudaError_t launch_tc(const PrefixParams &p, const CUtensorMap &tq, const CUtensorMap &tk, const CUtensorMap &tv,
+                             cudaStream_t s) {
     using C = TcCfg<D, PAIR>;
     auto kern = prefix_tc_kernel<D, PAIR>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
@@ -569,7 +683,7 @@ static cudaError_t launch_tc(const PrefixParams &p, const CUtensorMap &tk, const
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, tk, tv, p);
+    e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, p);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -579,9 +693,11 @@ int prefix_tc_smem_bytes(int d, int nt) {
     return TcCfg<64, false>::kSmemBytes;
 }
 
-cudaError_t launch_prefix_tc(const PrefixParams &p, const CUtensorMap &tk, const CUtensorMap &tv, int, cudaStream_t s) {
-    if (p.d == 128) return p.nt == 2 ? launch_tc<128, true>(p, tk, tv, s) : launch_tc<128, false>(p, tk, tv, s);
-    if (p.d == 64 && p.nt == 1) return launch_tc<64, false>(p, tk, tv, s);
+cudaError_t launch_prefix_tc(const PrefixParams &p, const CUtensorMap &tq, const CUtensorMap &tk, const CUtensorMap &tv,
+                             int, cudaStream_t s) {
+    if (p.d == 128)
+        return p.nt == 2 ? launch_tc<128, true>(p, tq, tk, tv, s) : launch_tc<128, false>(p, tq, tk, tv, s);
+    if (p.d == 64 && p.nt == 1) return launch_tc<64, false>(p, tq, tk, tv, s);
     return cudaErrorInvalidValue;
 }
 

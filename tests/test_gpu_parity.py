@@ -32,6 +32,8 @@ CASES = [
     (3, 5, 6, 3, 128, 300, "fp32", "V2", "random"),          # fp32 GQA
     (1, 1, 4, 4, 128, 1, "bf16", "V1", "chain"),             # single key, single node
     (2, 7, 4, 2, 64, 129, "fp32", "V0", "roots"),            # fp32 d=64, self-only tree
+    (1, 30, 6, 2, 128, 900, "bf16", "V1", "random"),         # G=3: Q staged by loads, one CTA
+    (2, 9, 6, 2, 64, 700, "bf16", "V2", "beam"),             # G=3, d=64
 ]
 
 

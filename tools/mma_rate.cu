@@ -12,8 +12,8 @@
 
 using namespace hta;
 
-template <bool PAIR, bool TS, int N, bool W = false>
-__global__ void __launch_bounds__(128, 1) mma_kernel(int iters, int per_commit, int b_mn_major, unsigned long long *cycles) {
+template <bool PAIR, bool TS, int N, bool W = false, int PW = 0>
+__global__ void __launch_bounds__(320, 1) mma_kernel(int iters, int per_commit, int b_mn_major, unsigned long long *cycles) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 65536);
     uint64_t *fin = bar + 1;
@@ -39,6 +39,25 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int iters, int per_commit, 
     if (PAIR) cluster_sync();
     tc_fence_after();
     const uint32_t tmem = *tslot;
+    volatile __shared__ int stop_flag;
+    if (threadIdx.x == 0) stop_flag = 0;
+    __syncthreads();
+    if (PW > 0 && warp >= 2 && warp < 2 + PW) {
+        // TMEM pressure: S-like loads of 64 columns per thread + P-like stores, as the softmax does
+        const int q = warp & 3;
+        const uint32_t lane_off = static_cast<uint32_t>(q * 32 + ((warp - 2) >> 2) * 16) << 16;
+        float acc = 0.f;
+        for (int it = 0; it < 4000 && !stop_flag; ++it) {
+            float v[64];
+            tmem_ld_16x64_split64(tmem + lane_off + 256, v);
+            uint32_t pk[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) pk[i] = __float_as_uint(v[2 * i] + v[2 * i + 1] + acc);
+            tmem_st_16x32_split<32>(tmem + lane_off + 320, pk);
+            acc += v[5];
+        }
+        if (acc == 1.2345f) cycles[1] = 1;
+    }
     if (W && warp == 0 && rank == 0) {
         // warp-converged issue with descriptors precomputed once and bumped by constants
         const uint32_t base = smem_u32(smem);
@@ -76,6 +95,7 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int iters, int per_commit, 
         mbar_wait(fin, 0);
         const unsigned long long t1 = clock64();
         if (lane == 0) cycles[blockIdx.x * 2] = t1 - t0;
+        stop_flag = 1;
     } else if (!W && warp == 0 && rank == 0 && lane == 0) {
         const uint32_t base = smem_u32(smem);
         const uint32_t idesc = idesc_bf16_f32(PAIR ? 256 : 128, N, b_mn_major);
@@ -126,9 +146,9 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int iters, int per_commit, 
     }
 }
 
-template <bool PAIR, bool TS, int N = 128, bool W = false>
+template <bool PAIR, bool TS, int N = 128, bool W = false, int PW = 0>
 void run(const char *name, int per_commit, int mn) {
-    auto kern = mma_kernel<PAIR, TS, N, W>;
+    auto kern = mma_kernel<PAIR, TS, N, W, PW>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
     unsigned long long *cyc;
     cudaMalloc(&cyc, 148 * 2 * 8);
@@ -136,7 +156,7 @@ void run(const char *name, int per_commit, int mn) {
     const int grid = 148;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(128);
+    cfg.blockDim = dim3(320);
     cfg.dynamicSmemBytes = 65536 + 1024;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -168,21 +188,100 @@ void run(const char *name, int per_commit, int mn) {
            err == cudaSuccess ? "" : cudaGetErrorString(err));
 }
 
-int main() {
-    run<false, false, 128, true>("WARP single SS M128", 8, 0);
-    run<false, true, 128, true>("WARP single TS M128 (MN B)", 8, 1);
-    run<true, false, 128, true>("WARP pair SS M256", 8, 0);
-    run<true, true, 128, true>("WARP pair TS M256 (MN B)", 8, 1);
-    run<true, false, 256, true>("WARP pair SS M256", 8, 0);
-    run<false, false, 256>("single SS M128", 8, 0);
-    run<true, false, 256>("pair SS M256", 8, 0);
-    run<true, true, 256>("pair TS M256", 8, 1);
-    for (int pc : {8}) {
-        run<false, false>("single SS M128 N128 (K-major B)", pc, 0);
-        run<false, false>("single SS M128 N128 (MN-major B)", pc, 1);
-        run<false, true>("single TS M128 N128 (MN-major B)", pc, 1);
-        run<true, false>("pair SS M256 N128 (K-major B)", pc, 0);
-        run<true, true>("pair TS M256 N128 (MN-major B)", pc, 1);
+
+// The prefix kernel's exact MMA stream for one pair: per tile S (SS, 8 x K16 into buffer j%3)
+// then PV (TS, 8 x K16 reading P from buffer (j-2)%3, into O), four commits per tile, no waits.
+template <bool PAIR>
+__global__ void __launch_bounds__(64, 1) seq_kernel(int tiles, unsigned long long *cycles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 65536 + 65536);
+    uint64_t *fin = bar + 8;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(bar + 9);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 9; ++i) mbar_init(&bar[i], 1);
+        fence_mbar_init();
     }
+    if (warp == 1) {
+        if (PAIR) { tmem_alloc2(tslot, 512); tmem_relinquish2(); } else { tmem_alloc(tslot, 512); tmem_relinquish(); }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (PAIR) cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    if (warp == 0 && rank == 0) {
+        const uint32_t base = smem_u32(smem);
+        const uint32_t idesc_qk = idesc_bf16_f32(PAIR ? 256 : 128, 128, 0);
+        const uint32_t idesc_pv = idesc_bf16_f32(PAIR ? 256 : 128, 128, 1);
+        const uint64_t qd0 = sdesc_sw128(base, 16, 1024);
+        const uint64_t kd0 = sdesc_sw128(base + 32768, 16, 1024);
+        const uint64_t vd0 = sdesc_sw128(base + 65536, 128 * 128, 1024);
+        const unsigned long long t0 = clock64();
+        for (int j = 0; j < tiles; ++j) {
+            const int buf = j % 3;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t qo = ((k / 4) * 16384 + (k % 4) * 32) >> 4;
+                const uint32_t ko = ((k / 4) * 8192 + (k % 4) * 32) >> 4;
+                if (PAIR) mma2_bf16_ss_elect(tmem + 128 * buf, qd0 + qo, kd0 + ko, idesc_qk, k > 0);
+                else mma_bf16_ss_elect(tmem + 128 * buf, qd0 + qo, kd0 + ko, idesc_qk, k > 0);
+            }
+            if (PAIR) { tc_commit2_mc_elect(&bar[buf]); tc_commit2_mc_elect(&bar[3]); }
+            else { tc_commit_elect(&bar[buf]); tc_commit_elect(&bar[3]); }
+            const int pb = (j + 1) % 3;  // PV of tile j-2
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (PAIR) mma2_bf16_ts_elect(tmem + 384, tmem + 128 * pb + k * 8, vd0 + k * 128, idesc_pv, 1u);
+                else mma_bf16_ts_elect(tmem + 384, tmem + 128 * pb + k * 8, vd0 + k * 128, idesc_pv, 1u);
+            }
+            if (PAIR) { tc_commit2_mc_elect(&bar[4 + pb]); tc_commit2_mc_elect(&bar[7]); }
+            else { tc_commit_elect(&bar[4 + pb]); tc_commit_elect(&bar[7]); }
+        }
+        if (PAIR) tc_commit2_mc_elect(fin); else tc_commit_elect(fin);
+        mbar_wait(fin, 0);
+        const unsigned long long t1 = clock64();
+        if (lane == 0) cycles[0] = t1 - t0;
+    }
+    if (PAIR && rank == 1 && threadIdx.x == 0) mbar_wait(fin, 0);
+    __syncthreads();
+    if (PAIR) cluster_sync();
+    if (warp == 1) { if (PAIR) tmem_dealloc2(tmem, 512); else tmem_dealloc(tmem, 512); }
+}
+
+template <bool PAIR>
+void run_seq(const char *name) {
+    auto kern = seq_kernel<PAIR>;
+    const int smem = 65536 * 2 + 1024;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    unsigned long long *cyc;
+    cudaMalloc(&cyc, 64);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(148);
+    cfg.blockDim = dim3(64);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = PAIR ? 2 : 1; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr; cfg.numAttrs = 1;
+    const int tiles = 1000;
+    for (int it = 0; it < 3; ++it) cudaLaunchKernelEx(&cfg, kern, tiles, cyc);
+    cudaDeviceSynchronize();
+    unsigned long long c0;
+    cudaMemcpy(&c0, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("%-40s %7.1f SM-cycles per tile (S + PV; 1024 = full rate) %s\n", name, double(c0) / tiles,
+           cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+    run_seq<true>("kernel MMA sequence, pair");
+    run_seq<false>("kernel MMA sequence, single");
+    run<true, false, 128, true, 0>("WARP pair SS M256, no pressure", 8, 0);
+    run<true, true, 128, true, 0>("WARP pair TS M256, no pressure", 8, 1);
+    run<true, false, 128, true, 8>("WARP pair SS M256, 8 TMEM warps", 8, 0);
+    run<true, true, 128, true, 8>("WARP pair TS M256, 8 TMEM warps", 8, 1);
+    run<true, true, 128, true, 4>("WARP pair TS M256, 4 TMEM warps", 8, 1);
+    run<false, true, 128, true, 8>("WARP single TS M128, 8 TMEM warps", 8, 1);
     return 0;
 }

@@ -1,0 +1,77 @@
+// softmax_rate.cu -- diagnostics: throughput of the prefix kernel's softmax inner loop (per row:
+// scale, exp2, row sum, pack to bf16) for different fractions of FMA-pipe polynomial exp2, with
+// 8 softmax warps per SM as in the kernel.  Registers only (no TMEM).  Build & run on the box:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude tools/softmax_rate.cu -o /tmp/sm_rate
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "../paper_2502_17421_b200/csrc/ptx_sm100.cuh"
+
+using namespace hta;
+
+template <int EMU8>  // number of column pairs out of every 8 computed by the polynomial
+__global__ void __launch_bounds__(256, 1) softmax_loop(int iters, float c, float *out) {
+    float s[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) s[i] = (threadIdx.x * 0.001f) - i * 0.01f;
+    float m = 0.5f, acc_all = 0.f;
+    uint32_t sink = 0;
+    for (int it = 0; it < iters; ++it) {
+        const float2 c2 = make_float2(c, c), neg2 = make_float2(-m, -m);
+        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+        const float2 *s2 = reinterpret_cast<const float2 *>(s);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const float2 x = __ffma2_rn(s2[i], c2, neg2);
+            float2 pp;
+            if ((i & 7) < EMU8) {
+                pp = exp2_poly2(x);
+            } else {
+                pp.x = fast_exp2(x.x);
+                pp.y = fast_exp2(x.y);
+            }
+            if (i & 1)
+                acc1 = __fadd2_rn(acc1, pp);
+            else
+                acc0 = __fadd2_rn(acc0, pp);
+            sink ^= pack_bf16x2(pp.x, pp.y);
+        }
+        acc_all += (acc0.x + acc1.x) + (acc0.y + acc1.y);
+        m += 1e-7f;  // loop-carried so the compiler cannot hoist the exps
+    }
+    if (sink == 0x12345 || acc_all == 1.2345f) out[threadIdx.x] = acc_all;
+}
+
+template <int EMU8>
+void run() {
+    float *out;
+    cudaMalloc(&out, 4096);
+    const int iters = 20000;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e9;
+    for (int r = 0; r < 4; ++r) {
+        cudaEventRecord(e0);
+        softmax_loop<EMU8><<<148, 256>>>(iters, 0.12f, out);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r > 0 && ms < best) best = ms;
+    }
+    // per SM: 8 warps x 32 lanes x 64 elements x iters; per SMSP: 2 warps
+    const double elems_per_smsp = 2.0 * 64 * iters;
+    printf("poly %d/8: %8.1f us  -> %.2f cycles per 32-wide element slot per SMSP @1.9GHz  (%.1f Gexp/s/SM)\n", EMU8,
+           best * 1e3, best * 1e-3 * 1.9e9 / elems_per_smsp, 8.0 * 32 * 64 * iters / (best * 1e-3) / 1e9);
+}
+
+int main() {
+    run<0>();
+    run<2>();
+    run<3>();
+    run<4>();
+    run<8>();
+    return 0;
+}
