@@ -9,7 +9,7 @@
 
 namespace hta {
 
-constexpr int kBlockN = 128;   // keys per KV tile of the prefix pass
+constexpr int kBlockN = 192;   // keys per KV tile of the prefix pass (2 x 192 S columns + O = 512 TMEM columns)
 constexpr int kRowsPerTile = 128;  // rows of one tcgen05 M=128 tile
 
 // Work decomposition of the prefix pass.

@@ -9,20 +9,24 @@
 //
 //  * rows: the T tree tokens x the G query heads of one KV head form the M dimension
 //    (row r = t*G + j, head h = g*G + j).  Each CTA owns 128 rows (one TMEM lane per row).
+//  * KV tiles of kBlockN = 192 keys: TMEM holds two S/P buffers of 192 fp32 columns and the
+//    128-column O accumulator (512 columns), and the fixed per-tile costs of the softmax warps
+//    (barrier checks, publication, reduction latency) are spread over 192 keys.
 //  * PAIR (M > 128, d = 128): a cluster of two CTAs on one TPC runs tcgen05.mma.cta_group::2
-//    with M = 256: each CTA holds its 128 Q rows, HALF of every K tile (64 keys) and HALF of
+//    with M = 256: each CTA holds its 128 Q rows, HALF of every K tile (96 keys) and HALF of
 //    every V tile (64 head-dim columns), so each KV byte is read from HBM once for 256 rows and
 //    each SM streams only half of the operand bytes through shared memory.
 //  * warp 0 (one lane) streams K and V tiles with TMA into two rings of smem slots (128B
 //    swizzle, the canonical UMMA layout) so K tiles can run ahead of V tiles; in a pair both
 //    CTAs' bytes are counted on the leader's barriers.
-//  * warp 1 of the leader CTA issues the MMAs from a non-blocking, warp-converged loop
-//    (elect.sync per instruction, descriptors advanced by constants): S = Q K^T into one of three
-//    TMEM buffers (fp32) as soon as a K tile and a buffer are free, and O += P V with A = P read
-//    from TMEM (the "TS" form) and B = V from smem (MN-major) as soon as P and the V tile are ready.
+//  * warp 1 of the leader CTA issues the MMAs in a fixed order with suspended barrier waits, one
+//    elected lane issuing each group (descriptors are warp-uniform and advanced by constants):
+//    S = Q K^T into one of two TMEM buffers (fp32) once a K tile and a buffer are free, and
+//    O += P V with A = P read from TMEM (the "TS" form) and B = V from smem (MN-major) once P and
+//    the V tile are ready.
 //  * warps 2-9 (softmax): the two warps that share a TMEM lane quarter own disjoint 16-row halves
-//    of it, and each row is shared by a pair of threads (lanes t and t+16) that each hold 64 of
-//    its 128 S values (tcgen05.ld .16x32bx2).  Per tile: row max (one shuffle between the pair),
+//    of it, and each row is shared by a pair of threads (lanes t and t+16) that each hold 96 of
+//    its 192 S values (tcgen05.ld .16x32bx2).  Per tile: row max (one shuffle between the pair),
 //    exp2 (3/8 of the pairs on the FMA pipe by polynomial, the rest on MUFU), row sum, P -> bf16
 //    -> tcgen05.st over S.  No two warps ever exchange data, so they drift freely and overlap
 //    each other's latency.  O is rescaled in TMEM only when the running max grows by more than
@@ -46,8 +50,8 @@ __device__ unsigned long long g_cta_times[1024][4];  // per CTA: entry ns, loop 
 constexpr int kTraceRecs = 200;  // per warp, in shared memory (flushed to g_trace at the end)
 #define HTA_TR(ev, tag, jj)                                                                              \
     do {                                                                                                 \
-        if (lane == 0 && tr_n < kTraceRecs)                                                              \
-            tr_buf[warp * kTraceRecs + tr_n++] = (static_cast<unsigned long long>(ev) << 56) |            \
+        if (lane == 0 && tr_n < C::kTraceCap)                                                            \
+            tr_buf[warp * C::kTraceCap + tr_n++] = (static_cast<unsigned long long>(ev) << 56) |            \
                                                  (static_cast<unsigned long long>(tag) << 52) |           \
                                                  (static_cast<unsigned long long>((jj) & 0xFFFFF) << 32) |\
                                                  static_cast<unsigned long long>(static_cast<uint32_t>(clock64())); \
@@ -62,9 +66,9 @@ __device__ __forceinline__ uint64_t trace_globaltimer() {
     do {                                                                                                 \
         const uint32_t c_ = static_cast<uint32_t>(clock64());                                            \
         const uint32_t t_ = static_cast<uint32_t>(trace_globaltimer());                                  \
-        if (lane == 0 && tr_n + 1 < kTraceRecs) {                                                        \
-            tr_buf[warp * kTraceRecs + tr_n++] = (static_cast<unsigned long long>(ev) << 56) | c_;       \
-            tr_buf[warp * kTraceRecs + tr_n++] = (static_cast<unsigned long long>(ev + 1) << 56) | t_;   \
+        if (lane == 0 && tr_n + 1 < C::kTraceCap) {                                                      \
+            tr_buf[warp * C::kTraceCap + tr_n++] = (static_cast<unsigned long long>(ev) << 56) | c_;     \
+            tr_buf[warp * C::kTraceCap + tr_n++] = (static_cast<unsigned long long>(ev + 1) << 56) | t_; \
         }                                                                                                \
     } while (0)
 #else
@@ -76,11 +80,7 @@ __device__ __forceinline__ uint64_t trace_globaltimer() {
 // leaving the TMA stream and the barrier protocol; HTA_SKIP=3 runs the MMAs with no TMA traffic
 // (operands are whatever sits in smem) and no softmax; HTA_SKIP=4 = 3 with the softmax.
 // Product builds use 0.
-// Ping-pong of the two softmax warps sharing an SM sub-partition (see the softmax loop).
-#ifndef HTA_PINGPONG
-#define HTA_PINGPONG 0
-#endif
-// Publish P_j only after the load of S_{j+1} is issued (see the softmax loop).
+// Publish P_j at the start of tile j+1 (see the softmax loop).
 #ifndef HTA_DEFER
 #define HTA_DEFER 1
 #endif
@@ -104,7 +104,9 @@ struct TcCfg {
     static constexpr int kKBytes = kKRows * D * 2;
     static constexpr int kVBytes = kBlockN * kVCols * 2;
 #ifdef HTA_TRACE
-    static constexpr int kRingBytes = 176 * 1024;  // 16 KiB of smem hold the trace records
+    // the trace records take 24 KiB of the ring (not for D = 128 single CTAs: two 48 KiB slots)
+    static constexpr int kTraceCap = (PAIR || D == 64) ? kTraceRecs : 0;
+    static constexpr int kRingBytes = kTraceCap ? 168 * 1024 : 192 * 1024;
 #else
     static constexpr int kRingBytes = 192 * 1024;
 #endif
@@ -115,14 +117,14 @@ struct TcCfg {
     static constexpr int kSlotsK = (kRingBytes / 2) / kKBytes;
     static constexpr int kSlotsV = (kRingBytes / 2) / kVBytes;
 #endif
-    static constexpr int kSBufs = 3;                            // S/P buffers in TMEM
+    static constexpr int kSBufs = 2;                            // S/P buffers in TMEM (2 x 192 columns)
     static constexpr int kSoftmaxWarps = 8;                     // two warpgroups
     static constexpr int kThreads = 64 + 32 * kSoftmaxWarps;    // warp 0 TMA, warp 1 MMA + TMEM
     static constexpr int kVOff = kQBytes + kSlotsK * kKBytes;   // start of the V ring
     static constexpr int kBarOff = kVOff + kSlotsV * kVBytes;
 #ifdef HTA_TRACE
     static constexpr int kTraceOff = kBarOff + 512;
-    static constexpr int kSmemBytes = kTraceOff + 10 * 200 * 8;
+    static constexpr int kSmemBytes = kTraceOff + 10 * kTraceCap * 8;
 #else
     static constexpr int kSmemBytes = kBarOff + 512;  // base is 1024-aligned (__align__ below)
 #endif
@@ -131,8 +133,8 @@ struct TcCfg {
 };
 
 // TMEM column map: S/P buffer b at 128*b (b = 0, 1, 2), O at 384.
-__device__ __forceinline__ uint32_t s_col(int buf) { return 128u * static_cast<uint32_t>(buf); }
-constexpr uint32_t kOCol = 384u;
+__device__ __forceinline__ uint32_t s_col(int buf) { return static_cast<uint32_t>(kBlockN * buf); }
+constexpr uint32_t kOCol = 2u * kBlockN;  // O: 128 fp32 columns after the two S buffers (384 + 128 = 512)
 
 template <int D, bool PAIR>
 __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     uint64_t *v_empty = v_full + C::kSlotsV;       // [kSlotsV]
     uint64_t *s_full = v_empty + C::kSlotsV;       // [kSBufs]
     uint64_t *p_full = s_full + C::kSBufs;         // [kSBufs]   (the leader's copy is the one used)
-    uint64_t *pv_done = p_full + C::kSBufs;        // [kSBufs]   PV_j arrives on pv_done[j % 3]
+    uint64_t *pv_done = p_full + C::kSBufs;        // [kSBufs]   PV_j arrives on pv_done[j % kSBufs]
     uint64_t *o_final = pv_done + C::kSBufs;       // [1]
     uint64_t *q_full = o_final + 1;                // [1]       Q staged (the leader's copy is the one used)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_full + 1);
@@ -371,8 +373,8 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             const bool issuer = elect_one() != 0;
             // Fixed order with hardware-suspended waits (no polling: a spinning issuer would take
             // issue slots from the softmax warps sharing its SM sub-partition):
-            //   S_0, S_1, S_2, then for every j: PV_j (needs V_j and P_j), S_{j+3} (needs K_{j+3};
-            //   its buffer was last read by PV_j, issued just before).
+            //   S_0, S_1, then for every j: PV_j (needs V_j and P_j), S_{j+2} (needs K_{j+2}; its
+            //   buffer was last read by PV_j, issued just before).
             constexpr bool kNoMem = HTA_SKIP >= 3;
             auto wait_all = [](uint64_t *bar, uint32_t parity) {
                 mbar_wait(bar, parity);
@@ -468,15 +470,6 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         const uint32_t pfull0 = PAIR ? mapa_shared(smem_u32(&p_full[0]), 0) : 0u;
         constexpr int kHalfCols = kBlockN / 2;
         float m_run = -INFINITY, l_run = 0.f;  // l_run: this thread's 64 columns only
-        // Ping-pong: warps w and w+4 share a sub-partition (same TMEM lane quarter) and would
-        // otherwise run every tile in phase -- both in the issue-bound exponential loop at once,
-        // both idle in the latency-bound TMEM load / store / barrier phases.  Named barriers
-        // make their exponential loops alternate (rh 0 on tile j, rh 1 on tile j, rh 0 on j+1,
-        // ...), so each warp's latency phases overlap its partner's arithmetic.
-        constexpr bool kPingPong = HTA_PINGPONG != 0 && (HTA_SKIP < 1 || HTA_SKIP == 4);
-        const uint32_t bar_mine = 1u + static_cast<uint32_t>(quarter + 4 * rh);
-        const uint32_t bar_partner = 1u + static_cast<uint32_t>(quarter + 4 * (1 - rh));
-        if (kPingPong && rh == 1) named_bar_arrive(bar_partner, 64);  // rh 0 goes first
         // Publish P_jp (stored to TMEM without waiting): wait for the stores (and any O rescale
         // of that tile), sanitise the garbage V rows of the last tile, signal the MMA warp.
         auto publish = [&](int jp) {
@@ -484,8 +477,9 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             if (jp == n_tiles - 1 && tail_zero) {
                 // V rows (keys) past the sequence end: zero this CTA's part of key row r (may be
                 // NaN); the thread pair of row r splits the row's 16-byte chunks
-                if (r >= tail_valid) {
-                    uint8_t *vrow = sV + ((n_tiles - 1) % C::kSlotsV) * C::kVBytes + r * 128;
+                for (int kr = r; kr < kBlockN; kr += kRowsPerTile) {  // key rows r and r + 128
+                    if (kr < tail_valid) continue;
+                    uint8_t *vrow = sV + ((n_tiles - 1) % C::kSlotsV) * C::kVBytes + kr * 128;
                     constexpr int kChunks16 = C::kVCols * 2 / 16;  // 16-byte chunks in this CTA's row
 #pragma unroll
                     for (int cch = chalf * (kChunks16 / 2); cch < (chalf + 1) * (kChunks16 / 2); ++cch)
@@ -507,9 +501,10 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             }
             HTA_TR(13, warp - 2, jp);
         };
-        // Deferred publication: P_{j-1} is published after the load of S_j is issued, so the
-        // store-completion wait overlaps the load latency instead of adding to each tile's
-        // critical path (the MMA warp has slack: 3 S buffers).
+        // Deferred publication: P_{j-1} is published once S_j is ready, just before S_j is loaded,
+        // so the completion of P_{j-1}'s stores is waited for a tile later (long done) instead of
+        // right after the exponentials, on each tile's critical path.  No deadlock: S_j needs only
+        // P_{j-2}, published at the start of tile j-1.
         constexpr bool kDefer = HTA_DEFER != 0;
         for (int j = 0; j < n_tiles; ++j) {
             const int buf = j % C::kSBufs;
@@ -519,63 +514,64 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             const bool last = j == n_tiles - 1;
             float mt = 0.f, lsum = 0.f;
             if (HTA_SKIP < 1 || HTA_SKIP == 4) {
-                float s[kHalfCols];
-                tmem_ld_16x64_split64_nowait(tmem + lane_off + s_col(buf), s);
+                float s[kHalfCols];  // this thread's 96 S values: keys [96*chalf, 96*chalf + 96)
                 if (kDefer && j > 0) publish(j - 1);
-                tmem_ld_wait64(s);
+                tmem_ld_x96<kHalfCols>(tmem + lane_off + s_col(buf), s);
                 if (last && tail_valid < kBlockN) {
                     // keys past the split end -> -inf (last tile only; the empty asm keeps this a
                     // real branch instead of per-element selects on every tile)
                     asm volatile("" ::: "memory");
+                    const int lim = tail_valid - chalf * kHalfCols;  // this thread's first invalid column
 #pragma unroll
                     for (int cc = 0; cc < kHalfCols; ++cc)
-                        if (chalf * kHalfCols + cc >= tail_valid) s[cc] = -INFINITY;
+                        if (cc >= lim) s[cc] = -INFINITY;
                 }
-                if (kPingPong) named_bar_sync(bar_mine, 64);
-                float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+                // P = exp2(S*c - m) -> bf16 over S in TMEM; returns this thread's row sum.  3 of
+                // every 8 column pairs use the FMA-pipe polynomial, the rest MUFU ex2 (MUFU alone
+                // would co-limit the MMAs).  P packed (2 bf16 per column): keys [96h, 96h+96) ->
+                // columns [48h, 48h+48), stored in three 16-column chunks without waiting (one
+                // wait::st before P is published).
+                auto exp_store = [&](float m_use) {
+                    const float2 c2 = make_float2(c, c), neg2 = make_float2(-m_use, -m_use);
+                    float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+                    const float2 *s2 = reinterpret_cast<const float2 *>(s);
+                    uint32_t pk[16];
 #pragma unroll
-                for (int cc = 4; cc < kHalfCols; cc += 8) {
-                    mx0 = fmaxf(mx0, fmaxf(s[cc], s[cc + 4]));
-                    mx1 = fmaxf(mx1, fmaxf(s[cc + 1], s[cc + 5]));
-                    mx2 = fmaxf(mx2, fmaxf(s[cc + 2], s[cc + 6]));
-                    mx3 = fmaxf(mx3, fmaxf(s[cc + 3], s[cc + 7]));
-                }
-                float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));  // the other half of the row
-                mt = mx * c;
-                if (warp == 2) HTA_TR(11, 0, j);
-                const float m_new = (mt > m_run + 8.0f) ? mt : m_run;
-                // P = exp2(S*c - m) -> bf16 over S in TMEM.  3 of every 8 column pairs use the
-                // FMA-pipe polynomial, the rest MUFU ex2 (MUFU alone would co-limit the MMAs).
-                const float2 c2 = make_float2(c, c), neg2 = make_float2(-m_new, -m_new);
-                float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-                const float2 *s2 = reinterpret_cast<const float2 *>(s);
-                uint32_t pk[kHalfCols / 2];
-                // P packed (2 bf16 per column): keys [64h, 64h+64) -> columns [32h, 32h+32).  Both
-                // halves of a row live in the same warp, whose S loads above already completed.
-                // Stored in two 16-column halves without waiting, so the first store overlaps the
-                // second half's exponentials; one wait::st before P is published.
-#pragma unroll
-                for (int i = 0; i < kHalfCols / 2; ++i) {
-                    const float2 x = __ffma2_rn(s2[i], c2, neg2);
-                    float2 pp;
-                    if ((i & 7) < 3) {
-                        pp = exp2_poly2(x);
-                    } else {
-                        pp.x = fast_exp2(x.x);
-                        pp.y = fast_exp2(x.y);
+                    for (int i = 0; i < kHalfCols / 2; ++i) {
+                        const float2 x = __ffma2_rn(s2[i], c2, neg2);
+                        float2 pp;
+                        if ((i & 7) < 3) {
+                            pp = exp2_poly2(x);
+                        } else {
+                            pp.x = fast_exp2(x.x);
+                            pp.y = fast_exp2(x.y);
+                        }
+                        if (i & 1)
+                            acc1 = __fadd2_rn(acc1, pp);
+                        else
+                            acc0 = __fadd2_rn(acc0, pp);
+                        pk[i & 15] = pack_bf16x2(pp.x, pp.y);
+                        if ((i & 15) == 15)
+                            tmem_st_16x16_split_nowait<kHalfCols / 2>(tmem + lane_off + s_col(buf) + (i - 15), pk);
                     }
-                    if (i & 1)
-                        acc1 = __fadd2_rn(acc1, pp);
-                    else
-                        acc0 = __fadd2_rn(acc0, pp);
-                    pk[i] = pack_bf16x2(pp.x, pp.y);
-                    if (i == 15) tmem_st_16x16_split_nowait<32>(tmem + lane_off + s_col(buf), pk);
-                }
-                tmem_st_16x16_split_nowait<32>(tmem + lane_off + s_col(buf) + 16, pk + 16);
-                if (kPingPong && (rh == 0 || !last)) named_bar_arrive(bar_partner, 64);
-                lsum = (acc0.x + acc1.x) + (acc0.y + acc1.y);
-                mt = m_new;
+                    return (acc0.x + acc1.x) + (acc0.y + acc1.y);
+                };
+                auto row_max = [&]() {  // max over the row (this thread's 96 values and its pair's)
+                    float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+#pragma unroll
+                    for (int cc = 4; cc < kHalfCols; cc += 8) {
+                        mx0 = fmaxf(mx0, fmaxf(s[cc], s[cc + 4]));
+                        mx1 = fmaxf(mx1, fmaxf(s[cc + 1], s[cc + 5]));
+                        mx2 = fmaxf(mx2, fmaxf(s[cc + 2], s[cc + 6]));
+                        mx3 = fmaxf(mx3, fmaxf(s[cc + 3], s[cc + 7]));
+                    }
+                    const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+                    return fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16)) * c;
+                };
+                const float mx = row_max();
+                if (warp == 2) HTA_TR(11, 0, j);
+                mt = (mx > m_run + 8.0f) ? mx : m_run;  // stale max: rescale only on a jump > 2^8
+                lsum = exp_store(mt);
             } else {
                 if (kDefer && j > 0) publish(j - 1);
                 mt = 0.f;
@@ -583,8 +579,8 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             }
             if (warp == 2) HTA_TR(12, 0, j);
             // Rescale O only when the running max moved.  O must then hold P_{j-1} V_{j-1} first:
-            // wait for PV_{j-1} on its own barrier pv_done[(j-1) % 3].  That barrier cannot run two
-            // phases ahead (PV_{j+2} needs P_{j+2}, not yet published), so the parity wait is exact
+            // wait for PV_{j-1} on its own barrier pv_done[(j-1) % 2].  That barrier cannot run a
+            // phase ahead (PV_{j+1} needs P_{j+1}, not yet published), so the parity wait is exact
             // although most tiles never wait.
             const bool need = (j > 0) && (mt != m_run);
             const float f = need ? fast_exp2(m_run - mt) : 1.0f;
@@ -640,7 +636,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         g_cta_times[blockIdx.x][2] = clock64() - g_cta_times[blockIdx.x][2];
     }
     if (g_trace != nullptr && blockIdx.x == g_trace_cta && lane == 0)
-        for (int i = 0; i < tr_n; ++i) g_trace[warp * 2048 + i] = tr_buf[warp * kTraceRecs + i];
+        for (int i = 0; i < tr_n; ++i) g_trace[warp * 2048 + i] = tr_buf[warp * C::kTraceCap + i];
 #endif
     tc_fence_before();
     __syncthreads();

@@ -59,13 +59,15 @@ def test_workspace_size_matches_split_plan(L):
     # split, 9 splits = 144 CTAs
     s = _shape()
     assert L.hta_workspace_size(ctypes.byref(s), 148) == 9 * part(s)
-    # forced splits are capped by the number of 128-key tiles
+    # forced splits are capped by the number of 192-key tiles
     s = _shape(N=300, splits=7)
-    assert L.hta_workspace_size(ctypes.byref(s), 148) == 3 * part(s)
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == 2 * part(s)
+    s = _shape(N=1000, splits=7)
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == 6 * part(s)
     s = _shape(N=0)
     assert L.hta_workspace_size(ctypes.byref(s), 148) == 1 * part(s)
     # QwQ-like: M = 320 -> 2 pair row groups x 8 kv heads x B=4 = 64 pairs = 128 CTAs per split;
-    # 1 split = 0.86 wave, 2 splits = 1.73 waves (cost 1.0 vs 1.02) -> 1 split
+    # 1 split = 0.86 wave, 2 splits = 1.73 waves -> 1 split
     s = _shape(B=4, H=40, N=32768)
     assert L.hta_workspace_size(ctypes.byref(s), 148) == 1 * part(s)
 

@@ -10,7 +10,9 @@
 
 using namespace hta;
 
-template <int EMU8>  // number of column pairs out of every 8 computed by the polynomial
+// EMU8: number of column pairs out of every 8 computed by the polynomial; SPREAD: poly pairs
+// spread evenly (i % 8 in {0, 3, 6}) instead of clustered ({0, 1, 2})
+template <int EMU8, bool SPREAD = false>
 __global__ void __launch_bounds__(256, 1) softmax_loop(int iters, float c, float *out) {
     float s[64];
 #pragma unroll
@@ -25,7 +27,9 @@ __global__ void __launch_bounds__(256, 1) softmax_loop(int iters, float c, float
         for (int i = 0; i < 32; ++i) {
             const float2 x = __ffma2_rn(s2[i], c2, neg2);
             float2 pp;
-            if ((i & 7) < EMU8) {
+            const bool poly = SPREAD ? (EMU8 == 3 && ((i & 7) == 0 || (i & 7) == 3 || (i & 7) == 6))
+                                     : ((i & 7) < EMU8);
+            if (poly) {
                 pp = exp2_poly2(x);
             } else {
                 pp.x = fast_exp2(x.x);
@@ -43,8 +47,8 @@ __global__ void __launch_bounds__(256, 1) softmax_loop(int iters, float c, float
     if (sink == 0x12345 || acc_all == 1.2345f) out[threadIdx.x] = acc_all;
 }
 
-template <int EMU8>
-void run() {
+template <int EMU8, bool SPREAD = false>
+void run(int threads = 256) {
     float *out;
     cudaMalloc(&out, 4096);
     const int iters = 20000;
@@ -54,24 +58,27 @@ void run() {
     float best = 1e9;
     for (int r = 0; r < 4; ++r) {
         cudaEventRecord(e0);
-        softmax_loop<EMU8><<<148, 256>>>(iters, 0.12f, out);
+        softmax_loop<EMU8, SPREAD><<<148, threads>>>(iters, 0.12f, out);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
         if (r > 0 && ms < best) best = ms;
     }
-    // per SM: 8 warps x 32 lanes x 64 elements x iters; per SMSP: 2 warps
-    const double elems_per_smsp = 2.0 * 64 * iters;
-    printf("poly %d/8: %8.1f us  -> %.2f cycles per 32-wide element slot per SMSP @1.9GHz  (%.1f Gexp/s/SM)\n", EMU8,
-           best * 1e3, best * 1e-3 * 1.9e9 / elems_per_smsp, 8.0 * 32 * 64 * iters / (best * 1e-3) / 1e9);
+    // per SMSP: threads/128 warps x 64 elements x iters
+    const double elems_per_smsp = threads / 128.0 * 64 * iters;
+    printf("poly %d/8%s, %d warps/SMSP: %8.1f us  -> %.2f cycles per 32-wide element slot per SMSP @1.9GHz\n", EMU8,
+           SPREAD ? " spread" : "", threads / 128, best * 1e3, best * 1e-3 * 1.9e9 / elems_per_smsp);
 }
 
 int main() {
-    run<0>();
-    run<2>();
-    run<3>();
-    run<4>();
-    run<8>();
+    for (int t : {128, 256}) {
+        run<0>(t);
+        run<2>(t);
+        run<3>(t);
+        run<3, true>(t);
+        run<4>(t);
+        run<8>(t);
+    }
     return 0;
 }

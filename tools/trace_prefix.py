@@ -106,6 +106,23 @@ def main():
         if d(10, 11):
             print(f"wg{w}: ld+max {statistics.mean(d(10, 11)):.0f}  exp {statistics.mean(d(11, 12)):.0f}  "
                   f"store+arrive {statistics.mean(d(12, 13)):.0f}  P->next S {statistics.mean(nxt) if nxt else 0:.0f}")
+    w = 0
+    seg = lambda a, b: [ev[(b, w, j)] - ev[(a, w, j)] for j in js[2:-2] if (a, w, j) in ev and (b, w, j) in ev]
+    nx = [ev[(10, w, j + 1)] - ev[(12, w, j)] for j in js[2:-2] if (12, w, j) in ev and (10, w, j + 1) in ev]
+    if seg(10, 16) and seg(16, 15):
+        print(f"warp 2 per tile: S wait->ld issued+publish {statistics.mean(seg(10, 16)):.0f}  ld wait "
+              f"{statistics.mean(seg(16, 15)):.0f}  max {statistics.mean(seg(15, 11)):.0f}  exp "
+              f"{statistics.mean(seg(11, 12)):.0f}  after exp->next S ready {statistics.mean(nx):.0f}")
+    nx19 = [ev[(19, w, j + 1)] - ev[(12, w, j)] for j in js[2:-2] if (12, w, j) in ev and (19, w, j + 1) in ev]
+    if nx19 and seg(19, 10):
+        print(f"  exp end -> loop top {statistics.mean(nx19):.0f}; try_wait(S, already complete) "
+              f"{statistics.mean(seg(19, 10)):.0f}; S ready -> publish start (fence, tail check, ld issue) "
+              f"{statistics.mean([ev[(18, w, j - 1)] - ev[(10, w, j)] for j in js if (18, w, j - 1) in ev and (10, w, j) in ev]):.0f} (incl. wait::st); "
+              f"wait::st done -> P arrive {statistics.mean([ev[(13, w, j)] - ev[(18, w, j)] for j in js if (13, w, j) in ev and (18, w, j) in ev]):.0f}")
+    rdy = [1 for j in js if (17, 1, j) in ev]
+    nrd = [1 for j in js if (17, 0, j) in ev]
+    if rdy or nrd:
+        print(f"S(j+1) already complete when exp(j) ends: {len(rdy)} of {len(rdy) + len(nrd)} tiles")
     tiles = [ev[(10, 0, j)] for j in js if (10, 0, j) in ev]
     if len(tiles) > 2:
         print(f"period (wg0 S ready to S ready): {(tiles[-1] - tiles[1]) / (len(tiles) - 2):.0f} cycles")
