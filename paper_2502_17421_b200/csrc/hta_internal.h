@@ -9,7 +9,13 @@
 
 namespace hta {
 
-constexpr int kBlockN = 192;   // keys per KV tile of the prefix pass (2 x 192 S columns + O = 512 TMEM columns)
+#ifndef HTA_BLOCK_N
+#define HTA_BLOCK_N 192
+#endif
+// Keys per KV tile of the prefix pass: TMEM holds 384 / kBlockN S/P buffers (2 x 192 or
+// 3 x 128 columns) and the 128-column O accumulator (512 columns in all).
+constexpr int kBlockN = HTA_BLOCK_N;
+static_assert(kBlockN == 128 || kBlockN == 192, "KV tile of 128 or 192 keys");
 constexpr int kRowsPerTile = 128;  // rows of one tcgen05 M=128 tile
 
 // Work decomposition of the prefix pass.

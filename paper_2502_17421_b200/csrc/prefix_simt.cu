@@ -9,6 +9,7 @@
 // fp64 (B200 runs FP64 at half the FP32 rate): fp32 rounding of a 128-term dot product is
 // ~1e-5 of a logit near 100, which would spend the whole 1e-5 budget on extreme inputs.
 #include "hta_internal.h"
+#include "ptx_sm100.cuh"
 
 namespace hta {
 
@@ -18,6 +19,7 @@ __global__ void __launch_bounds__(128) prefix_simt_kernel(const PrefixParams p) 
     constexpr int U = 8;
     const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
+    pdl_launch_dependents();  // the dependent tree/merge grid may start its tree pass now
     if (row >= p.B * p.T * p.H) return;
     const int h = row % p.H;
     const int t = (row / p.H) % p.T;

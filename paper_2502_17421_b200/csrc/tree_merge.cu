@@ -74,160 +74,199 @@ struct VecIO<__nv_bfloat16, 2> {
     }
 };
 
-template <typename Tin, typename Tout, int D>
-__global__ void __launch_bounds__(128) tree_merge_kernel(const TreeMergeParams p) {
+// Tree pass of one output row: normalised tree partial in ot[] and its natural-log LSE.
+template <typename Tin, int D>
+__device__ __forceinline__ float tree_row(const TreeMergeParams &p, int b, int t, int h, int lane,
+                                          float (&ot)[D / 32]) {
     constexpr int E = D / 32;
-    const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (row >= p.B * p.T * p.Hr) return;
-    const int hl = row % p.Hr;
-    const int t = (row / p.Hr) % p.T;
-    const int b = row / (p.Hr * p.T);
-    const int h = p.h0 + hl;
     const int g = h / p.G;
-
-    // ------------------------------------------------------------- tree pass
-    float ot[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) ot[e] = 0.f;
-    float lse_t = -INFINITY;
-    if (p.do_tree) {
-        float qv[E];
-        VecIO<Tin, E>::load(static_cast<const Tin *>(p.q) + b * p.qs0 + t * p.qs1 + h * p.qs2 + lane * E, qv);
-        const Tin *Kt = static_cast<const Tin *>(p.kt) + b * p.ts0 + g * p.ts2 + lane * E;
-        const Tin *Vt = static_cast<const Tin *>(p.vt) + b * p.ts0 + g * p.ts2 + lane * E;
-        const uint8_t *mrow = p.mask + b * p.mask_bs + static_cast<int64_t>(t) * p.T;
-        using Acc = typename std::conditional<std::is_same<Tin, float>::value, double, float>::type;
-        float l = 0.f;
-        Acc m_acc = static_cast<Acc>(-INFINITY);  // running max kept at accumulation precision
-        for (int c0 = 0; c0 < p.T; c0 += 32) {
-            const int s = c0 + lane;
-            uint32_t bits = __ballot_sync(0xffffffffu, s < p.T && mrow[s] != 0);
-            while (bits) {
-                int idx[4];
+    float qv[E];
+    VecIO<Tin, E>::load(static_cast<const Tin *>(p.q) + b * p.qs0 + t * p.qs1 + h * p.qs2 + lane * E, qv);
+    const Tin *Kt = static_cast<const Tin *>(p.kt) + b * p.ts0 + g * p.ts2 + lane * E;
+    const Tin *Vt = static_cast<const Tin *>(p.vt) + b * p.ts0 + g * p.ts2 + lane * E;
+    const uint8_t *mrow = p.mask + b * p.mask_bs + static_cast<int64_t>(t) * p.T;
+    using Acc = typename std::conditional<std::is_same<Tin, float>::value, double, float>::type;
+    float l = 0.f;
+    Acc m_acc = static_cast<Acc>(-INFINITY);  // running max kept at accumulation precision
+    for (int c0 = 0; c0 < p.T; c0 += 32) {
+        const int s = c0 + lane;
+        uint32_t bits = __ballot_sync(0xffffffffu, s < p.T && mrow[s] != 0);
+        while (bits) {
+            int idx[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (bits) {
-                        idx[u] = c0 + __ffs(bits) - 1;
-                        bits &= bits - 1;
-                    } else {
-                        idx[u] = -1;
-                    }
-                }
-                Acc z[4];
-                float vv[4][E];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    float kk[E];
-                    const int sidx = idx[u] < 0 ? idx[0] : idx[u];
-                    VecIO<Tin, E>::load(Kt + sidx * p.ts1, kk);
-                    VecIO<Tin, E>::load(Vt + sidx * p.ts1, vv[u]);
-                    Acc a = 0;
-#pragma unroll
-                    for (int e = 0; e < E; ++e) a = fma(static_cast<Acc>(qv[e]), static_cast<Acc>(kk[e]), a);
-                    z[u] = a;
-                }
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) z[u] += __shfl_xor_sync(0xffffffffu, z[u], off);
-                Acc mx = m_acc;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    z[u] = idx[u] >= 0 ? z[u] * static_cast<Acc>(p.scale) : static_cast<Acc>(-INFINITY);
-                    mx = z[u] > mx ? z[u] : mx;
-                }
-                const float corr = expf(static_cast<float>(m_acc - mx));
-                l *= corr;
-#pragma unroll
-                for (int e = 0; e < E; ++e) ot[e] *= corr;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const float w = expf(static_cast<float>(z[u] - mx));  // 0 for unused slots
-                    l += w;
-#pragma unroll
-                    for (int e = 0; e < E; ++e) ot[e] = fmaf(w, vv[u][e], ot[e]);
-                }
-                m_acc = mx;
-            }
-        }
-        if (l > 0.f) {
-            const float inv = 1.0f / l;
-#pragma unroll
-            for (int e = 0; e < E; ++e) ot[e] *= inv;
-            lse_t = static_cast<float>(m_acc + static_cast<Acc>(logf(l)));
-        }
-    }
-
-    // ------------------------------------------------------------- merge with prefix parts
-    float out[E];
-    float lse_out = lse_t;
-#pragma unroll
-    for (int e = 0; e < E; ++e) out[e] = ot[e];
-    if (p.n_parts > 0) {
-        pdl_wait_primary();  // the partials come from the preceding prefix kernel
-        const int64_t lrow = (static_cast<int64_t>(b) * p.Hr + hl) * p.T + t;
-        const int64_t orow = ((static_cast<int64_t>(b) * p.T + t) * p.Hr + hl) * D + lane * E;
-        float mx = lse_t;
-        for (int s = lane; s < p.n_parts; s += 32) mx = fmaxf(mx, p.lse_parts[s * p.lse_part_stride + lrow]);
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-        if (mx == -INFINITY) {
-#pragma unroll
-            for (int e = 0; e < E; ++e) out[e] = 0.f;
-            lse_out = -INFINITY;
-        } else {
-            float W = 0.f, acc[E];
-            const float wt = expf(lse_t - mx);  // 0 when the tree part is a sentinel
-            W += wt;
-#pragma unroll
-            for (int e = 0; e < E; ++e) acc[e] = wt * ot[e];
-            for (int s0 = 0; s0 < p.n_parts; s0 += 32) {
-                const int s = s0 + lane;
-                const float ws = s < p.n_parts ? expf(p.lse_parts[s * p.lse_part_stride + lrow] - mx) : 0.f;
-                const int cnt = min(32, p.n_parts - s0);
-                // eight partial rows in flight per lane (the partials are L2-resident)
-                for (int u = 0; u < cnt; u += 8) {
-                    float w8[8], v8[8][E];
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        w8[k] = __shfl_sync(0xffffffffu, ws, (u + k) & 31);
-                        if (u + k < cnt) {
-                            VecIO<float, E>::load(p.o_parts + (s0 + u + k) * p.o_part_stride + orow, v8[k]);
-                        } else {
-                            w8[k] = 0.f;
-#pragma unroll
-                            for (int e = 0; e < E; ++e) v8[k][e] = 0.f;
-                        }
-                    }
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        W += w8[k];
-#pragma unroll
-                        for (int e = 0; e < E; ++e) acc[e] = fmaf(w8[k], v8[k][e], acc[e]);
-                    }
+            for (int u = 0; u < 4; ++u) {
+                if (bits) {
+                    idx[u] = c0 + __ffs(bits) - 1;
+                    bits &= bits - 1;
+                } else {
+                    idx[u] = -1;
                 }
             }
-            const float inv = 1.0f / W;
+            Acc z[4];
+            float vv[4][E];
 #pragma unroll
-            for (int e = 0; e < E; ++e) out[e] = acc[e] * inv;
-            lse_out = mx + logf(W);
+            for (int u = 0; u < 4; ++u) {
+                float kk[E];
+                const int sidx = idx[u] < 0 ? idx[0] : idx[u];
+                VecIO<Tin, E>::load(Kt + sidx * p.ts1, kk);
+                VecIO<Tin, E>::load(Vt + sidx * p.ts1, vv[u]);
+                Acc a = 0;
+#pragma unroll
+                for (int e = 0; e < E; ++e) a = fma(static_cast<Acc>(qv[e]), static_cast<Acc>(kk[e]), a);
+                z[u] = a;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) z[u] += __shfl_xor_sync(0xffffffffu, z[u], off);
+            Acc mx = m_acc;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                z[u] = idx[u] >= 0 ? z[u] * static_cast<Acc>(p.scale) : static_cast<Acc>(-INFINITY);
+                mx = z[u] > mx ? z[u] : mx;
+            }
+            const float corr = expf(static_cast<float>(m_acc - mx));
+            l *= corr;
+#pragma unroll
+            for (int e = 0; e < E; ++e) ot[e] *= corr;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float w = expf(static_cast<float>(z[u] - mx));  // 0 for unused slots
+                l += w;
+#pragma unroll
+                for (int e = 0; e < E; ++e) ot[e] = fmaf(w, vv[u][e], ot[e]);
+            }
+            m_acc = mx;
         }
     }
-
-    const int blk = hl / p.out_hb, hh = hl % p.out_hb;
-    Tout *dst = static_cast<Tout *>(p.o) + blk * p.o_block_stride + b * p.os0 + t * p.os1 + hh * p.os2 + lane * E;
-    VecIO<Tout, E>::store(dst, out);
-    if (p.lse != nullptr && lane == 0)
-        p.lse[blk * p.lse_block_stride + (static_cast<int64_t>(b) * p.out_hb + hh) * p.T + t] = lse_out;
+    if (!(l > 0.f)) return -INFINITY;
+    const float inv = 1.0f / l;
+#pragma unroll
+    for (int e = 0; e < E; ++e) ot[e] *= inv;
+    return static_cast<float>(m_acc + static_cast<Acc>(logf(l)));
 }
 
-template <typename Tin, typename Tout>
-static cudaError_t launch_tm(const TreeMergeParams &p, int d, bool pdl, cudaStream_t s) {
+// One warp per output row, R rows per warp (rows warp, warp + W, ...; W = total warps).  The
+// tree passes of all R rows run first -- with programmatic dependent launch they overlap the
+// prefix kernel, which lets this grid start early -- and the merges with the prefix partials
+// run after griddepcontrol.wait.
+template <typename Tin, typename Tout, int D, int R>
+__global__ void __launch_bounds__(128) tree_merge_kernel(const TreeMergeParams p) {
+    constexpr int E = D / 32;
+    const int nrows = p.B * p.T * p.Hr;
+    const int warp_id = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int nwarps = gridDim.x * 4;
+    const int lane = threadIdx.x & 31;
+
+    // ------------------------------------------------------------- tree pass
+    float ot[R][E], lse_t[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int row = warp_id + k * nwarps;
+        lse_t[k] = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < E; ++e) ot[k][e] = 0.f;
+        if (row < nrows && p.do_tree) {
+            const int hl = row % p.Hr, t = (row / p.Hr) % p.T, b = row / (p.Hr * p.T);
+            lse_t[k] = tree_row<Tin, D>(p, b, t, p.h0 + hl, lane, ot[k]);
+        }
+    }
+    if (p.n_parts > 0) pdl_wait_primary();  // the partials come from the preceding prefix kernel
+
+    // ------------------------------------------------------------- merge with prefix parts
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int row = warp_id + k * nwarps;
+        if (row >= nrows) break;
+        const int hl = row % p.Hr, t = (row / p.Hr) % p.T, b = row / (p.Hr * p.T);
+        float out[E];
+        float lse_out = lse_t[k];
+#pragma unroll
+        for (int e = 0; e < E; ++e) out[e] = ot[k][e];
+        if (p.n_parts > 0) {
+            const int64_t lrow = (static_cast<int64_t>(b) * p.Hr + hl) * p.T + t;
+            const int64_t orow = ((static_cast<int64_t>(b) * p.T + t) * p.Hr + hl) * D + lane * E;
+            float mx = lse_t[k];
+            for (int s = lane; s < p.n_parts; s += 32) mx = fmaxf(mx, p.lse_parts[s * p.lse_part_stride + lrow]);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            if (mx == -INFINITY) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) out[e] = 0.f;
+                lse_out = -INFINITY;
+            } else {
+                float W = 0.f, acc[E];
+                const float wt = expf(lse_t[k] - mx);  // 0 when the tree part is a sentinel
+                W += wt;
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc[e] = wt * ot[k][e];
+                for (int s0 = 0; s0 < p.n_parts; s0 += 32) {
+                    const int s = s0 + lane;
+                    const float ws = s < p.n_parts ? expf(p.lse_parts[s * p.lse_part_stride + lrow] - mx) : 0.f;
+                    const int cnt = min(32, p.n_parts - s0);
+                    // eight partial rows in flight per lane (the partials are L2-resident)
+                    for (int u = 0; u < cnt; u += 8) {
+                        float w8[8], v8[8][E];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            w8[j] = __shfl_sync(0xffffffffu, ws, (u + j) & 31);
+                            if (u + j < cnt) {
+                                VecIO<float, E>::load(p.o_parts + (s0 + u + j) * p.o_part_stride + orow, v8[j]);
+                            } else {
+                                w8[j] = 0.f;
+#pragma unroll
+                                for (int e = 0; e < E; ++e) v8[j][e] = 0.f;
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            W += w8[j];
+#pragma unroll
+                            for (int e = 0; e < E; ++e) acc[e] = fmaf(w8[j], v8[j][e], acc[e]);
+                        }
+                    }
+                }
+                const float inv = 1.0f / W;
+#pragma unroll
+                for (int e = 0; e < E; ++e) out[e] = acc[e] * inv;
+                lse_out = mx + logf(W);
+            }
+        }
+        const int blk = hl / p.out_hb, hh = hl % p.out_hb;
+        Tout *dst = static_cast<Tout *>(p.o) + blk * p.o_block_stride + b * p.os0 + t * p.os1 + hh * p.os2 + lane * E;
+        VecIO<Tout, E>::store(dst, out);
+        if (p.lse != nullptr && lane == 0)
+            p.lse[blk * p.lse_block_stride + (static_cast<int64_t>(b) * p.out_hb + hh) * p.T + t] = lse_out;
+    }
+}
+
+static int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) !=
+                                                       cudaSuccess || n <= 0)
+            n = 148;
+    }
+    return n;
+}
+
+template <typename Tin, typename Tout, int D>
+static cudaError_t launch_tm_d(const TreeMergeParams &p, bool pdl, cudaStream_t s) {
     const int rows = p.B * p.T * p.Hr;
     if (rows == 0) return cudaSuccess;
+    // with PDL the grid should fit beside the prefix kernel (one 4-warp block per SM): up to 8
+    // rows per warp; without PDL one row per warp spreads the latency-bound work widest
+#ifndef HTA_TM_RMAX
+#define HTA_TM_RMAX 1
+#endif
+    int R = 1;
+    if (pdl)
+        while (R < HTA_TM_RMAX && static_cast<int64_t>(num_sms()) * 4 * R < rows) R *= 2;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((rows + 3) / 4);
+    cfg.gridDim = dim3((rows + 4 * R - 1) / (4 * R));
     cfg.blockDim = dim3(128);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
@@ -237,14 +276,21 @@ static cudaError_t launch_tm(const TreeMergeParams &p, int d, bool pdl, cudaStre
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     cudaError_t e;
-    if (d == 128)
-        e = cudaLaunchKernelEx(&cfg, tree_merge_kernel<Tin, Tout, 128>, p);
-    else if (d == 64)
-        e = cudaLaunchKernelEx(&cfg, tree_merge_kernel<Tin, Tout, 64>, p);
-    else
-        return cudaErrorInvalidValue;
+    switch (R) {
+        case 1: e = cudaLaunchKernelEx(&cfg, tree_merge_kernel<Tin, Tout, D, 1>, p); break;
+        case 2: e = cudaLaunchKernelEx(&cfg, tree_merge_kernel<Tin, Tout, D, 2>, p); break;
+        case 4: e = cudaLaunchKernelEx(&cfg, tree_merge_kernel<Tin, Tout, D, 4>, p); break;
+        default: e = cudaLaunchKernelEx(&cfg, tree_merge_kernel<Tin, Tout, D, 8>, p); break;
+    }
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
+}
+
+template <typename Tin, typename Tout>
+static cudaError_t launch_tm(const TreeMergeParams &p, int d, bool pdl, cudaStream_t s) {
+    if (d == 128) return launch_tm_d<Tin, Tout, 128>(p, pdl, s);
+    if (d == 64) return launch_tm_d<Tin, Tout, 64>(p, pdl, s);
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_tree_merge(const TreeMergeParams &p, int d, hta_dtype_t in_dtype, hta_dtype_t out_dtype,

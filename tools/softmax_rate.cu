@@ -2,6 +2,7 @@
 // scale, exp2, row sum, pack to bf16) for different fractions of FMA-pipe polynomial exp2, with
 // 8 softmax warps per SM as in the kernel.  Registers only (no TMEM).  Build & run on the box:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude tools/softmax_rate.cu -o /tmp/sm_rate
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -12,6 +13,18 @@ using namespace hta;
 
 // EMU8: number of column pairs out of every 8 computed by the polynomial; SPREAD: poly pairs
 // spread evenly (i % 8 in {0, 3, 6}) instead of clustered ({0, 1, 2})
+// EMU8 = -1: exp2 of a pair as one MUFU ex2.approx.f16x2 (fp16 in/out), unpacked to fp32 for the
+// row sum and repacked to bf16; EMU8 = -2: same but the row sum is accumulated in f16x2.
+__device__ __forceinline__ uint32_t ex2_f16x2(uint32_t x) {
+    uint32_t y;
+    asm("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
 template <int EMU8, bool SPREAD = false>
 __global__ void __launch_bounds__(256, 1) softmax_loop(int iters, float c, float *out) {
     float s[64];
@@ -27,6 +40,24 @@ __global__ void __launch_bounds__(256, 1) softmax_loop(int iters, float c, float
         for (int i = 0; i < 32; ++i) {
             const float2 x = __ffma2_rn(s2[i], c2, neg2);
             float2 pp;
+            if (EMU8 < 0) {
+                const uint32_t e = ex2_f16x2(pack_f16x2(x.x, x.y));
+                __half2 h = *reinterpret_cast<const __half2 *>(&e);
+                if (EMU8 == -2) {
+                    __half2 a = *reinterpret_cast<__half2 *>(&sink);
+                    a = __hadd2(a, h);
+                    pp = __half22float2(h);
+                    sink ^= pack_bf16x2(pp.x, pp.y) + *reinterpret_cast<uint32_t *>(&a);
+                    continue;
+                }
+                pp = __half22float2(h);
+                if (i & 1)
+                    acc1 = __fadd2_rn(acc1, pp);
+                else
+                    acc0 = __fadd2_rn(acc0, pp);
+                sink ^= pack_bf16x2(pp.x, pp.y);
+                continue;
+            }
             const bool poly = SPREAD ? (EMU8 == 3 && ((i & 7) == 0 || (i & 7) == 3 || (i & 7) == 6))
                                      : ((i & 7) < EMU8);
             if (poly) {
@@ -67,12 +98,14 @@ void run(int threads = 256) {
     }
     // per SMSP: threads/128 warps x 64 elements x iters
     const double elems_per_smsp = threads / 128.0 * 64 * iters;
-    printf("poly %d/8%s, %d warps/SMSP: %8.1f us  -> %.2f cycles per 32-wide element slot per SMSP @1.9GHz\n", EMU8,
+    printf("mode %d/8%s, %d warps/SMSP: %8.1f us  -> %.2f cycles per 32-wide element slot per SMSP @1.9GHz\n", EMU8,
            SPREAD ? " spread" : "", threads / 128, best * 1e3, best * 1e-3 * 1.9e9 / elems_per_smsp);
 }
 
 int main() {
-    for (int t : {128, 256}) {
+    for (int t : {256, 512}) {
+        run<-1>(t);
+        run<-2>(t);
         run<0>(t);
         run<2>(t);
         run<3>(t);

@@ -31,7 +31,7 @@ def main():
     L = hta.lib()
     L.hta_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
     L.hta_debug_cta_times.argtypes = [ctypes.c_void_p]
-    buf = torch.zeros(16 * 2048, dtype=torch.int64, device=dev)
+    buf = torch.zeros(32 * 2048, dtype=torch.int64, device=dev)
     hta.hta_forward(*x, mask)
     torch.cuda.synchronize()
     assert L.hta_debug_set_trace(ctypes.c_void_p(buf.data_ptr()), cta) == 0
@@ -62,7 +62,7 @@ def main():
               f"(max {max(pro):.1f}); exit min {min(ext):.1f} median {statistics.median(ext):.1f} max {max(ext):.1f} us; "
               f"SM clock {statistics.median(mhz):.0f} MHz")
     recs = []
-    for warp, row in enumerate(buf.view(16, 2048).cpu().tolist()):
+    for warp, row in enumerate(buf.view(32, 2048).cpu().tolist()):
         for v in row:
             if v == 0:
                 break
@@ -80,52 +80,40 @@ def main():
         ev[(e, wg, j)] = c - t0
     js = sorted({k[2] for k in ev})
     print(f"{name} cta {cta}: {len(js)} KV tiles")
-    rk = 1 if cta % 2 else 0
-    print("  j | half A: Srdy   max    exp   Ppub | half B: Srdy   max    exp   Ppub | mma: Sissued PVA   PVB | tma K  V")
+    print("   j | K issued  K landed  S issued | S ready  max   exp | P all pub | V issued  V landed  P seen(PV) | K lat  V lat")
+    rows = []
     for j in js:
-        g = lambda e, w: ev.get((e, w, j), -1)
-        print(f"{j:3d} | {g(10,0):9d} {g(11,0):6d} {g(12,0):6d} {g(13,0):6d} | {g(10,1):9d} {g(11,1):6d} {g(12,1):6d} "
-              f"{g(13,1):6d} | {g(21,0):8d} {g(1,0):6d} {g(1,1):6d} | {g(30,0):7d} {g(31,0):7d}")
-    qs = [ev[(14, w, 0)] for w in range(8) if (14, w, 0) in ev]
-    if qs:
-        print(f"Q staged by softmax warps: {min(qs)}..{max(qs)}; MMA saw q_full at {ev.get((22, 0, 0), -1)}; "
-              f"first K TMA {ev.get((30, 0, 0), -1)}, first S issued {ev.get((21, 0, 0), -1)}")
-    # per-tile skew of P publication across the 8 softmax warps of this CTA (event 13, tag = warp - 2)
-    sk = []
-    for j in js:
-        ts = [ev[(13, w, j)] for w in range(8) if (13, w, j) in ev]
-        if len(ts) == 8:
-            sk.append((j, min(ts), max(ts), [t - min(ts) for t in ts]))
-    for j, a, b, rel in sk[20:26]:
-        print(f"P published tile {j}: first {a} last {b} skew {b - a}  per warp {rel}")
-    if sk:
-        print("mean P skew across warps:", statistics.mean(b - a for _, a, b, _ in sk))
-    for w in (0,):
-        d = lambda a, b: [ev[(b, w, j)] - ev[(a, w, j)] for j in js if (a, w, j) in ev and (b, w, j) in ev]
-        nxt = [ev[(10, w, j + 1)] - ev[(13, w, j)] for j in js if (13, w, j) in ev and (10, w, j + 1) in ev]
-        if d(10, 11):
-            print(f"wg{w}: ld+max {statistics.mean(d(10, 11)):.0f}  exp {statistics.mean(d(11, 12)):.0f}  "
-                  f"store+arrive {statistics.mean(d(12, 13)):.0f}  P->next S {statistics.mean(nxt) if nxt else 0:.0f}")
-    w = 0
-    seg = lambda a, b: [ev[(b, w, j)] - ev[(a, w, j)] for j in js[2:-2] if (a, w, j) in ev and (b, w, j) in ev]
-    nx = [ev[(10, w, j + 1)] - ev[(12, w, j)] for j in js[2:-2] if (12, w, j) in ev and (10, w, j + 1) in ev]
-    if seg(10, 16) and seg(16, 15):
-        print(f"warp 2 per tile: S wait->ld issued+publish {statistics.mean(seg(10, 16)):.0f}  ld wait "
-              f"{statistics.mean(seg(16, 15)):.0f}  max {statistics.mean(seg(15, 11)):.0f}  exp "
-              f"{statistics.mean(seg(11, 12)):.0f}  after exp->next S ready {statistics.mean(nx):.0f}")
-    nx19 = [ev[(19, w, j + 1)] - ev[(12, w, j)] for j in js[2:-2] if (12, w, j) in ev and (19, w, j + 1) in ev]
-    if nx19 and seg(19, 10):
-        print(f"  exp end -> loop top {statistics.mean(nx19):.0f}; try_wait(S, already complete) "
-              f"{statistics.mean(seg(19, 10)):.0f}; S ready -> publish start (fence, tail check, ld issue) "
-              f"{statistics.mean([ev[(18, w, j - 1)] - ev[(10, w, j)] for j in js if (18, w, j - 1) in ev and (10, w, j) in ev]):.0f} (incl. wait::st); "
-              f"wait::st done -> P arrive {statistics.mean([ev[(13, w, j)] - ev[(18, w, j)] for j in js if (13, w, j) in ev and (18, w, j) in ev]):.0f}")
-    rdy = [1 for j in js if (17, 1, j) in ev]
-    nrd = [1 for j in js if (17, 0, j) in ev]
-    if rdy or nrd:
-        print(f"S(j+1) already complete when exp(j) ends: {len(rdy)} of {len(rdy) + len(nrd)} tiles")
-    tiles = [ev[(10, 0, j)] for j in js if (10, 0, j) in ev]
-    if len(tiles) > 2:
-        print(f"period (wg0 S ready to S ready): {(tiles[-1] - tiles[1]) / (len(tiles) - 2):.0f} cycles")
+        g = lambda e, w=0: ev.get((e, w, j), -1)
+        pub = [ev[(13, w, j)] for w in range(16) if (13, w, j) in ev]
+        pm = max(pub) if pub else -1
+        rows.append((j, g(30), g(23), g(21), g(10), g(11), g(12), pm, g(31), g(24), g(1)))
+        print(f"{j:4d} | {g(30):8d} {g(23):8d} {g(21):8d} | {g(10):8d} {g(11)-g(10):5d} {g(12)-g(11):5d} | {pm:8d} | "
+              f"{g(31):8d} {g(24):8d} {g(1):8d} | {g(23)-g(30):5d} {g(24)-g(31):5d}")
+    mid = rows[3:-3] if len(rows) > 8 else rows
+    if len(mid) > 2:
+        per = (mid[-1][4] - mid[0][4]) / (len(mid) - 1)
+        print(f"period (S ready to S ready, middle tiles): {per:.0f} cycles")
+        wait_k = statistics.mean(max(0, r[2] - r[7 - 0] if False else 0) for r in mid)
+        kl = statistics.mean(r[2] - r[1] for r in mid)
+        vl = statistics.mean(r[9] - r[8] for r in mid)
+        print(f"mean TMA latency (issue -> MMA warp sees full): K {kl:.0f}  V {vl:.0f} cycles")
+        # what gated each PV issue: the later of V landed and P published
+        gate_p = sum(1 for r in mid if r[10] - r[9] > 50)
+        print(f"PV gated by P publication on {gate_p} of {len(mid)} tiles (else by V data)")
+        print(" warp sm  SMSP  S->max  max->exp  exp->pub(next tile)  pub lag vs earliest warp")
+        jm = [r[0] for r in mid]
+        for w in range(16):
+            a = [ev[(11, w, j)] - ev[(10, w, j)] for j in jm if (11, w, j) in ev and (10, w, j) in ev]
+            b = [ev[(12, w, j)] - ev[(11, w, j)] for j in jm if (12, w, j) in ev and (11, w, j) in ev]
+            c = [ev[(13, w, j)] - ev[(12, w, j)] for j in jm if (13, w, j) in ev and (12, w, j) in ev]
+            lag = [ev[(13, w, j)] - min(ev[(13, x, j)] for x in range(16) if (13, x, j) in ev) for j in jm
+                   if (13, w, j) in ev]
+            if a:
+                print(f"  {w:3d}  {(w + 3) % 4:3d}  {statistics.mean(a):6.0f}  {statistics.mean(b):7.0f}  "
+                      f"{statistics.mean(c) if c else 0:10.0f}  {statistics.mean(lag) if lag else 0:10.0f}")
+        sm = statistics.mean(r[5] - r[4] for r in mid)
+        se = statistics.mean(r[6] - r[5] for r in mid)
+        print(f"softmax warp 0: S ready -> max {sm:.0f}, max -> exp done {se:.0f}")
 
 
 if __name__ == "__main__":

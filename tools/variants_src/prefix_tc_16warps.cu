@@ -125,29 +125,38 @@ struct TcCfg {
     static constexpr int kSlotsV = (kRingBytes / 2) / kVBytes;
 #endif
     static constexpr int kSBufs = 384 / kBlockN;                // S/P buffers in TMEM (2 x 192 or 3 x 128)
-    static constexpr int kSoftmaxWarps = 8;                     // two per SM sub-partition
+    static constexpr int kSoftmaxWarps = 16;                    // four per SM sub-partition
     static constexpr int kFirstSoftmaxWarp = 3;                 // warp 0 K TMA, 1 MMA + TMEM, 2 V TMA
-    static constexpr int kThreads = 32 * (kFirstSoftmaxWarp + kSoftmaxWarps);
+    static constexpr int kWarps = kFirstSoftmaxWarp + kSoftmaxWarps;
+    static constexpr int kThreads = 32 * kWarps;
+    static constexpr int kCols = kBlockN / 4;                   // S columns per softmax thread (48)
+    static constexpr int kOCols = D / 4;                        // O columns per softmax thread
     static constexpr int kVOff = kQBytes + kSlotsK * kKBytes;   // start of the V ring
-    static constexpr int kBarOff = kVOff + kSlotsV * kVBytes;
+    static constexpr int kXchOff = kVOff + kSlotsV * kVBytes;   // row-max exchange [2 parity][2 half][128 rows]
+    static constexpr int kBarOff = kXchOff + 2 * 2 * kRowsPerTile * 4;
     static constexpr int kSmemBytes = kBarOff + 512;  // base is 1024-aligned (__align__ below)
     static_assert(kSlotsK >= 2 && kSlotsV >= 2, "need at least 2 slots per ring");
     static_assert(kSmemBytes <= 232448, "shared memory budget");
 };
 
-// TMEM column map: S/P buffer b at 128*b (b = 0, 1, 2), O at 384.
+// TMEM column map: S/P buffer b at kBlockN*b, O at 384 (128 fp32 columns; 512 in all).
 __device__ __forceinline__ uint32_t s_col(int buf) { return static_cast<uint32_t>(kBlockN * buf); }
-constexpr uint32_t kOCol = 384u;  // O: 128 fp32 columns after the S buffers (384 + 128 = 512)
+constexpr uint32_t kOCol = 384u;
 
-// this thread's N S values (N = 64 or 96; the other half of the warp at +N columns) and the wait
-template <int N>
+// this thread's kCols S values (half offset kCols) / kCols/2 packed P columns (half offset kCols/2)
+template <int kCols>
 __device__ __forceinline__ void tmem_ld_S(uint32_t taddr, float *v) {
-    if constexpr (N == 96) {
-        tmem_ld_x96<96>(taddr, v);
-    } else {
-        tmem_ld_x64_nowait<64>(taddr, v);
-        tmem_ld_wait_fence<64>(v);
-    }
+    if constexpr (kCols == 48)
+        tmem_ld_x48<48>(taddr, v);
+    else
+        tmem_ld_x32_wait<32>(taddr, v);
+}
+template <int kCols>
+__device__ __forceinline__ void tmem_st_P(uint32_t taddr, const uint32_t *pk) {
+    if constexpr (kCols == 48)
+        tmem_st_x24_nowait<24>(taddr, pk);
+    else
+        tmem_st_16x16_split_nowait<16>(taddr, pk);
 }
 
 template <int D, bool PAIR>
@@ -159,6 +168,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     uint8_t *sQ = smem;
     uint8_t *sK = smem + C::kQBytes;
     uint8_t *sV = smem + C::kVOff;
+    float *xch = reinterpret_cast<float *>(smem + C::kXchOff);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::kBarOff);
     uint64_t *k_full = bars;                       // [kSlotsK]  (the leader's copy is the one used)
     uint64_t *k_empty = k_full + C::kSlotsK;       // [kSlotsK]
@@ -261,6 +271,11 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     if (PAIR) cluster_sync();  // barrier inits and TMEM allocation visible to the peer
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+#if HTA_EARLY_PDL
+    // Let the dependent tree/merge grid start now: its tree pass needs nothing from this kernel
+    // and its merge waits (griddepcontrol.wait) for this grid to complete.
+    pdl_launch_dependents();
+#endif
 
     if (warp == 0) HTA_TR_CLK(50);
 #ifdef HTA_TRACE
@@ -348,10 +363,6 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             const uint64_t qd0 = sdesc_sw128(smem_u32(sQ), 16, 1024);
             const uint64_t kd0 = sdesc_sw128(smem_u32(sK), 16, 1024);
             const uint64_t vd0 = sdesc_sw128(smem_u32(sV), kBlockN * 128, 1024);
-            // One elected lane issues each group of MMAs; the descriptors are warp-uniform values
-            // computed outside the elected branch, so ptxas keeps them in uniform registers and
-            // each tcgen05.mma costs a few instructions (issue must stay well under 64 cycles per
-            // N=128 MMA, and this warp shares its sub-partition with two softmax warps).
             auto commit = [](uint64_t *bar) {
                 if (PAIR)
                     tc_commit2_mc(bar);
@@ -391,8 +402,8 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             const bool issuer = elect_one() != 0;
             // Fixed order with hardware-suspended waits (no polling: a spinning issuer would take
             // issue slots from the softmax warps sharing its SM sub-partition):
-            //   S_0, S_1, then for every j: PV_j (needs V_j and P_j), S_{j+2} (needs K_{j+2}; its
-            //   buffer was last read by PV_j, issued just before).
+            //   S_0 .. S_{B-1} (B = kSBufs), then for every j: PV_j (needs V_j and P_j), S_{j+B}
+            //   (needs K_{j+B}; its buffer was last read by PV_j, issued just before).
             constexpr bool kNoMem = HTA_SKIP >= 3;
             auto wait_all = [](uint64_t *bar, uint32_t parity) {
                 mbar_wait(bar, parity);
@@ -439,8 +450,12 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         }
         __syncwarp();
     } else {
-        // ================= softmax: warp w owns rows 32*(w%4) + 16*rh .. +15 of the tile (rh =
-        // (w-3)/4); lane t holds row (t & 15) of them, keys [96*(t>>4), 96*(t>>4) + 96)
+        // ================= softmax: 16 warps, four per TMEM lane quarter (= SM sub-partition).
+        // Warp w (k = (w - 3) / 4) owns rows 32*(w%4) + 16*(k&1) .. +15 and the key half
+        // kh = k >> 1 of every tile (kBlockN/2 columns); lane t holds row (t & 15) of them, keys
+        // [kBlockN/2*kh + kCols*(t>>4), +kCols) with kCols = kBlockN/4.  A row is thus shared by four threads in two warps of the same
+        // sub-partition: the row max is combined with one shuffle and, between the two warps, an
+        // exchange through shared memory at a 64-thread named barrier.
         const int sw = warp - C::kFirstSoftmaxWarp;
         if (!p.q_tma) {  // this CTA's 128 Q rows -> smem in the canonical K-major SWIZZLE_128B
             // layout (G does not divide 128: no TMA box), staged by the softmax warps
@@ -482,28 +497,33 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             }
         }
         const int quarter = warp & 3;
-        const int rh = sw >> 2;
-        const int chalf = lane >> 4;
-        const int r = quarter * 32 + rh * 16 + (lane & 15);
+        const int kq = sw >> 2;
+        const int rh = kq & 1;                   // row half of the quarter
+        const int kh = kq >> 1;                  // key half of the tile
+        const int chalf = lane >> 4;             // key quarter within the half
+        const int rloc = rh * 16 + (lane & 15);  // row within the quarter
+        const int r = quarter * 32 + rloc;
         const int grow = row0 + r;
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32 + rh * 16) << 16;
+        const uint32_t xbar = 1u + static_cast<uint32_t>(quarter * 2 + rh);  // named barrier of the warp pair
+        const int kcol0 = kh * (kBlockN / 2) + chalf * C::kCols;             // this thread's first key
         const float c = p.scale_log2;
         const uint32_t pfull0 = PAIR ? mapa_shared(smem_u32(&p_full[0]), 0) : 0u;
-        constexpr int kHalfCols = kBlockN / 2;
-        float m_run = -INFINITY, l_run = 0.f;  // l_run: this thread's 64 columns only
+        float m_run = -INFINITY, l_run = 0.f;  // l_run: this thread's columns only
         // Publish P_jp (stored to TMEM without waiting): wait for the stores (and any O rescale
         // of that tile), sanitise the garbage V rows of the last tile, signal the MMA warp.
         auto publish = [&](int jp) {
             tmem_st_wait();
             if (jp == n_tiles - 1 && tail_zero) {
-                // V rows (keys) past the sequence end: zero this CTA's part of key row r (may be
-                // NaN); the thread pair of row r splits the row's 16-byte chunks
-                for (int kr = r; kr < kBlockN; kr += kRowsPerTile) {  // key rows r and r + 128
+                // V rows (keys) past the sequence end: zero this CTA's part of key rows r and
+                // r + 128; the four threads of row r split the row's 16-byte chunks
+                for (int kr = r; kr < kBlockN; kr += kRowsPerTile) {
                     if (kr < tail_valid) continue;
                     uint8_t *vrow = sV + ((n_tiles - 1) % C::kSlotsV) * C::kVBytes + kr * 128;
                     constexpr int kChunks16 = C::kVCols * 2 / 16;  // 16-byte chunks in this CTA's row
+                    const int qi = kh * 2 + chalf;
 #pragma unroll
-                    for (int cch = chalf * (kChunks16 / 2); cch < (chalf + 1) * (kChunks16 / 2); ++cch)
+                    for (int cch = qi * (kChunks16 / 4); cch < (qi + 1) * (kChunks16 / 4); ++cch)
                         *reinterpret_cast<uint4 *>(vrow + (cch / 8) * (kBlockN * 128) + (cch % 8) * 16) =
                             make_uint4(0u, 0u, 0u, 0u);
                 }
@@ -525,8 +545,13 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         // Deferred publication: P_{j-1} is published once S_j is ready, just before S_j is loaded,
         // so the completion of P_{j-1}'s stores is waited for a tile later (long done) instead of
         // right after the exponentials, on each tile's critical path.  No deadlock: S_j needs only
-        // P_{j-2}, published at the start of tile j-1.
+        // P_{j-kSBufs}, published at the start of tile j-kSBufs+1.
         constexpr bool kDefer = HTA_DEFER != 0;
+        if (HTA_PHASE > 0 && rh == 1) {  // diagnostics: start one warp pair per sub-partition late
+            const long long t0 = clock64();
+            while (clock64() - t0 < HTA_PHASE) {
+            }
+        }
         for (int j = 0; j < n_tiles; ++j) {
             const int buf = j % C::kSBufs;
             mbar_wait(&s_full[buf], static_cast<uint32_t>((j / C::kSBufs) & 1));
@@ -535,30 +560,48 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             const bool last = j == n_tiles - 1;
             float mt = 0.f, lsum = 0.f;
             if (HTA_SKIP < 1 || HTA_SKIP == 4) {
-                float s[kHalfCols];  // this thread's S values: keys [kHalfCols*chalf, +kHalfCols)
+                float s[C::kCols];  // this thread's S values: keys [kcol0, kcol0 + kCols)
                 if (kDefer && j > 0) publish(j - 1);
-                tmem_ld_S<kHalfCols>(tmem + lane_off + s_col(buf), s);
+                tmem_ld_S<C::kCols>(tmem + lane_off + s_col(buf) + kh * (kBlockN / 2), s);
                 if (last && tail_valid < kBlockN) {
                     // keys past the split end -> -inf (last tile only; the empty asm keeps this a
                     // real branch instead of per-element selects on every tile)
                     asm volatile("" ::: "memory");
-                    const int lim = tail_valid - chalf * kHalfCols;  // this thread's first invalid column
+                    const int lim = tail_valid - kcol0;  // this thread's first invalid column
 #pragma unroll
-                    for (int cc = 0; cc < kHalfCols; ++cc)
+                    for (int cc = 0; cc < C::kCols; ++cc)
                         if (cc >= lim) s[cc] = -INFINITY;
                 }
-                // P = exp2(S*c - m) -> bf16 over S in TMEM; returns this thread's row sum.  3 of
-                // every 8 column pairs use the FMA-pipe polynomial, the rest MUFU ex2 (MUFU alone
-                // would co-limit the MMAs).  P packed (2 bf16 per column): keys [Ch, Ch + C) ->
-                // columns [Ch/2, Ch/2 + C/2) (C = kHalfCols, h = chalf), stored in 16-column
-                // chunks without waiting (one wait::st before P is published).
-                auto exp_store = [&](float m_use) {
-                    const float2 c2 = make_float2(c, c), neg2 = make_float2(-m_use, -m_use);
+                // row max over this thread's values, its lane pair's and the partner warp's
+                float mx;
+                {
+                    float mx0 = fmaxf(s[0], s[1]), mx1 = fmaxf(s[2], s[3]);
+#pragma unroll
+                    for (int cc = 4; cc < C::kCols; cc += 4) {
+                        mx0 = fmaxf(mx0, fmaxf(s[cc], s[cc + 1]));
+                        mx1 = fmaxf(mx1, fmaxf(s[cc + 2], s[cc + 3]));
+                    }
+                    mx = fmaxf(mx0, mx1);
+                    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+                    float *xrow = xch + (j & 1) * (2 * kRowsPerTile);
+                    if (chalf == 0) xrow[kh * kRowsPerTile + r] = mx;
+                    named_bar_sync(xbar, 64);
+                    mx = fmaxf(mx, xrow[(kh ^ 1) * kRowsPerTile + r]) * c;
+                }
+                HTA_TR(11, sw, j);
+                mt = (mx > m_run + 8.0f) ? mx : m_run;  // stale max: rescale only on a jump > 2^8
+                // P = exp2(S*c - m) -> bf16 over S in TMEM; 3 of every 8 column pairs use the
+                // FMA-pipe polynomial, the rest MUFU ex2 (MUFU alone would co-limit the MMAs).
+                // P packed (2 bf16 per column): keys [kcol0, kcol0 + kCols) -> columns
+                // [kcol0/2, kcol0/2 + kCols/2), stored without waiting (one wait::st before P is
+                // published).
+                {
+                    const float2 c2 = make_float2(c, c), neg2 = make_float2(-mt, -mt);
                     float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
                     const float2 *s2 = reinterpret_cast<const float2 *>(s);
-                    uint32_t pk[16];
+                    uint32_t pk[C::kCols / 2];
 #pragma unroll
-                    for (int i = 0; i < kHalfCols / 2; ++i) {
+                    for (int i = 0; i < C::kCols / 2; ++i) {
                         const float2 x = __ffma2_rn(s2[i], c2, neg2);
                         float2 pp;
                         if ((i & 7) < HTA_POLY) {
@@ -571,33 +614,11 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                             acc1 = __fadd2_rn(acc1, pp);
                         else
                             acc0 = __fadd2_rn(acc0, pp);
-                        pk[i & 15] = pack_bf16x2(pp.x, pp.y);
-                        if ((i & 15) == 15)
-                            tmem_st_16x16_split_nowait<kHalfCols / 2>(tmem + lane_off + s_col(buf) + (i - 15), pk);
+                        pk[i] = pack_bf16x2(pp.x, pp.y);
                     }
-                    return (acc0.x + acc1.x) + (acc0.y + acc1.y);
-                };
-                auto row_max = [&]() {  // max over the row (this thread's values and its pair's)
-                    float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
-#pragma unroll
-                    for (int cc = 4; cc + 8 <= kHalfCols; cc += 8) {
-                        mx0 = fmaxf(mx0, fmaxf(s[cc], s[cc + 4]));
-                        mx1 = fmaxf(mx1, fmaxf(s[cc + 1], s[cc + 5]));
-                        mx2 = fmaxf(mx2, fmaxf(s[cc + 2], s[cc + 6]));
-                        mx3 = fmaxf(mx3, fmaxf(s[cc + 3], s[cc + 7]));
-                    }
-                    static_assert(kHalfCols % 8 == 0, "4 + 8k + 4 columns");
-                    mx0 = fmaxf(mx0, s[kHalfCols - 4]);
-                    mx1 = fmaxf(mx1, s[kHalfCols - 3]);
-                    mx2 = fmaxf(mx2, s[kHalfCols - 2]);
-                    mx3 = fmaxf(mx3, s[kHalfCols - 1]);
-                    const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-                    return fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16)) * c;
-                };
-                const float mx = row_max();
-                HTA_TR(11, sw, j);
-                mt = (mx > m_run + 8.0f) ? mx : m_run;  // stale max: rescale only on a jump > 2^8
-                lsum = exp_store(mt);
+                    tmem_st_P<C::kCols>(tmem + lane_off + s_col(buf) + kh * (kBlockN / 4), pk);
+                    lsum = (acc0.x + acc1.x) + (acc0.y + acc1.y);
+                }
             } else {
                 if (kDefer && j > 0) publish(j - 1);
                 mt = 0.f;
@@ -605,33 +626,38 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             }
             HTA_TR(12, sw, j);
             // Rescale O only when the running max moved.  O must then hold P_{j-1} V_{j-1} first:
-            // wait for PV_{j-1} on its own barrier pv_done[(j-1) % 2].  That barrier cannot run a
+            // wait for PV_{j-1} on its own barrier pv_done[(j-1) % kSBufs].  That barrier cannot run a
             // phase ahead (PV_{j+1} needs P_{j+1}, not yet published), so the parity wait is exact
-            // although most tiles never wait.
+            // although most tiles never wait.  The four threads of a row rescale a quarter each.
             const bool need = (j > 0) && (mt != m_run);
             const float f = need ? fast_exp2(m_run - mt) : 1.0f;
             l_run = l_run * f + lsum;
             if (__any_sync(0xffffffffu, need)) {
                 mbar_wait(&pv_done[(j - 1) % C::kSBufs], static_cast<uint32_t>(((j - 1) / C::kSBufs) & 1));
                 tc_fence_after();
-#pragma unroll 1
-                for (int ch = 0; ch < D / 2; ch += 32) {  // this thread's D/2 columns of the O row
-                    float o[32];
-                    tmem_ld_16x32_split<D / 2>(tmem + lane_off + kOCol + ch, o);
+                float o[C::kOCols];
+                tmem_ld_o<C::kOCols>(tmem + lane_off + kOCol + kh * (D / 2), o);
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) o[e] *= f;
-                    tmem_st_16x32_split<D / 2>(tmem + lane_off + kOCol + ch, *reinterpret_cast<uint32_t(*)[32]>(o));
-                }
+                for (int e = 0; e < C::kOCols; ++e) o[e] *= f;
+                tmem_st_o<C::kOCols>(tmem + lane_off + kOCol + kh * (D / 2), o);
             }
             m_run = mt;
             if (!kDefer) publish(j);
         }
         if (kDefer && n_tiles > 0) publish(n_tiles - 1);
-        // ---- epilogue: the thread pair of a row adds its two partial row sums
+        // ---- epilogue: the four threads of a row add their partial row sums
+        float l_tot = l_run + __shfl_xor_sync(0xffffffffu, l_run, 16);
+        {
+            float *xrow = xch + (n_tiles & 1) * (2 * kRowsPerTile);
+            if (chalf == 0) xrow[kh * kRowsPerTile + r] = l_tot;
+            named_bar_sync(xbar, 64);
+            l_tot += xrow[(kh ^ 1) * kRowsPerTile + r];
+        }
         mbar_wait(o_final, 0);
         tc_fence_after();
+#if !HTA_EARLY_PDL
         pdl_launch_dependents();
-        const float l_tot = l_run + __shfl_xor_sync(0xffffffffu, l_run, 16);
+#endif
         const float inv = 1.0f / l_tot;
         const bool row_ok = grow < p.M;
         int t = 0, h = 0;
@@ -639,19 +665,16 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             t = grow / p.G;
             h = g * p.G + grow % p.G;
         }
-        float *dst = o_base + ((static_cast<int64_t>(b) * p.T + t) * p.H + h) * D + chalf * (D / 2);
+        float o[C::kOCols];
+        tmem_ld_o<C::kOCols>(tmem + lane_off + kOCol + kh * (D / 2), o);
+        if (row_ok) {
+            float *dst = o_base + ((static_cast<int64_t>(b) * p.T + t) * p.H + h) * D + kh * (D / 2) + chalf * C::kOCols;
 #pragma unroll
-        for (int ch = 0; ch < D / 2; ch += 32) {
-            float o[32];
-            tmem_ld_16x32_split<D / 2>(tmem + lane_off + kOCol + ch, o);
-            if (row_ok) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    reinterpret_cast<float4 *>(dst + ch)[e] =
-                        make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
-            }
+            for (int e = 0; e < C::kOCols / 4; ++e)
+                reinterpret_cast<float4 *>(dst)[e] =
+                    make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
         }
-        if (row_ok && chalf == 0)
+        if (row_ok && chalf == 0 && kh == 0)
             lse_base[(static_cast<int64_t>(b) * p.H + h) * p.T + t] = (m_run + log2f(l_tot)) * 0.69314718055994530942f;
     }
 
