@@ -12,6 +12,7 @@
 #include <cstring>
 
 #include "hta_internal.h"
+#include "ptx_sm100.cuh"
 
 namespace hta {
 
@@ -35,6 +36,9 @@ __global__ void __launch_bounds__(256) build_mask_kernel(const int32_t *__restri
                                                          uint8_t *__restrict__ mask) {
     __shared__ int32_t par[256];
     const int i = threadIdx.x;
+    // the next kernel (hta_forward's prefix pass, which needs no mask) may start its prologue now;
+    // whoever reads the mask does so after griddepcontrol.wait
+    pdl_launch_dependents();
     if (i < T) par[i] = parents[i];  // one coalesced load; the chain walks below hit smem
     __syncthreads();
     if (i >= T) return;

@@ -138,11 +138,14 @@ def _num_sms(dev) -> int:
     return torch.cuda.get_device_properties(dev).multi_processor_count
 
 
+def new_workspace(shape: hta_shape_t, device) -> torch.Tensor:
+    """A (zero-filled) workspace for hta_forward / hta_prefix_attn of this shape."""
+    return torch.zeros(max(workspace_size(shape, _num_sms(device)), 16), dtype=torch.uint8, device=device)
+
+
 def _workspace(shape: hta_shape_t, device, ws: Optional[torch.Tensor]) -> torch.Tensor:
-    n = workspace_size(shape, _num_sms(device))
-    if ws is None or ws.numel() * ws.element_size() < n:
-        ws = torch.empty(max(n, 16), dtype=torch.uint8, device=device)
-    return ws
+    """The caller's workspace as given (libhta checks its size), else a new zero-filled one."""
+    return new_workspace(shape, device) if ws is None else ws
 
 
 def _out_like_q(q: torch.Tensor, o: Optional[torch.Tensor]) -> torch.Tensor:
@@ -168,7 +171,7 @@ def hta_prefix_attn(q, k_cache, v_cache, cache_seqlens=None, o_part=None, lse_pa
     ws = _workspace(shape, q.device, ws)
     _check("hta_prefix_attn", lib().hta_prefix_attn(ctypes.byref(shape), _ptr(q), _ptr(k_cache), _ptr(v_cache),
                                                     _ptr(cache_seqlens), _ptr(o_part), _ptr(lse_part), _ptr(ws),
-                                                    ws.numel(), _stream(stream)))
+                                                    ws.numel() * ws.element_size(), _stream(stream)))
     return o_part, lse_part
 
 
@@ -218,12 +221,12 @@ def hta_forward(q, k_cache, v_cache, k_tree, v_tree, mask, cache_seqlens=None, o
     if events is None:
         _check("hta_forward", lib().hta_forward(ctypes.byref(shape), _ptr(q), _ptr(k_cache), _ptr(v_cache),
                                                 _ptr(cache_seqlens), _ptr(k_tree), _ptr(v_tree), _ptr(mask), mbs,
-                                                _ptr(o), _ptr(lse_out), _ptr(ws), ws.numel(), _stream(stream)))
+                                                _ptr(o), _ptr(lse_out), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
     else:
         ev0, ev1 = (ctypes.c_void_p(e.cuda_event) for e in events)
         _check("hta_forward_timed", lib().hta_forward_timed(
             ctypes.byref(shape), _ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(cache_seqlens), _ptr(k_tree),
-            _ptr(v_tree), _ptr(mask), mbs, _ptr(o), _ptr(lse_out), _ptr(ws), ws.numel(), _stream(stream), ev0, ev1))
+            _ptr(v_tree), _ptr(mask), mbs, _ptr(o), _ptr(lse_out), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream), ev0, ev1))
     return o, lse_out
 
 
@@ -322,7 +325,7 @@ class HtaComm:
         _check("hta_forward_seqpar", lib().hta_forward_seqpar(
             self.handle, ctypes.byref(shape), _ptr(q), _ptr(k_cache_local), _ptr(v_cache_local),
             _ptr(cache_seqlens_local), _ptr(k_tree), _ptr(v_tree), _ptr(mask), mbs, _ptr(o), _ptr(lse_out),
-            1 if gather_output else 0, _ptr(ws), ws.numel(), _stream(stream)))
+            1 if gather_output else 0, _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
         return o, lse_out
 
 

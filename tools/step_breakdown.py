@@ -31,7 +31,7 @@ def main():
     mask = hta.hta_build_tree_mask(parents)
     o, lse = hta.hta_forward(x["q"], x["k_cache"], x["v_cache"], x["k_tree"], x["v_tree"], mask)
     shape = hta.make_shape(x["q"], k_cache=x["k_cache"], k_tree=x["k_tree"])
-    wsb = torch.empty(hta.workspace_size(shape, 148), dtype=torch.uint8, device=dev)
+    wsb = hta.new_workspace(shape, dev)
     path = torch.empty(T, dtype=torch.int32, device=dev)
     plen = torch.empty(1, dtype=torch.int32, device=dev)
     bonus = torch.empty(1, dtype=torch.int32, device=dev)

@@ -38,6 +38,7 @@
 
 #include "hta_internal.h"
 #include "ptx_sm100.cuh"
+#include "tree_pass.cuh"
 
 namespace hta {
 
@@ -46,7 +47,7 @@ namespace hta {
 #ifdef HTA_TRACE
 __device__ unsigned long long *g_trace = nullptr;
 __device__ int g_trace_cta = 0;
-__device__ unsigned long long g_cta_times[1024][4];  // per CTA: entry ns, loop start ns/clk, exit ns, exit clk
+__device__ unsigned long long g_cta_times[1024][8];  // per CTA: entry ns, loop start ns, clk, exit ns, epilogue start ns, merge start ns, merge end ns
 constexpr int kTraceRecs = 2048;  // per warp, written straight to g_trace (traced CTA only)
 #define HTA_TR(ev, tag, jj)                                                                              \
     do {                                                                                                 \
@@ -88,6 +89,9 @@ __device__ __forceinline__ uint64_t trace_globaltimer() {
 #define HTA_SKIP 0
 #endif
 // Pairs of every 8 whose exp2 runs on the FMA pipe (polynomial) instead of MUFU.
+#ifndef HTA_FUSED_PDL
+#define HTA_FUSED_PDL 0
+#endif
 #ifndef HTA_RING_KB
 #define HTA_RING_KB 192
 #endif
@@ -150,6 +154,99 @@ __device__ __forceinline__ void tmem_ld_S(uint32_t taddr, float *v) {
     }
 }
 
+
+// ------------------------------------------------------------------ fused epilogue
+// Rows [lo, hi) (row r of KV head g: t = r / G, h = g*G + r % G) of this CTA's (b, g, row group)
+// that it merges in the fused epilogue: the group's rows split evenly over its CTAs.
+template <bool PAIR>
+__device__ __forceinline__ void merge_slice(const PrefixParams &p, int mg, int split, uint32_t rank, int &lo,
+                                            int &hi) {
+    const int n_grp = p.splits * (PAIR ? 2 : 1);
+    const int k = split * (PAIR ? 2 : 1) + static_cast<int>(rank);
+    const int rows = PAIR ? 2 * kRowsPerTile : kRowsPerTile;
+    const int r0 = mg * rows;
+    const int R = min(rows, p.M - r0);
+    lo = r0 + k * R / n_grp;
+    hi = r0 + (k + 1) * R / n_grp;
+}
+
+// The merge of one row of the fused epilogue: its tree partial from tree_o / tree_lse, then
+// merge_row.
+template <typename Tout, int D>
+__device__ __forceinline__ void merge_row_ool(const TreeMergeParams &p, int b, int t, int h, int lane,
+                                           const float *tree_o, const float *tree_lse) {
+    constexpr int E = D / 32;
+    float ot[E];
+    float lt = -INFINITY;
+    if (p.do_tree) {
+        load_cg<E>(tree_o + ((static_cast<int64_t>(b) * p.T + t) * p.H + h) * D + lane * E, ot);
+        lt = __ldcg(tree_lse + (static_cast<int64_t>(b) * p.H + h) * p.T + t);
+    } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) ot[e] = 0.f;
+    }
+    merge_row<Tout, D, true>(p, b, t, h, lane, ot, lt);
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int *ptr) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+    return v;
+}
+
+// All threads of the CTA, after its split partial is written: arrive at the group's counter,
+// wait for the group's other CTAs (co-resident: the host launches this path only when the whole
+// grid fits on the GPU at once) and for the tree-pass grid, merge rows [lo, hi) -- the S split
+// partials and the tree partial (n-ary, max-shifted) -- into the output, and
+// leave; the group's last CTA to leave resets the counters for the next launch.
+template <int D, bool PAIR, int kWarps>
+__device__ void fused_epilogue(const PrefixParams &p, int b, int g, int mg, int split, uint32_t rank) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int lo, hi;
+    merge_slice<PAIR>(p, mg, split, rank, lo, hi);
+    int *cnt = p.sync + 2 * ((b * p.H_kv + g) * p.n_mgroups + mg);
+    const int n_grp = p.splits * (PAIR ? 2 : 1);
+#ifdef HTA_TRACE
+    if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_times[blockIdx.x][4] = trace_globaltimer();
+#endif
+    __threadfence();  // this thread's partial stores, device-wide, before the arrival below
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(cnt, 1);
+    if (threadIdx.x == 0) {
+        uint32_t polls = 0;
+        while (ld_acquire_gpu(cnt) < n_grp) {
+            __nanosleep(100);
+            if (++polls > (1u << 26)) {
+                printf("hta: fused merge wait timeout (block %d, group counter %d of %d)\n", blockIdx.x,
+                       ld_acquire_gpu(cnt), n_grp);
+                __trap();
+            }
+        }
+    }
+    __syncthreads();
+    // the tree partials come from the tree-pass kernel launched just before this one (a no-op
+    // unless this grid was launched with programmatic dependent launch, HTA_FUSED_PDL)
+    pdl_wait_primary();
+#ifdef HTA_TRACE
+    if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_times[blockIdx.x][5] = trace_globaltimer();
+#endif
+    for (int r = lo + warp; r < hi; r += kWarps) {
+        const int t = r / p.G, h = g * p.G + r % p.G;
+        if (p.out_dtype == HTA_BF16)
+            merge_row_ool<__nv_bfloat16, D>(p.tm, b, t, h, lane, p.tree_o, p.tree_lse);
+        else
+            merge_row_ool<float, D>(p.tm, b, t, h, lane, p.tree_o, p.tree_lse);
+    }
+    __syncthreads();
+#ifdef HTA_TRACE
+    if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_times[blockIdx.x][6] = trace_globaltimer();
+#endif
+    if (threadIdx.x == 0 && atomicAdd(cnt + 1, 1) == n_grp - 1) {
+        cnt[0] = 0;  // every CTA of the group is past its wait: reset for the next launch
+        cnt[1] = 0;
+    }
+}
+
 template <int D, bool PAIR>
 __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     prefix_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
@@ -192,8 +289,38 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     rest /= p.splits;
     const int g = rest % p.H_kv;
     const int b = rest / p.H_kv;
-    // ---- one-time setup (reads no input: it overlaps the previous kernel under programmatic
-    // dependent launch)
+    int64_t n_b = p.N_max;
+    if (p.seqlens != nullptr) {
+        n_b = p.seqlens[b];
+        n_b = n_b < 0 ? 0 : (n_b > p.N_max ? p.N_max : n_b);
+    }
+    const int64_t key_lo = static_cast<int64_t>(split) * p.tiles_per_split * kBlockN;
+    int64_t key_hi = key_lo + static_cast<int64_t>(p.tiles_per_split) * kBlockN;
+    if (key_hi > n_b) key_hi = n_b;
+    const int n_tiles = key_hi > key_lo ? static_cast<int>((key_hi - key_lo + kBlockN - 1) / kBlockN) : 0;
+    const int row0 = mg * kRowsPerTile * (PAIR ? 2 : 1) + static_cast<int>(rank) * kRowsPerTile;
+    // the last tile of a split that ends at the sequence end may hold garbage rows (Z13)
+    const int tail_valid = static_cast<int>(key_hi - (key_lo + static_cast<int64_t>(n_tiles - 1) * kBlockN));
+    const bool tail_zero = n_tiles > 0 && tail_valid < kBlockN && key_hi == n_b && n_b < p.N_max;
+
+    float *o_base = p.o_out + static_cast<int64_t>(split) * p.o_split_stride;
+    float *lse_base = p.lse_out + static_cast<int64_t>(split) * p.lse_split_stride;
+
+    if (n_tiles == 0) {  // empty split: sentinel rows (both CTAs of a pair take this branch)
+        for (int r = threadIdx.x; r < kRowsPerTile; r += blockDim.x) {
+            const int grow = row0 + r;
+            if (grow >= p.M) continue;
+            const int t = grow / p.G, h = g * p.G + grow % p.G;
+            float4 *dst = reinterpret_cast<float4 *>(o_base + ((static_cast<int64_t>(b) * p.T + t) * p.H + h) * D);
+#pragma unroll
+            for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+            lse_base[(static_cast<int64_t>(b) * p.H + h) * p.T + t] = -INFINITY;
+        }
+        if (p.fused) fused_epilogue<D, PAIR, C::kFirstSoftmaxWarp + C::kSoftmaxWarps>(p, b, g, mg, split, rank);
+        return;
+    }
+
+    // ---- one-time setup
     if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0u) __trap();  // swizzle atoms need 1 KiB alignment
     if (warp == 0 && lane == 0) {
         if (p.q_tma) tma_prefetch_desc(&tmap_q);
@@ -233,29 +360,6 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    // Inputs (q, K/V, seqlens) may come from the kernel before this one on the stream: wait for it
-    // (griddepcontrol.wait; a no-op unless it triggered this grid's launch early, as the tree-mask
-    // kernel does).  The tree/merge kernel after this one reads the mask after its own wait.
-    pdl_wait_primary();
-
-    int64_t n_b = p.N_max;
-    if (p.seqlens != nullptr) {
-        n_b = p.seqlens[b];
-        n_b = n_b < 0 ? 0 : (n_b > p.N_max ? p.N_max : n_b);
-    }
-    const int64_t key_lo = static_cast<int64_t>(split) * p.tiles_per_split * kBlockN;
-    int64_t key_hi = key_lo + static_cast<int64_t>(p.tiles_per_split) * kBlockN;
-    if (key_hi > n_b) key_hi = n_b;
-    const int n_tiles = key_hi > key_lo ? static_cast<int>((key_hi - key_lo + kBlockN - 1) / kBlockN) : 0;
-    const int row0 = mg * kRowsPerTile * (PAIR ? 2 : 1) + static_cast<int>(rank) * kRowsPerTile;
-    // the last tile of a split that ends at the sequence end may hold garbage rows (Z13)
-    const int tail_valid = static_cast<int>(key_hi - (key_lo + static_cast<int64_t>(n_tiles - 1) * kBlockN));
-    const bool tail_zero = n_tiles > 0 && tail_valid < kBlockN && key_hi == n_b && n_b < p.N_max;
-
-    float *o_base = p.o_out + static_cast<int64_t>(split) * p.o_split_stride;
-    float *lse_base = p.lse_out + static_cast<int64_t>(split) * p.lse_split_stride;
-
-
     if (warp == 0) HTA_TR_CLK(50);
 #ifdef HTA_TRACE
     if (threadIdx.x == 0 && blockIdx.x < 1024) {
@@ -263,17 +367,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         g_cta_times[blockIdx.x][2] = clock64();
     }
 #endif
-    if (n_tiles == 0) {  // empty split: sentinel rows (both CTAs of a pair take this branch)
-        for (int r = threadIdx.x; r < kRowsPerTile; r += blockDim.x) {
-            const int grow = row0 + r;
-            if (grow >= p.M) continue;
-            const int t = grow / p.G, h = g * p.G + grow % p.G;
-            float4 *dst = reinterpret_cast<float4 *>(o_base + ((static_cast<int64_t>(b) * p.T + t) * p.H + h) * D);
-#pragma unroll
-            for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-            lse_base[(static_cast<int64_t>(b) * p.H + h) * p.T + t] = -INFINITY;
-        }
-    } else if (warp == 0) {
+    if (warp == 0) {
         // ================= TMA producer of Q and the K ring (K_j is consumed by S_j).  K and V
         // have producers of their own, so K tiles run ahead of V tiles by as many slots as the
         // K ring has (S_j frees K_j long before PV_j frees V_j).
@@ -676,6 +770,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         else
             tmem_dealloc(tmem, 512);
     }
+    if (p.fused) fused_epilogue<D, PAIR, C::kFirstSoftmaxWarp + C::kSoftmaxWarps>(p, b, g, mg, split, rank);
 }
 
 #ifdef HTA_TRACE
@@ -705,15 +800,58 @@ static cudaError_t launch_tc(const PrefixParams &p, const CUtensorMap &tq, const
     attr[0].val.clusterDim.x = PAIR ? 2 : 1;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    // programmatic dependent launch: the prologue (barriers, TMEM, descriptor prefetch) overlaps
-    // the previous kernel when it allows it (griddepcontrol.wait guards every input read)
+    // fused forward: start while the tree-pass kernel (one warp per SM) is still running
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = (HTA_FUSED_PDL && p.fused) ? 2 : 1;
     e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, p);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
+}
+
+// Can every CTA of a grid of `ctas` CTAs be resident at once (one per SM; pairs as clusters)?
+// The fused epilogue waits for the other CTAs of a group, so it needs that.
+template <int D, bool PAIR>
+static bool coresident(int ctas) {
+    using C = TcCfg<D, PAIR>;
+    static int max_units = -1;  // max co-resident clusters (PAIR) or CTAs
+    if (max_units < 0) {
+        auto kern = prefix_tc_kernel<D, PAIR>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
+            return false;
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (PAIR) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(2 * sms);
+            cfg.blockDim = dim3(C::kThreads);
+            cfg.dynamicSmemBytes = C::kSmemBytes;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int n = 0;
+            max_units = cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess ? n : 0;
+        } else {
+            int per_sm = 0;
+            max_units = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::kThreads, C::kSmemBytes) ==
+                                cudaSuccess
+                            ? per_sm * sms
+                            : 0;
+        }
+        cudaGetLastError();
+    }
+    return (PAIR ? ctas / 2 : ctas) <= max_units;
+}
+
+bool prefix_tc_coresident(int d, int nt, int ctas) {
+    if (d == 128) return nt == 2 ? coresident<128, true>(ctas) : coresident<128, false>(ctas);
+    return coresident<64, false>(ctas);
 }
 
 int prefix_tc_smem_bytes(int d, int nt) {
