@@ -6,8 +6,10 @@
 A step is one pass of the whole hot path for one layer, on seeded synthetic
 inputs shaped like BASELINE.json's workload: a0 tree mask from the parent array (device), a1-a4
 prefix pass + tree pass + LSE merge (hta_forward; hta_forward_seqpar for N > 1, which adds a5,
-the NCCL exchange of head-sliced partials), a6 greedy accepted path (device).  Inputs live in
-HBM; the L2 is flushed (a 512 MiB write) before every timed step and the flush is not timed.
+the NCCL exchange of head-sliced partials), a6 greedy accepted path (device; it needs only the
+tree and the target argmax, so it runs on a forked stream beside a0-a4).  On one GPU the step is
+captured once as a CUDA graph and replayed.  Inputs live in HBM; the L2 is flushed before every
+timed step (a 512 MiB write, then a read of it) and the flush is not timed.
 Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
@@ -105,6 +107,21 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+def packed(specs, device):
+    """One byte buffer (pinned if on the host) holding a tensor per {name: (shape, dtype)} at
+    256-byte aligned offsets; returns (buffer, {name: view})."""
+    offs, total = {}, 0
+    for k, (shape, dt) in specs.items():
+        n = math.prod(shape) * torch.tensor([], dtype=dt).element_size()
+        offs[k] = (total, n)
+        total += (n + 255) // 256 * 256
+    buf = torch.zeros(total, dtype=torch.uint8, device=device)
+    if buf.device.type == "cpu":
+        buf = buf.pin_memory()
+    views = {k: buf[a:a + n].view(specs[k][1]).view(specs[k][0]) for k, (a, n) in offs.items()}
+    return buf, views
 
 
 def created_events(n):
@@ -212,36 +229,45 @@ def main():
     sl = torch.clamp(w.seqlens - lo, 0, hi - lo).to(torch.int32).to(dev)
     parents_h = w.parents[0].contiguous()
     draft_h, tgt_h, ctx = accept_tokens(parents_h, seed=0, vocab=32000, p_match=0.8)
-    host = {"q": w.q.pin_memory(), "kt": w.k_tree.pin_memory(), "vt": w.v_tree.pin_memory(),
-            "parents": parents_h.pin_memory(), "draft": draft_h.pin_memory(), "tgt": tgt_h.pin_memory()}
-    d_in = {k: v.to(dev) for k, v in host.items()}
+    src = {"q": w.q, "kt": w.k_tree, "vt": w.v_tree, "parents": parents_h, "draft": draft_h, "tgt": tgt_h}
+    # per-step inputs packed in one pinned staging buffer (one H2D copy per end-to-end step)
+    host_buf, host = packed({k: (v.shape, v.dtype) for k, v in src.items()}, "cpu")
+    for k, v in src.items():
+        host[k].copy_(v)
+    d_in = {k: v.to(dev) for k, v in src.items()}
     T = w.T
     mask = torch.empty(T, T, dtype=torch.uint8, device=dev)
     Hx = w.H // ws
-    o = torch.empty(w.B, T, Hx, w.d, dtype=w.torch_dtype, device=dev)
+    # outputs of the step packed in one device buffer (one D2H copy per end-to-end step)
+    out_buf, out = packed({"o": ((w.B, T, Hx, w.d), w.torch_dtype), "path": ((T,), torch.int32),
+                           "plen": ((1,), torch.int32), "bonus": ((1,), torch.int32)}, dev)
+    o, path, plen, bonus = out["o"], out["path"], out["plen"], out["bonus"]
     lse = torch.empty(w.B, Hx, T, dtype=torch.float32, device=dev)
-    path = torch.empty(T, dtype=torch.int32, device=dev)
-    plen = torch.empty(1, dtype=torch.int32, device=dev)
-    bonus = torch.empty(1, dtype=torch.int32, device=dev)
     shape = hta.make_shape(d_in["q"], k_cache=kc, k_tree=d_in["kt"])
     if ws > 1:
         wsb = torch.empty(comm.workspace_size(shape), dtype=torch.uint8, device=dev)
     else:
-        wsb = torch.empty(hta.workspace_size(shape, torch.cuda.get_device_properties(dev).multi_processor_count),
-                          dtype=torch.uint8, device=dev)
+        wsb = hta.new_workspace(shape, dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
-    o_host = torch.empty(o.shape, dtype=o.dtype).pin_memory()
-    res_host = torch.empty(T + 2, dtype=torch.int32).pin_memory()
+    out_host = torch.empty(out_buf.numel(), dtype=torch.uint8).pin_memory()
+
+    side = torch.cuda.Stream(device=dev)
 
     def step(x, events=None):
+        """One verification step: a0 -> a1..a4 (a5) on the current stream; a6 (independent of
+        the attention: it needs only the tree and the target's argmax) on a forked stream."""
+        cur = torch.cuda.current_stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            hta.hta_accept_greedy(x["parents"], x["draft"], x["tgt"], root=0, context_argmax=ctx,
+                                  path=path, path_len=plen, bonus=bonus)                    # a6
         hta.hta_build_tree_mask(x["parents"], mask)                                         # a0
         if ws > 1:                                                                          # a1-a5
             comm.forward(x["q"], kc, vc, x["kt"], x["vt"], mask, cache_seqlens_local=sl, o=o, lse_out=lse, ws=wsb)
         else:                                                                               # a1-a4
             hta.hta_forward(x["q"], kc, vc, x["kt"], x["vt"], mask, cache_seqlens=sl, o=o, lse_out=lse, ws=wsb,
                             events=events)
-        hta.hta_accept_greedy(x["parents"], x["draft"], x["tgt"], root=0, context_argmax=ctx,
-                              path=path, path_len=plen, bonus=bonus)                        # a6
+        cur.wait_stream(side)
 
     launches_per_step = 4 if ws == 1 else 5
 
@@ -254,13 +280,45 @@ def main():
         step(d_in)
     torch.cuda.synchronize()
 
+    # The step and the end-to-end step (H2D of the step's inputs from pinned memory, the step,
+    # D2H of O and the accepted path) are captured once as CUDA graphs and replayed.
+    def e2e_body():
+        e2e_buf.copy_(host_buf, non_blocking=True)
+        step(e2e_in)
+        out_host.copy_(out_buf, non_blocking=True)
+
+    e2e_buf, e2e_in = packed({k: (v.shape, v.dtype) for k, v in src.items()}, dev)
+    graphs = {}
+    if ws == 1:  # (NCCL calls of the sequence-parallel step are issued eagerly)
+        for name, fn in (("step", lambda: step(d_in)), ("e2e", e2e_body)):
+            cs = torch.cuda.Stream(device=dev)
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cs):
+                fn()
+            torch.cuda.current_stream().wait_stream(cs)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            graphs[name] = g
+        for _ in range(args.warmup):
+            graphs["step"].replay()
+            graphs["e2e"].replay()
+        torch.cuda.synchronize()
+    run_step = graphs["step"].replay if "step" in graphs else (lambda: step(d_in))
+    run_e2e = graphs["e2e"].replay if "e2e" in graphs else e2e_body
+    flush32 = flush.view(torch.float32)
+
     def timed(fn, K):
-        """Per-step CUDA-event times (ms) of K steps; L2 flushed (untimed) before each."""
+        """Per-step CUDA-event times (ms) of K steps; L2 flushed (untimed) before each: a 512 MiB
+        write, then a read of it, so that the write-back of the flush's own dirty lines is not
+        charged to the step."""
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         barrier()
         torch.cuda.synchronize()
         for i in range(K):
             flush.fill_(i & 0xFF)
+            flush32.sum()
             evs[i][0].record()
             fn(i)
             evs[i][1].record()
@@ -276,8 +334,8 @@ def main():
         return float(t.item())
 
     with ClockSampler(local) as clk:
-        # (1) device-resident step
-        times = timed(lambda i: step(d_in), args.steps)
+        # (1) device-resident step (graph replay)
+        times = timed(lambda i: run_step(), args.steps)
         # (2) dominant kernel (prefix pass) timed on its own launch stream with CUDA events
         if ws == 1:
             ev = created_events(2 * args.steps)
@@ -286,23 +344,15 @@ def main():
             prefix_ms = statistics.mean(a.elapsed_time(b) for a, b in pev)
         else:
             prefix_ms = None
-
         # (3) end to end through the public API: per-step inputs H2D from pinned host memory,
         # result (O + accepted path) D2H; the KV cache is resident model state.
-        def e2e_step(i):
-            x = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
-            step(x)
-            o_host.copy_(o, non_blocking=True)
-            res_host[:T].copy_(path, non_blocking=True)
-            res_host[T:T + 1].copy_(plen, non_blocking=True)
-            res_host[T + 1:].copy_(bonus, non_blocking=True)
-        e2e_times = timed(e2e_step, args.steps)
+        e2e_times = timed(lambda i: run_e2e(), args.steps)
     clocks = clk.summary()
 
     t_ms = max_over_ranks(statistics.mean(times))
     e2e_ms = max_over_ranks(statistics.mean(e2e_times))
-    h2d = sum(v.numel() * v.element_size() for v in host.values())
-    d2h = o_host.numel() * o_host.element_size() + res_host.numel() * 4
+    h2d = host_buf.numel()
+    d2h = out_host.numel()
 
     # roofline of the dominant kernel (per launch = per step, this rank's KV slice)
     n_keys = hi - lo
@@ -341,13 +391,16 @@ def main():
         "scaling": "strong" if ws > 1 else "strong", "vs_baseline": None, "dtype": cfg["dtype"],
         "data": "synthetic (seeded; value distribution V1 sink+local; beam-search tree)",
         "config": {"workload": args.workload, "B": w.B, "T": T, "H": w.H, "H_kv": w.H_kv, "d": w.d, "N": w.N,
-                   "parallelism": f"seq{ws}", "l2": "flushed (512 MiB write) before every timed step",
-                   "step": "a0 mask + hta_forward (a1-a4) + accept (a6)" + (" + NCCL exchange (a5)" if ws > 1 else "")},
+                   "parallelism": f"seq{ws}",
+                   "l2": "flushed before every timed step (512 MiB write, then a read of it; untimed)",
+                   "step": ("a0 mask + hta_forward (a1-a4) | accept (a6) on a forked stream"
+                            + (" + NCCL exchange (a5)" if ws > 1 else "; CUDA graph replay"))},
         "clocks": clocks,
         "gpu_launches": launches_per_step * args.steps,
         "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                "note": "per-step inputs (q, tree K/V, parents, draft/target tokens) H2D; KV cache resident"},
+                "note": ("per-step inputs (q, tree K/V, parents, draft/target tokens) H2D as one copy from a pinned "
+                         "staging buffer, O + accepted path D2H as one copy; KV cache resident; CUDA graph")},
         "roofline": roof,
     }
 
@@ -383,8 +436,7 @@ def bench_config(name, dev, flush, k=10):
     mask = hta.hta_build_tree_mask(x["parents"])
     o, lse = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask)
     shape = hta.make_shape(x["q"], k_cache=x["kc"], k_tree=x["kt"])
-    wsb = torch.empty(hta.workspace_size(shape, torch.cuda.get_device_properties(dev).multi_processor_count),
-                      dtype=torch.uint8, device=dev)
+    wsb = hta.new_workspace(shape, dev)
     ts, tp = [], []
     for i in range(k + 3):
         e = created_events(4)

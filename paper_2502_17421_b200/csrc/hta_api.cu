@@ -99,7 +99,8 @@ PrefixPlan make_plan(const Shape &sh, int num_sms) {
         pl.n_mgroups = 1;
         pl.units = (s.B * s.T * s.H + 3) / 4;  // SIMT: 4 rows per block
     }
-    pl.n_tiles = static_cast<int>((s.N_max + kBlockN - 1) / kBlockN);
+    const int blk = s.dtype == HTA_BF16 ? kBlockN : kSimtBlock;
+    pl.n_tiles = static_cast<int>((s.N_max + blk - 1) / blk);
     int S;
     if (s.num_splits > 0) {
         S = s.num_splits;

@@ -16,6 +16,7 @@ namespace hta {
 // 3 x 128 columns) and the 128-column O accumulator (512 columns in all).
 constexpr int kBlockN = HTA_BLOCK_N;
 static_assert(kBlockN == 128 || kBlockN == 192, "KV tile of 128 or 192 keys");
+constexpr int kSimtBlock = 32;   // key block (split granularity) of the fp32 SIMT prefix pass
 constexpr int kRowsPerTile = 128;  // rows of one tcgen05 M=128 tile
 
 // Work decomposition of the prefix pass.
@@ -25,7 +26,7 @@ struct PrefixPlan {
     int nt;           // M tiles (of 128 rows) per CTA: 1 or 2
     int n_mgroups;    // ceil(M / (128 * nt))
     int units;        // B * H_kv * n_mgroups
-    int n_tiles;      // ceil(N_max / kBlockN)
+    int n_tiles;      // ceil(N_max / kBlockN) (bf16) or ceil(N_max / kSimtBlock) (fp32)
     int tiles_per_split;
     int splits;       // S
 };

@@ -32,8 +32,8 @@ __global__ void __launch_bounds__(128) prefix_simt_kernel(const PrefixParams p) 
         n_b = p.seqlens[b];
         n_b = n_b < 0 ? 0 : (n_b > p.N_max ? p.N_max : n_b);
     }
-    const int64_t lo = static_cast<int64_t>(split) * p.tiles_per_split * kBlockN;
-    int64_t hi = lo + static_cast<int64_t>(p.tiles_per_split) * kBlockN;
+    const int64_t lo = static_cast<int64_t>(split) * p.tiles_per_split * kSimtBlock;
+    int64_t hi = lo + static_cast<int64_t>(p.tiles_per_split) * kSimtBlock;
     if (hi > n_b) hi = n_b;
 
     const float *q = static_cast<const float *>(p.q) + b * p.qs0 + t * p.qs1 + h * p.qs2 + lane * E;
@@ -48,15 +48,23 @@ __global__ void __launch_bounds__(128) prefix_simt_kernel(const PrefixParams p) 
     double m = -INFINITY;
     float l = 0.f;
     for (int64_t j = lo; j < hi; j += U) {
+        // the K and V rows of U keys in flight at once: one round trip per U keys
+        float kk[U][E], vv[U][E];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t jj = j + u < hi ? j + u : j;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                kk[u][e] = K[jj * p.ks1 + e];
+                vv[u][e] = V[jj * p.ks1 + e];
+            }
+        }
         double z[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             double acc = 0.0;
-            if (j + u < hi) {
-                const float *k = K + (j + u) * p.ks1;
 #pragma unroll
-                for (int e = 0; e < E; ++e) acc = fma(static_cast<double>(qv[e]), static_cast<double>(k[e]), acc);
-            }
+            for (int e = 0; e < E; ++e) acc = fma(static_cast<double>(qv[e]), static_cast<double>(kk[u][e]), acc);
             z[u] = acc;
         }
 #pragma unroll
@@ -75,13 +83,10 @@ __global__ void __launch_bounds__(128) prefix_simt_kernel(const PrefixParams p) 
         for (int e = 0; e < E; ++e) o[e] *= corr;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if (j + u < hi) {
-                const float w = expf(static_cast<float>(z[u] - mx));
-                l += w;
-                const float *v = V + (j + u) * p.ks1;
+            const float w = (j + u < hi) ? expf(static_cast<float>(z[u] - mx)) : 0.f;
+            l += w;
 #pragma unroll
-                for (int e = 0; e < E; ++e) o[e] = fmaf(w, v[e], o[e]);
-            }
+            for (int e = 0; e < E; ++e) o[e] = fmaf(w, vv[u][e], o[e]);
         }
         m = mx;
     }
