@@ -1,0 +1,40 @@
+"""hta_forward_seqpar on the GPU with a one-rank NCCL communicator (the only world size a single
+B200 allows): the local split-KV pass combined into one destination-major partial, the NCCL
+exchange (self copy), and the final merge with the tree pass -- vs the fp64 oracle, with and
+without the output all-gather.  The P = 2 data flow is covered on CPU by test_seqpar_gloo.py."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2502_17421_b200 import hta
+from workloads import make_workload
+
+from gpu_util import compare, oracle_masks, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def comm(cuda_device):
+    try:
+        c = hta.HtaComm(0, 1)
+    except hta.HtaError as e:
+        pytest.fail(f"NCCL communicator: {e}")
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("gather", [False, True])
+@pytest.mark.parametrize("case", [(1, 64, 32, 8, 128, 3000, "beam"), (2, 13, 8, 2, 128, 1000, "random"),
+                                  (1, 9, 6, 2, 64, 700, "star")])
+def test_seqpar_one_rank_vs_oracle(cuda_device, comm, case, gather):
+    B, T, H, Hkv, d, N, tree = case
+    w = make_workload(B, T, H, Hkv, d, N, "bf16", dist="V1", seed=5, tree=tree)
+    mask = oracle_masks(w)
+    x = to_dev(w, cuda_device)
+    o_ref, l_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask, seqlens=w.seqlens)
+    o, l = comm.forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], torch.from_numpy(mask).to(cuda_device),
+                        cache_seqlens_local=x["sl"], gather_output=gather)
+    torch.cuda.synchronize()
+    compare(o, l, o_ref, l_ref, "bf16", f"seqpar P=1 gather={gather}")
