@@ -83,47 +83,65 @@ int device_sms() {
     return sms;
 }
 
+// Makespan model of the split-KV schedule: waves(S) x (tiles per split + a fixed per-CTA cost of
+// ~3 tiles for prologue and epilogue), with a 1%-per-split penalty for the partials each split
+// adds (wave quantisation over the SMs, 1 CTA per SM).  Measured on B200: LongChat-16k is faster
+// as one wave of 4 splits than as two waves of 9 (tools/split_sweep.py).  Returns the best S.
+int best_splits(int ctas, int n_tiles, int num_sms, double *cost_out) {
+    const int smax = std::max(1, std::min(n_tiles, 4 * num_sms / ctas + 1));
+    double best = 1e30;
+    int S = 1;
+    for (int c = 1; c <= smax; ++c) {
+        const int waves = (ctas * c + num_sms - 1) / num_sms;
+        const int per = (n_tiles + c - 1) / c;
+        const double cost = double(waves) * (per + 3) * (1.0 + 0.01 * c);
+        if (cost < best - 1e-12) {
+            best = cost;
+            S = c;
+        }
+    }
+    *cost_out = best;
+    return S;
+}
+
 // Split-KV work plan.
 PrefixPlan make_plan(const Shape &sh, int num_sms) {
     const hta_shape_t &s = sh.s;
     PrefixPlan pl{};
     pl.G = sh.G;
     pl.M = s.T * sh.G;
+    const int blk = s.dtype == HTA_BF16 ? kBlockN : kSimtBlock;
+    pl.n_tiles = static_cast<int>((s.N_max + blk - 1) / blk);
+    int S = 1;
     if (s.dtype == HTA_BF16) {
-        // More than 128 rows per KV head: CTA pairs (cta_group::2, 256 rows per pair).
-        pl.nt = (pl.M > 128 && s.d == 128) ? 2 : 1;
+        // More than 128 rows per KV head: CTA pairs (cta_group::2, 256 rows per pair), unless
+        // single-CTA 128-row groups pack the rows tighter into a shorter schedule (G = 5, T = 64:
+        // 320 rows = 2.5 x 128 fill 3 single groups at 83 % but 2 pair groups at 63 %).
+        auto layout = [&](int nt, int *S_out) {
+            const int mg = (pl.M + 128 * nt - 1) / (128 * nt);
+            const int ctas = s.B * s.H_kv * mg * nt;  // CTAs per split (a pair is two CTAs, two SMs)
+            double cost = 0.0;
+            *S_out = s.num_splits > 0 ? s.num_splits : best_splits(ctas, std::max(pl.n_tiles, 1), num_sms, &cost);
+            return cost;
+        };
+        int S1 = 1, S2 = 1;
+        const double c1 = layout(1, &S1);
+        pl.nt = 1;
+        S = S1;
+        if (pl.M > 128 && s.d == 128) {
+            const double c2 = layout(2, &S2);
+            if (s.num_splits > 0 || c2 <= c1) {
+                pl.nt = 2;
+                S = S2;
+            }
+        }
         pl.n_mgroups = (pl.M + 128 * pl.nt - 1) / (128 * pl.nt);
         pl.units = s.B * s.H_kv * pl.n_mgroups;
     } else {
         pl.nt = 1;
         pl.n_mgroups = 1;
         pl.units = (s.B * s.T * s.H + 3) / 4;  // SIMT: 4 rows per block
-    }
-    const int blk = s.dtype == HTA_BF16 ? kBlockN : kSimtBlock;
-    pl.n_tiles = static_cast<int>((s.N_max + blk - 1) / blk);
-    int S;
-    if (s.num_splits > 0) {
-        S = s.num_splits;
-    } else if (s.dtype == HTA_BF16) {
-        // Shortest makespan: waves(S) x (tiles per split + a fixed per-CTA cost of ~3 tiles for
-        // prologue and epilogue), with a 1%-per-split penalty for the partials each split adds
-        // (wave quantisation over the SMs, 1 CTA per SM).  Measured on B200: LongChat-16k is
-        // faster as one wave of 4 splits than as two waves of 9 (tools/split_sweep.py).
-        const int ctas = pl.units * pl.nt;  // CTAs per split (a pair is two CTAs, two SMs)
-        const int smax = std::max(1, std::min(pl.n_tiles, 4 * num_sms / ctas + 1));
-        double best = 1e30;
-        S = 1;
-        for (int c = 1; c <= smax; ++c) {
-            const int waves = (ctas * c + num_sms - 1) / num_sms;
-            const int per = (pl.n_tiles + c - 1) / c;
-            const double cost = double(waves) * (per + 3) * (1.0 + 0.01 * c);
-            if (cost < best - 1e-12) {
-                best = cost;
-                S = c;
-            }
-        }
-    } else {
-        S = (4 * num_sms + pl.units - 1) / pl.units;
+        S = s.num_splits > 0 ? s.num_splits : (4 * num_sms + pl.units - 1) / pl.units;
     }
     if (S < 1) S = 1;
     if (pl.n_tiles > 0 && S > pl.n_tiles) S = pl.n_tiles;

@@ -16,7 +16,7 @@ namespace hta {
 // 3 x 128 columns) and the 128-column O accumulator (512 columns in all).
 constexpr int kBlockN = HTA_BLOCK_N;
 static_assert(kBlockN == 128 || kBlockN == 192, "KV tile of 128 or 192 keys");
-constexpr int kSimtBlock = 32;   // key block (split granularity) of the fp32 SIMT prefix pass
+constexpr int kSimtBlock = 16;   // key block (split granularity) of the fp32 SIMT prefix pass
 constexpr int kRowsPerTile = 128;  // rows of one tcgen05 M=128 tile
 
 // Work decomposition of the prefix pass.

@@ -16,7 +16,7 @@ namespace hta {
 template <int D>
 __global__ void __launch_bounds__(128) prefix_simt_kernel(const PrefixParams p) {
     constexpr int E = D / 32;
-    constexpr int U = 8;
+    constexpr int U = 16;  // keys in flight per round trip (= kSimtBlock: one round trip per split block)
     const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     pdl_launch_dependents();  // the dependent tree/merge grid may start its tree pass now
