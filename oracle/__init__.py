@@ -10,8 +10,9 @@ Contents
   merge(parts)       the LSE aggregation of PAPER.md:203-219 (max-shifted, reading Z11).
   tree_mask(...)     ancestor mask by recursive set walk (oracle/tree.py).
   accept_greedy(...) longest accepted root path by brute-force enumeration (oracle/tree.py).
+  commit_kv(...)     append the accepted nodes' K/V rows to the cache in path order (oracle/tree.py).
 
 Parity status of each function is recorded in DESIGN.md "Oracle pins".
 """
 from .attention import attention, merge, load_library, build_library  # noqa: F401
-from .tree import tree_mask, accept_greedy  # noqa: F401
+from .tree import tree_mask, accept_greedy, commit_kv  # noqa: F401

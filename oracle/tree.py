@@ -13,6 +13,11 @@ accept_greedy  PAPER.md:190 (the target verifies the tree "without altering the 
                argmax at its parent; ties -> lexicographically smallest node-index sequence;
                bonus = target argmax at the path's last node.  Computed by brute force over
                every node's root path.
+commit_kv      PAPER.md:172 ("the large model only updates its KV cache upon verification
+               completion") and SPEC commit_kv: the cache is extended by exactly
+               the accepted nodes' K/V rows in path order; rejected rows are discarded.
+               Plain row-by-row copy.  Rows that would land at or beyond N_max are dropped
+               (the committed length saturates at N_max: reading Z18).
 """
 from __future__ import annotations
 
@@ -91,3 +96,32 @@ def accept_greedy(parents, draft_tokens, target_argmax, root: int = 0,
     best_len = max(len(p) for p in candidates)
     best = min(p for p in candidates if len(p) == best_len)  # lexicographic on index lists
     return best, int(tgt[best[-1]])
+
+
+def commit_kv(k_cache, v_cache, seqlens, k_tree, v_tree, paths, path_lens):
+    """(k_cache', v_cache', seqlens') after appending, for every batch b, the tree K/V rows of
+    nodes paths[b][0 .. path_lens[b]) at cache positions seqlens[b], seqlens[b] + 1, ...
+
+    k_cache/v_cache [B, N, H_kv, d]; k_tree/v_tree [B, T, H_kv, d]; seqlens [B]; paths [B][>= len];
+    path_lens [B].  Inputs are not modified (numpy copies are returned).
+    """
+    kc = np.array(k_cache, copy=True)
+    vc = np.array(v_cache, copy=True)
+    kt = np.asarray(k_tree)
+    vt = np.asarray(v_tree)
+    B, N = kc.shape[0], kc.shape[1]
+    T = kt.shape[1]
+    out_len = []
+    for b in range(B):
+        n = int(seqlens[b])
+        L = int(path_lens[b])
+        path = [int(x) for x in paths[b][:L]]
+        for i, node in enumerate(path):
+            if not 0 <= node < T:
+                raise ValueError(f"path node {node} outside [0, {T})")
+            if n + i >= N:
+                break
+            kc[b, n + i] = kt[b, node]
+            vc[b, n + i] = vt[b, node]
+        out_len.append(min(n + L, N))
+    return kc, vc, np.asarray(out_len, np.int64)
