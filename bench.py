@@ -404,6 +404,30 @@ def main():
         "roofline": roof,
     }
 
+    # ---- commit of the accepted path's K/V rows into the cache (device, after
+    # a6), timed on its own (L2 flushed); measured after the step timings since it writes rows
+    # of the (then no longer used) cache
+    if ws == 1:
+        sl_commit = torch.full((w.B,), max(0, (hi - lo) - T), dtype=torch.int32, device=dev)
+        out_sl = torch.empty_like(sl_commit)
+        ct = []
+        for i in range(args.warmup + args.steps):
+            flush.fill_(i & 0xFF)
+            flush32.sum()
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            hta.hta_commit_kv(path, plen, d_in["kt"], d_in["vt"], kc, vc, sl_commit, seqlens_out=out_sl)
+            b_.record()
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                ct.append(a.elapsed_time(b_) * 1e3)
+        rows = int(plen.item())
+        esz = 2 if cfg["dtype"] == "bf16" else 4
+        line["next_rows"] = {"f1_commit_kv": {
+            "us": statistics.mean(ct), "rows": rows, "bytes": 2 * 2 * rows * w.H_kv * w.d * esz,
+            "note": "accepted path of the step's tree (device accept -> commit, no host sync); latency-bound "
+                    "(one CTA per batch entry)"}}
+
     # ---- cpu baseline (rank 0, N = 1 only): the oracle as it stands, bounded sample
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         import oracle

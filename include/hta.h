@@ -186,6 +186,26 @@ hta_status_t hta_accept_greedy(const int32_t *parents, const int32_t *draft_toke
                                int32_t context_argmax, int32_t *path, int32_t *path_len,
                                int32_t *bonus, int32_t on_device, hta_stream_t stream);
 
+/* commit_kv ("the large model only updates its KV cache upon
+ * verification completion"): append the accepted tree nodes' K/V rows to the cache, in path
+ * order, on the device (no host round trip between acceptance and the next step).
+ *   shape        B, T, H_kv, d, N_max, dtype, kv_strides (cache), tkv_strides (tree) as above
+ *   path         device int32 [B][path_stride]: accepted node indices (rows of k_tree / v_tree)
+ *                in path order, e.g. hta_accept_greedy's `path` (path_stride = T)
+ *   path_len     device int32 [B]: accepted nodes of batch b (<= 0: nothing to commit)
+ *   k_tree, v_tree  [B, T, H_kv, d] (read);  k_cache, v_cache [B, N_max, H_kv, d] (written at
+ *                rows cache_seqlens[b] ... cache_seqlens[b] + path_len[b] - 1 only)
+ *   cache_seqlens   device int32 [B]: committed length n_b before the call (read)
+ *   seqlens_out     device int32 [B]: n_b + the rows written (may be cache_seqlens itself: the
+ *                update is made after the copies).  Rows that would land at or beyond N_max, and
+ *                everything from the first node index outside [0, T) on, are not written and not
+ *                counted (reading Z18).
+ * Enqueued on `stream`; one CTA per batch entry.  Host-checkable errors as for hta_forward. */
+hta_status_t hta_commit_kv(const hta_shape_t *shape, const int32_t *path, int64_t path_stride,
+                           const int32_t *path_len, const void *k_tree, const void *v_tree,
+                           void *k_cache, void *v_cache, const int32_t *cache_seqlens,
+                           int32_t *seqlens_out, hta_stream_t stream);
+
 /* ---------------------------------------------------------------- sequence parallel
  * The prefix KV is split contiguously along the sequence across P ranks (one process per
  * GPU); rank r holds KV[:, r*N/P : (r+1)*N/P].  Each rank runs the prefix pass on its slice,

@@ -490,6 +490,37 @@ hta_status_t hta_validate_tree_mask(const uint8_t *mask, int32_t T) {
     return HTA_OK;
 }
 
+hta_status_t hta_commit_kv(const hta_shape_t *shape, const int32_t *path, int64_t path_stride,
+                           const int32_t *path_len, const void *k_tree, const void *v_tree, void *k_cache,
+                           void *v_cache, const int32_t *cache_seqlens, int32_t *seqlens_out, hta_stream_t stream) {
+    Shape sh;
+    hta_status_t r = check_shape(shape, &sh);
+    if (r != HTA_OK) return r;
+    const hta_shape_t &s = sh.s;
+    if (!path || !path_len || !k_tree || !v_tree || !k_cache || !v_cache || !cache_seqlens || !seqlens_out)
+        return HTA_ERR_INVALID_ARGUMENT;
+    if (path_stride < s.T) return HTA_ERR_INVALID_ARGUMENT;
+    if (!is_aligned(k_tree, 16) || !is_aligned(v_tree, 16) || !is_aligned(k_cache, 16) || !is_aligned(v_cache, 16))
+        return HTA_ERR_INVALID_ARGUMENT;
+    if ((r = check_device()) != HTA_OK) return r;
+    CommitGeom gm;
+    gm.T = s.T;
+    gm.H_kv = s.H_kv;
+    gm.esize = static_cast<int>(sh.esize);
+    gm.row_bytes = static_cast<int>(s.d * sh.esize);
+    gm.N_max = s.N_max;
+    gm.ks0 = s.kv_strides[0];
+    gm.ks1 = s.kv_strides[1];
+    gm.ks2 = s.kv_strides[2];
+    gm.ts0 = s.tkv_strides[0];
+    gm.ts1 = s.tkv_strides[1];
+    gm.ts2 = s.tkv_strides[2];
+    return launch_commit_kv(path, path_stride, path_len, k_tree, v_tree, k_cache, v_cache, cache_seqlens, seqlens_out,
+                            gm, s.B, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? HTA_OK
+               : HTA_ERR_CUDA;
+}
+
 hta_status_t hta_accept_greedy(const int32_t *parents, const int32_t *draft_tokens, const int32_t *target_argmax,
                                int32_t T, int32_t root, int32_t context_argmax, int32_t *path, int32_t *path_len,
                                int32_t *bonus, int32_t on_device, hta_stream_t stream) {

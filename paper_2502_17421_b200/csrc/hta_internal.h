@@ -80,6 +80,16 @@ int prefix_tc_smem_bytes(int d, int nt);
 cudaError_t launch_prefix_simt(const PrefixParams &p, cudaStream_t s);
 cudaError_t launch_tree_merge(const TreeMergeParams &p, int d, hta_dtype_t in_dtype, hta_dtype_t out_dtype,
                               bool pdl, cudaStream_t s);
+// Geometry of hta_commit_kv (element strides; esize bytes per element).
+struct CommitGeom {
+    int T, H_kv, row_bytes, esize;
+    int64_t N_max;
+    int64_t ks0, ks1, ks2;  // cache [B, N, H_kv]
+    int64_t ts0, ts1, ts2;  // tree  [B, T, H_kv]
+};
+cudaError_t launch_commit_kv(const int32_t *path, int64_t path_stride, const int32_t *path_len, const void *kt,
+                             const void *vt, void *kc, void *vc, const int32_t *seqlens, int32_t *seqlens_out,
+                             const CommitGeom &gm, int B, cudaStream_t s);
 cudaError_t launch_build_mask(const int32_t *parents, int T, uint8_t *mask, cudaStream_t s);
 cudaError_t launch_accept(const int32_t *parents, const int32_t *draft, const int32_t *tgt, int T, int root,
                           int ctx, int32_t *path, int32_t *path_len, int32_t *bonus, cudaStream_t s);

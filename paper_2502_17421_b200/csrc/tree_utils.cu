@@ -263,4 +263,59 @@ cudaError_t launch_accept(const int32_t *parents, const int32_t *draft, const in
     return cudaGetLastError();
 }
 
+// ----------------------------------------------------------------------------- commit
+
+// One CTA per batch entry b: path_len[b] rows of H_kv * d elements each (K and V) copied as
+// 16-byte chunks by all threads, then the committed length updated by thread 0 after a barrier
+// (so seqlens_out may alias cache_seqlens).
+__global__ void __launch_bounds__(256) commit_kv_kernel(const int32_t *__restrict__ path, int64_t path_stride,
+                                                        const int32_t *__restrict__ path_len, const uint8_t *kt,
+                                                        const uint8_t *vt, uint8_t *kc, uint8_t *vc,
+                                                        const int32_t *seqlens, int32_t *seqlens_out, CommitGeom gm) {
+    const int b = blockIdx.x;
+    __shared__ int s_rows;
+    __shared__ int s_node[256];
+    __shared__ int64_t s_n;
+    // every load at once (one round trip): the path entries, the committed length, the path length
+    if (threadIdx.x < gm.T) s_node[threadIdx.x] = path[b * path_stride + threadIdx.x];
+    if (threadIdx.x == 0) {
+        s_n = seqlens[b];
+        s_rows = path_len[b];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int L = s_rows > 0 ? s_rows : 0;
+        if (L > gm.T) L = gm.T;
+        int rows = 0;
+        while (rows < L && s_n + rows < gm.N_max && s_node[rows] >= 0 && s_node[rows] < gm.T)
+            ++rows;  // stop at N_max or at the first invalid node
+        s_rows = rows;
+    }
+    __syncthreads();
+    const int rows = s_rows;
+    const int64_t n = s_n;
+    const int chunks = gm.row_bytes / 16;  // per head: d * esize / 16
+    for (int idx = threadIdx.x; idx < rows * gm.H_kv * chunks; idx += blockDim.x) {
+        const int c = idx % chunks;
+        const int hh = (idx / chunks) % gm.H_kv;
+        const int i = idx / (chunks * gm.H_kv);
+        const int node = s_node[i];
+        const int64_t src = (b * gm.ts0 + node * gm.ts1 + hh * gm.ts2) * gm.esize + c * 16;
+        const int64_t dst = (b * gm.ks0 + (n + i) * gm.ks1 + hh * gm.ks2) * gm.esize + c * 16;
+        *reinterpret_cast<uint4 *>(kc + dst) = *reinterpret_cast<const uint4 *>(kt + src);
+        *reinterpret_cast<uint4 *>(vc + dst) = *reinterpret_cast<const uint4 *>(vt + src);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) seqlens_out[b] = static_cast<int32_t>(n + rows);
+}
+
+cudaError_t launch_commit_kv(const int32_t *path, int64_t path_stride, const int32_t *path_len, const void *kt,
+                             const void *vt, void *kc, void *vc, const int32_t *seqlens, int32_t *seqlens_out,
+                             const CommitGeom &gm, int B, cudaStream_t s) {
+    commit_kv_kernel<<<B, 256, 0, s>>>(path, path_stride, path_len, static_cast<const uint8_t *>(kt),
+                                       static_cast<const uint8_t *>(vt), static_cast<uint8_t *>(kc),
+                                       static_cast<uint8_t *>(vc), seqlens, seqlens_out, gm);
+    return cudaGetLastError();
+}
+
 }  // namespace hta

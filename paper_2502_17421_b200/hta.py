@@ -51,6 +51,7 @@ _SIG = {
     "hta_validate_tree_mask": (ctypes.c_int, [_P, ctypes.c_int32]),
     "hta_accept_greedy": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _P,
                                          ctypes.c_int32, _P]),
+    "hta_commit_kv": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, ctypes.c_int64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hta_comm_unique_id": (ctypes.c_int, [_P]),
     "hta_comm_create": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]),
     "hta_comm_destroy": (ctypes.c_int, [_P]),
@@ -272,6 +273,32 @@ def hta_accept_greedy(parents, draft_tokens, target_argmax, root: int = 0, conte
         return path, path_len, bonus
     n = int(path_len[0])
     return [int(x) for x in path[:n].tolist()], int(bonus[0])
+
+
+def hta_commit_kv(path, path_len, k_tree, v_tree, k_cache, v_cache, cache_seqlens, seqlens_out=None,
+                  stream=None):
+    """Append the accepted tree K/V rows to the cache in path order (device, in place).
+    path int32 [B, >= T] (or [T] for B = 1), path_len int32 [B] (or [1]); returns seqlens_out
+    (int32 [B], a new tensor unless given; may be cache_seqlens itself)."""
+    B, T, Hkv, d = k_tree.shape
+    s = hta_shape_t()
+    s.B, s.T, s.H, s.H_kv, s.d = B, T, Hkv, Hkv, d
+    s.N_max = k_cache.shape[1]
+    s.softmax_scale = 1.0
+    s.dtype = _dtype_code(k_tree.dtype)
+    s.q_strides = (ctypes.c_int64 * 3)(T * Hkv * d, Hkv * d, d)
+    s.kv_strides = _strides3(k_cache)
+    s.tkv_strides = _strides3(k_tree)
+    path = path.to(torch.int32).reshape(B, -1)
+    if path.stride(-1) != 1:
+        path = path.contiguous()
+    if seqlens_out is None:
+        seqlens_out = torch.empty(B, dtype=torch.int32, device=k_cache.device)
+    _check("hta_commit_kv", lib().hta_commit_kv(ctypes.byref(s), _ptr(path), path.stride(0),
+                                                _ptr(path_len.to(torch.int32).reshape(B)), _ptr(k_tree), _ptr(v_tree),
+                                                _ptr(k_cache), _ptr(v_cache), _ptr(cache_seqlens), _ptr(seqlens_out),
+                                                _stream(stream)))
+    return seqlens_out
 
 
 # --------------------------------------------------------------------------- sequence parallel
