@@ -427,6 +427,31 @@ def main():
             "us": statistics.mean(ct), "rows": rows, "bytes": 2 * 2 * rows * w.H_kv * w.d * esz,
             "note": "accepted path of the step's tree (device accept -> commit, no host sync); latency-bound "
                     "(one CTA per batch entry)"}}
+        # f2: the draft model's cross-attention over the same target KV: hta_prefix_attn with the
+        # beam frontier as queries (16 tokens x G query rows per KV head)
+        qd = d_in["q"][:, :16].contiguous()
+        shp = hta.make_shape(qd, k_cache=kc)
+        wsd = hta.new_workspace(shp, dev)
+        od = torch.empty(w.B, 16, w.H, w.d, dtype=torch.float32, device=dev)
+        ld = torch.empty(w.B, w.H, 16, dtype=torch.float32, device=dev)
+        xt = []
+        for i in range(args.warmup + args.steps):
+            flush.fill_(i & 0xFF)
+            flush32.sum()
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            hta.hta_prefix_attn(qd, kc, vc, o_part=od, lse_part=ld, ws=wsd)
+            b_.record()
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                xt.append(a.elapsed_time(b_) * 1e3)
+        xb, xf = algorithmic_work(dict(cfg, T=16), hi - lo)
+        pk = peaks()
+        t_roof = max(xb / (pk["hbm_gbs"] * 1e9), xf / (pk["bf16_tflops"] * 1e12))
+        line["next_rows"]["f2_draft_xattn"] = {
+            "us": statistics.mean(xt), "queries": 16, "roofline_us": t_roof * 1e6,
+            "frac_of_roofline": t_roof * 1e6 / statistics.mean(xt), "bound": "hbm" if xb / pk["hbm_gbs"] > xf / (pk["bf16_tflops"] * 1e3) else "tensor",
+            "note": "hta_prefix_attn over the step's KV cache (split-KV kernel + split merge), 16 frontier queries"}
 
     # ---- cpu baseline (rank 0, N = 1 only): the oracle as it stands, bounded sample
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

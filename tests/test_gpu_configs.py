@@ -41,3 +41,21 @@ def test_config_full_size_sampled(cuda_device, name, dist):
     print(name, dist, stats)
     # properties that hold at any size, on every row: finite, no NaN, LSE >= the prefix LSE
     assert torch.isfinite(o.float()).all() and torch.isfinite(l).all()
+
+
+@pytest.mark.parametrize("T", [16, 4])
+def test_draft_cross_attention_full_size(cuda_device, T):
+    """the draft model's cross-attention over the target's KV cache is the
+    same unmasked prefix contraction with a small M (queries = the beam frontier, <= 16 tokens x
+    G): hta_prefix_attn at the Llama-8B-64k cache size, sampled rows vs the oracle's cache part."""
+    w = config_workload("llama8b_64k", dist="V1", seed=3)
+    q = w.q[:, :T].contiguous()
+    x = to_dev(w, cuda_device)
+    o, l = hta.hta_prefix_attn(q.to(cuda_device), x["kc"], x["vc"])
+    torch.cuda.synchronize()
+    rows = sample_rows(w.B, T, w.H, 48, seed=2)
+    mask = np.zeros((w.B, T, T), np.uint8)
+    ro, rl = oracle.attention(q, w.k_cache, w.v_cache, w.k_tree[:, :T], w.v_tree[:, :T], mask, part="cache",
+                              rows=rows)
+    idx = torch.tensor(rows)
+    compare(o[idx[:, 0], idx[:, 1], idx[:, 2]], l[idx[:, 0], idx[:, 2], idx[:, 1]], ro, rl, "bf16", f"xattn T={T}")
