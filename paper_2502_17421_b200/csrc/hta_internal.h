@@ -15,7 +15,7 @@ namespace hta {
 // Keys per KV tile of the prefix pass: TMEM holds 384 / kBlockN S/P buffers (2 x 192 or
 // 3 x 128 columns) and the 128-column O accumulator (512 columns in all).
 constexpr int kBlockN = HTA_BLOCK_N;
-static_assert(kBlockN == 128 || kBlockN == 192, "KV tile of 128 or 192 keys");
+static_assert(kBlockN == 96 || kBlockN == 128 || kBlockN == 192, "KV tile of 96, 128 or 192 keys");
 constexpr int kSimtBlock = 16;   // key block (split granularity) of the fp32 SIMT prefix pass
 constexpr int kRowsPerTile = 128;  // rows of one tcgen05 M=128 tile
 

@@ -94,9 +94,6 @@ __device__ __forceinline__ uint64_t trace_globaltimer() {
 #ifndef HTA_PHASE
 #define HTA_PHASE 0
 #endif
-#ifndef HTA_EARLY_PDL
-#define HTA_EARLY_PDL 0
-#endif
 #ifndef HTA_POLY
 #define HTA_POLY 3
 #endif
@@ -144,6 +141,8 @@ template <int N>
 __device__ __forceinline__ void tmem_ld_S(uint32_t taddr, float *v) {
     if constexpr (N == 96) {
         tmem_ld_x96<96>(taddr, v);
+    } else if constexpr (N == 48) {
+        tmem_ld_x48<48>(taddr, v);
     } else {
         tmem_ld_x64_nowait<64>(taddr, v);
         tmem_ld_wait_fence<64>(v);
@@ -490,6 +489,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         const int chalf = lane >> 4;
         const int r = quarter * 32 + rh * 16 + (lane & 15);
         const int grow = row0 + r;
+        const bool pad_warp = row0 + quarter * 32 + rh * 16 >= p.M;  // warp-uniform
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32 + rh * 16) << 16;
         const float c = p.scale_log2;
         const uint32_t pfull0 = PAIR ? mapa_shared(smem_u32(&p_full[0]), 0) : 0u;
@@ -538,7 +538,12 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             tc_fence_after();
             const bool last = j == n_tiles - 1;
             float mt = 0.f, lsum = 0.f;
-            if (HTA_SKIP < 1 || HTA_SKIP == 4) {
+            if (pad_warp) {
+                // all 16 rows of this warp are padding (row >= M, e.g. M = 64 for MHA with T = 64):
+                // no softmax -- their P (and O) rows are never used -- only the protocol
+                if (kDefer && j > 0) publish(j - 1);
+                mt = m_run;
+            } else if (HTA_SKIP < 1 || HTA_SKIP == 4) {
                 float s[kHalfCols];  // this thread's S values: keys [kHalfCols*chalf, +kHalfCols)
                 if (kDefer && j > 0) publish(j - 1);
                 tmem_ld_S<kHalfCols>(tmem + lane_off + s_col(buf), s);
@@ -578,6 +583,8 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                         pk[i & 15] = pack_bf16x2(pp.x, pp.y);
                         if ((i & 15) == 15)
                             tmem_st_16x16_split_nowait<kHalfCols / 2>(tmem + lane_off + s_col(buf) + (i - 15), pk);
+                        else if (i == kHalfCols / 2 - 1)  // a last chunk of 8 columns (48-column halves)
+                            tmem_st_16x8_split_nowait<kHalfCols / 2>(tmem + lane_off + s_col(buf) + (i & ~15), pk);
                     }
                     return (acc0.x + acc1.x) + (acc0.y + acc1.y);
                 };
