@@ -66,13 +66,22 @@ __device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads)
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// Wait for the phase with the given parity to complete.  A watchdog turns a protocol bug
-// into a trap (a reported kernel fault) instead of a hung GPU.
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Watchdog of the waits below: a wait that has not completed after kWatchdogNs of wall time is a
+// protocol bug; trap (a reported kernel fault) instead of hanging the GPU.
+constexpr uint64_t kWatchdogNs = 2000000000ull;  // 2 s (the longest kernel runs well under 1 ms)
+
+// Wait for the phase with the given parity to complete.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
-    uint32_t tries = 0;
+    if (mbar_try_wait(a, parity)) return;
+    const uint64_t t0 = global_ns();
     while (!mbar_try_wait(a, parity)) {
-        if (++tries > (1u << 24)) {
+        if (global_ns() - t0 > kWatchdogNs) {
             printf("hta: mbarrier wait timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
             __trap();
         }
@@ -93,9 +102,10 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar_addr, uint32_
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
-    uint32_t tries = 0;
+    if (mbar_try_wait_cluster(a, parity)) return;
+    const uint64_t t0 = global_ns();
     while (!mbar_try_wait_cluster(a, parity)) {
-        if (++tries > (1u << 24)) {
+        if (global_ns() - t0 > kWatchdogNs) {
             printf("hta: cluster mbarrier wait timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
             __trap();
         }
