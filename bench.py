@@ -452,6 +452,46 @@ def main():
             "us": statistics.mean(xt), "queries": 16, "roofline_us": t_roof * 1e6,
             "frac_of_roofline": t_roof * 1e6 / statistics.mean(xt), "bound": "hbm" if xb / pk["hbm_gbs"] > xf / (pk["bf16_tflops"] * 1e3) else "tensor",
             "note": "hta_prefix_attn over the step's KV cache (split-KV kernel + split merge), 16 frontier queries"}
+    if ws == 1 and (hi - lo) % 16 == 0:
+        # f3: the same forward over a paged cache (16-key pages, vLLM's default block size, pages
+        # shuffled in the pool) -- hta_forward_paged, timed like the prefix kernel alone
+        page = 16
+        maxp = (hi - lo) // page
+        perm = torch.randperm(w.B * maxp, generator=torch.Generator().manual_seed(0)).view(w.B, maxp)
+        kp = torch.empty(w.B * maxp, page, w.H_kv, w.d, dtype=kc.dtype, device=dev)
+        vp = torch.empty_like(kp)
+        kp[perm.to(dev).view(-1)] = kc.reshape(w.B * maxp, page, w.H_kv, w.d)
+        vp[perm.to(dev).view(-1)] = vc.reshape(w.B * maxp, page, w.H_kv, w.d)
+        bt = perm.to(torch.int32).to(dev)
+        pt = []
+        for i in range(args.warmup + args.steps):
+            flush.fill_(i & 0xFF)
+            flush32.sum()
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            hta.hta_forward_paged(d_in["q"], kp, vp, bt, d_in["kt"], d_in["vt"], mask, cache_seqlens=sl, o=o,
+                                  lse_out=lse, ws=wsb)
+            b_.record()
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                pt.append(a.elapsed_time(b_) * 1e3)
+        fw = []
+        for i in range(args.warmup + args.steps):
+            flush.fill_(i & 0xFF)
+            flush32.sum()
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            hta.hta_forward(d_in["q"], kc, vc, d_in["kt"], d_in["vt"], mask, cache_seqlens=sl, o=o, lse_out=lse,
+                            ws=wsb)
+            b_.record()
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                fw.append(a.elapsed_time(b_) * 1e3)
+        line["next_rows"]["f3_paged_kv"] = {
+            "us": statistics.mean(pt), "contiguous_us": statistics.mean(fw), "page_size": page,
+            "note": "hta_forward (a1-a4) over 16-key pages shuffled in a pool vs the same forward on the contiguous "
+                    "cache; 16-row TMA boxes through the block table"}
+        del kp, vp
 
     # ---- cpu baseline (rank 0, N = 1 only): the oracle as it stands, bounded sample
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

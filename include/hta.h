@@ -151,6 +151,23 @@ hta_status_t hta_forward_timed(const hta_shape_t *shape, const void *q, const vo
                                size_t ws_bytes, hta_stream_t stream, void *ev_prefix_begin,
                                void *ev_prefix_end);
 
+/* hybrid_tree_attention over a PAGED KV cache (the block-table layout of
+ * flash_attn_with_kvcache, for batched serving): as hta_forward (bf16 only), with
+ *   k_pool, v_pool  bf16 [num_pages, page_size, H_kv, d] contiguous (the pages of all batches)
+ *   page_size       a multiple of 16 (16-row TMA boxes)
+ *   block_table     device int32 [B, max_pages]: logical key k of batch b lives in page
+ *                   block_table[b][k / page_size], row k % page_size.  Entries past the pages a
+ *                   batch uses are not read for valid keys (negative ones read page 0, masked).
+ *   shape->N_max    ignored (the logical capacity is max_pages * page_size); kv_strides ignored.
+ * The result equals hta_forward on the gathered contiguous cache (the same tiles in the same
+ * order: bit-identical). */
+hta_status_t hta_forward_paged(const hta_shape_t *shape, const void *q, const void *k_pool,
+                               const void *v_pool, int32_t num_pages, int32_t page_size,
+                               const int32_t *block_table, int32_t max_pages,
+                               const int32_t *cache_seqlens, const void *k_tree, const void *v_tree,
+                               const uint8_t *mask, int64_t mask_batch_stride, void *o,
+                               float *lse_out, void *ws, size_t ws_bytes, hta_stream_t stream);
+
 /* Tree mask from a parent array ("attention masks derived from prefix trees"; reading
  * Z4: mask[i][j] = 1 iff j == i or j is an ancestor of i).
  *   parents  int32 [T], parents[i] in [-1, i) (-1 = child of the committed context; reading Z6)

@@ -208,12 +208,43 @@ bool make_q_map(CUtensorMap *map, const void *q, const hta_shape_t &s, int G) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Paged KV cache: a contiguous pool [num_pages, page_size, H_kv, d] and a
+// block table [B][max_pages] of page indices.
+struct PagedArgs {
+    const int32_t *block_table;
+    int32_t max_pages;
+    int32_t page_size;
+    int32_t num_pages;
+};
+
+// 4-D map over the page pool seen as [1, num_pages * page_size, H_kv, d]: 16-row boxes.
+hta_status_t make_pool_map(CUtensorMap *map, const void *base, const hta_shape_t &s, const PagedArgs &pg) {
+    EncodeTiledFn enc = encode_fn();
+    if (enc == nullptr) return HTA_ERR_CUDA;
+    const cuuint64_t rows = cuuint64_t(pg.num_pages) * cuuint64_t(pg.page_size);
+    cuuint64_t dims[4] = {cuuint64_t(s.d), cuuint64_t(s.H_kv), rows, 1};
+    const cuuint64_t row_bytes = cuuint64_t(s.H_kv) * s.d * 2;
+    cuuint64_t strides[3] = {cuuint64_t(s.d) * 2, row_bytes, rows * row_bytes};
+    cuuint32_t box[4] = {64, 1, 16, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? HTA_OK : HTA_ERR_INVALID_ARGUMENT;
+}
+
 // Enqueue the prefix pass writing `splits` partials at (o_out, lse_out) with the given strides.
 hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, const void *k, const void *v,
                         const int32_t *seqlens, float *o_out, float *lse_out, int64_t o_split_stride,
-                        int64_t lse_split_stride, cudaStream_t st) {
+                        int64_t lse_split_stride, cudaStream_t st, const PagedArgs *pg = nullptr) {
     const hta_shape_t &s = sh.s;
     PrefixParams p{};
+    if (pg != nullptr) {
+        p.block_table = pg->block_table;
+        p.bt_stride = pg->max_pages;
+        p.page_size = pg->page_size;
+        p.max_pages = pg->max_pages;
+    }
     p.q = q;
     p.qs0 = s.q_strides[0];
     p.qs1 = s.q_strides[1];
@@ -245,11 +276,15 @@ hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, co
     cudaError_t e;
     if (s.dtype == HTA_BF16) {
         CUtensorMap tk, tv;
-        // a CTA of a pair loads half of each K tile (64 keys) and half of each V tile (64 columns)
-        hta_status_t r = make_kv_map(&tk, k, s, pl.nt == 2 ? kBlockN / 2 : kBlockN);
-        if (r != HTA_OK) return r;
-        r = make_kv_map(&tv, v, s, kBlockN);
-        if (r != HTA_OK) return r;
+        hta_status_t r;
+        if (pg != nullptr) {
+            if ((r = make_pool_map(&tk, k, s, *pg)) != HTA_OK) return r;
+            if ((r = make_pool_map(&tv, v, s, *pg)) != HTA_OK) return r;
+        } else {
+            // a CTA of a pair loads half of each K tile (96 keys) and half of each V tile (64 columns)
+            if ((r = make_kv_map(&tk, k, s, pl.nt == 2 ? kBlockN / 2 : kBlockN)) != HTA_OK) return r;
+            if ((r = make_kv_map(&tv, v, s, kBlockN)) != HTA_OK) return r;
+        }
         CUtensorMap tq;
         std::memset(&tq, 0, sizeof(tq));
         p.q_tma = make_q_map(&tq, q, s, sh.G) ? 1 : 0;
@@ -403,7 +438,7 @@ hta_status_t hta_merge_lse(const hta_shape_t *shape, int32_t n_parts, const floa
                : HTA_ERR_CUDA;
 }
 
-hta_status_t hta_forward_timed(const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,
+static hta_status_t forward_impl(const PagedArgs *pg, const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,
                                const int32_t *cache_seqlens, const void *k_tree, const void *v_tree,
                                const uint8_t *mask, int64_t mask_batch_stride, void *o, float *lse_out, void *ws,
                                size_t ws_bytes, hta_stream_t stream, void *ev_begin, void *ev_end) {
@@ -427,7 +462,7 @@ hta_status_t hta_forward_timed(const hta_shape_t *shape, const void *q, const vo
     const int64_t lstride = int64_t(s.B) * s.H * s.T;
     if (ev_begin != nullptr && cudaEventRecord(static_cast<cudaEvent_t>(ev_begin), st) != cudaSuccess)
         return HTA_ERR_CUDA;
-    r = run_prefix(sh, pl, q, k_cache, v_cache, cache_seqlens, o_ws, lse_ws, ostride, lstride, st);
+    r = run_prefix(sh, pl, q, k_cache, v_cache, cache_seqlens, o_ws, lse_ws, ostride, lstride, st, pg);
     if (r != HTA_OK) return r;
     if (ev_end != nullptr && cudaEventRecord(static_cast<cudaEvent_t>(ev_end), st) != cudaSuccess)
         return HTA_ERR_CUDA;
@@ -450,6 +485,32 @@ hta_status_t hta_forward_timed(const hta_shape_t *shape, const void *q, const vo
     p.lse = lse_out;
     return launch_tree_merge(p, s.d, s.dtype, s.dtype, ev_end == nullptr, st) == cudaSuccess ? HTA_OK
                                                                                               : HTA_ERR_CUDA;
+}
+
+hta_status_t hta_forward_timed(const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,
+                               const int32_t *cache_seqlens, const void *k_tree, const void *v_tree,
+                               const uint8_t *mask, int64_t mask_batch_stride, void *o, float *lse_out, void *ws,
+                               size_t ws_bytes, hta_stream_t stream, void *ev_begin, void *ev_end) {
+    return forward_impl(nullptr, shape, q, k_cache, v_cache, cache_seqlens, k_tree, v_tree, mask, mask_batch_stride, o,
+                        lse_out, ws, ws_bytes, stream, ev_begin, ev_end);
+}
+
+hta_status_t hta_forward_paged(const hta_shape_t *shape, const void *q, const void *k_pool, const void *v_pool,
+                               int32_t num_pages, int32_t page_size, const int32_t *block_table, int32_t max_pages,
+                               const int32_t *cache_seqlens, const void *k_tree, const void *v_tree,
+                               const uint8_t *mask, int64_t mask_batch_stride, void *o, float *lse_out, void *ws,
+                               size_t ws_bytes, hta_stream_t stream) {
+    if (shape == nullptr || block_table == nullptr || num_pages < 1 || max_pages < 1 || page_size < 16 ||
+        page_size % 16 != 0)
+        return HTA_ERR_INVALID_ARGUMENT;
+    if (shape->dtype != HTA_BF16) return HTA_ERR_UNSUPPORTED;
+    if (int64_t(num_pages) * page_size > (int64_t(1) << 31) - 1024) return HTA_ERR_INVALID_ARGUMENT;
+    hta_shape_t s = *shape;
+    s.N_max = int64_t(max_pages) * page_size;  // logical capacity of a batch entry
+    s.kv_strides[0] = s.kv_strides[1] = s.kv_strides[2] = 0;  // (the pool is contiguous)
+    const PagedArgs pg{block_table, max_pages, page_size, num_pages};
+    return forward_impl(&pg, &s, q, k_pool, v_pool, cache_seqlens, k_tree, v_tree, mask, mask_batch_stride, o, lse_out,
+                        ws, ws_bytes, stream, nullptr, nullptr);
 }
 
 hta_status_t hta_forward(const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,

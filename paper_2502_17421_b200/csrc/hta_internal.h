@@ -43,6 +43,14 @@ struct PrefixParams {
     float scale_log2;                 // scale * log2(e)
     int nt, n_mgroups, splits, tiles_per_split;
     int q_tma;                                  // Q rows of a tile come from tmap_q (G divides 128)
+    // Paged KV (page_size > 0): the K/V maps cover a pool of pages seen as
+    // one [rows, H_kv, d] tensor; logical key k of batch b sits at pool row
+    // block_table[b * bt_stride + k / page_size] * page_size + k % page_size.  TMA boxes are 16
+    // rows (page_size % 16 == 0).
+    const int32_t *block_table;
+    int64_t bt_stride;
+    int page_size;
+    int max_pages;                              // entries per block-table row (clamp)
     float *o_out;                     // [S][B][T][H][d] fp32, normalised partials
     float *lse_out;                   // [S][B][H][T] natural-log LSE
     int64_t o_split_stride, lse_split_stride;  // elements between splits

@@ -149,6 +149,16 @@ __device__ __forceinline__ void tmem_ld_S(uint32_t taddr, float *v) {
     }
 }
 
+// Pool row of logical key k of batch b (paged KV); pages past the table or negative entries read
+// page 0 (such keys are past cache_seqlens: masked, and their V rows zeroed).
+__device__ __forceinline__ int paged_row(const PrefixParams &p, int b, int k) {
+    int page = k / p.page_size;
+    page = page < p.max_pages ? page : p.max_pages - 1;
+    int e = p.block_table[b * p.bt_stride + page];
+    e = e < 0 ? 0 : e;
+    return e * p.page_size + k % p.page_size;
+}
+
 template <int D, bool PAIR>
 __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     prefix_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
@@ -293,7 +303,41 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                                 kPolicyEvictNormal);
             }
         }
-        if (lane == 0 && HTA_SKIP < 3) {
+        if (p.page_size > 0 && HTA_SKIP < 3) {
+            // paged KV: the whole warp runs the loop; lane i translates box i (16 keys) of the
+            // tile through the block table, lane 0 issues the TMA boxes
+            const uint32_t kfull0 = PAIR ? mapa_shared(smem_u32(&k_full[0]), 0) : 0u;
+            constexpr int kBoxes = C::kKRows / 16;
+            for (int j = 0; j < n_tiles; ++j) {
+                const int n0 = static_cast<int>(key_lo) + j * kBlockN + (PAIR ? static_cast<int>(rank) * C::kKRows : 0);
+                const int prow = paged_row(p, b, n0 + 16 * (lane < kBoxes ? lane : 0));
+                const int slot = j % C::kSlotsK;
+                if (lane == 0) mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);
+                __syncwarp();
+                uint8_t *dst = sK + slot * C::kKBytes;
+                if (lane == 0) {
+                    if (PAIR) {
+                        if (leader) mbar_arrive_expect_tx(&k_full[slot], 2u * C::kKBytes);
+                    } else {
+                        mbar_arrive_expect_tx(&k_full[slot], C::kKBytes);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < kBoxes; ++i) {
+                    const int r = __shfl_sync(0xffffffffu, prow, i);
+                    if (lane == 0) {
+#pragma unroll
+                        for (int kb = 0; kb < C::kKB; ++kb) {
+                            uint8_t *dd = dst + kb * (C::kKRows * 128) + i * 2048;
+                            if (PAIR)
+                                tma_load_4d_pair(dd, &tmap_k, kfull0 + 8u * slot, kb * 64, g, r, 0, kKvPolicy);
+                            else
+                                tma_load_4d(dd, &tmap_k, &k_full[slot], kb * 64, g, r, 0, kKvPolicy);
+                        }
+                    }
+                }
+            }
+        } else if (lane == 0 && HTA_SKIP < 3) {
             const uint32_t kfull0 = PAIR ? mapa_shared(smem_u32(&k_full[0]), 0) : 0u;
             for (int j = 0; j < n_tiles; ++j) {
                 const int n0 = static_cast<int>(key_lo) + j * kBlockN;
@@ -318,7 +362,40 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         __syncwarp();
     } else if (warp == 2) {
         // ================= TMA producer of the V ring (V_j is consumed by PV_j)
-        if (lane == 0 && HTA_SKIP < 3) {
+        if (p.page_size > 0 && HTA_SKIP < 3) {
+            const uint32_t vfull0 = PAIR ? mapa_shared(smem_u32(&v_full[0]), 0) : 0u;
+            constexpr int kBoxes = kBlockN / 16;
+            for (int j = 0; j < n_tiles; ++j) {
+                const int n0 = static_cast<int>(key_lo) + j * kBlockN;
+                const int prow = paged_row(p, b, n0 + 16 * (lane < kBoxes ? lane : 0));
+                const int slot = j % C::kSlotsV;
+                if (lane == 0) mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
+                __syncwarp();
+                uint8_t *dst = sV + slot * C::kVBytes;
+                if (lane == 0) {
+                    if (PAIR) {
+                        if (leader) mbar_arrive_expect_tx(&v_full[slot], 2u * C::kVBytes);
+                    } else {
+                        mbar_arrive_expect_tx(&v_full[slot], C::kVBytes);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < kBoxes; ++i) {
+                    const int r = __shfl_sync(0xffffffffu, prow, i);
+                    if (lane == 0) {
+                        if (PAIR) {
+                            tma_load_4d_pair(dst + i * 2048, &tmap_v, vfull0 + 8u * slot, static_cast<int>(rank) * 64,
+                                             g, r, 0, kKvPolicy);
+                        } else {
+#pragma unroll
+                            for (int kb = 0; kb < C::kKB; ++kb)
+                                tma_load_4d(dst + kb * (kBlockN * 128) + i * 2048, &tmap_v, &v_full[slot], kb * 64, g,
+                                            r, 0, kKvPolicy);
+                        }
+                    }
+                }
+            }
+        } else if (lane == 0 && HTA_SKIP < 3) {
             const uint32_t vfull0 = PAIR ? mapa_shared(smem_u32(&v_full[0]), 0) : 0u;
             for (int j = 0; j < n_tiles; ++j) {
                 const int n0 = static_cast<int>(key_lo) + j * kBlockN;

@@ -47,6 +47,9 @@ _SIG = {
                                    _P, ctypes.c_size_t, _P]),
     "hta_forward_timed": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, _P, _P, _P, ctypes.c_int64,
                                          _P, _P, _P, ctypes.c_size_t, _P, _P, _P]),
+    "hta_forward_paged": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, _P, _P, ctypes.c_int32, ctypes.c_int32, _P,
+                                         ctypes.c_int32, _P, _P, _P, _P, ctypes.c_int64, _P, _P, _P, ctypes.c_size_t,
+                                         _P]),
     "hta_build_tree_mask": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int32, _P]),
     "hta_validate_tree_mask": (ctypes.c_int, [_P, ctypes.c_int32]),
     "hta_accept_greedy": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _P,
@@ -228,6 +231,28 @@ def hta_forward(q, k_cache, v_cache, k_tree, v_tree, mask, cache_seqlens=None, o
         _check("hta_forward_timed", lib().hta_forward_timed(
             ctypes.byref(shape), _ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(cache_seqlens), _ptr(k_tree),
             _ptr(v_tree), _ptr(mask), mbs, _ptr(o), _ptr(lse_out), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream), ev0, ev1))
+    return o, lse_out
+
+
+def hta_forward_paged(q, k_pool, v_pool, block_table, k_tree, v_tree, mask, cache_seqlens=None, o=None,
+                      lse_out=None, ws=None, want_lse=True, scale=None, num_splits=0, stream=None):
+    """hta_forward over a paged cache: k_pool/v_pool [num_pages, page_size, H_kv, d] bf16,
+    block_table int32 [B, max_pages] (device)."""
+    num_pages, page_size, Hkv, d = k_pool.shape
+    B, T, H, _ = q.shape
+    max_pages = block_table.shape[1]
+    shape = make_shape(q, k_tree=k_tree, H_kv=Hkv, N_max=max_pages * page_size, scale=scale, num_splits=num_splits)
+    shape.N_max = max_pages * page_size
+    mbs = 0 if mask.dim() == 2 else mask.stride(0)
+    o = _out_like_q(q, o)
+    if want_lse and lse_out is None:
+        lse_out = torch.empty(B, H, T, dtype=torch.float32, device=q.device)
+    ws = _workspace(shape, q.device, ws)
+    bt = block_table.to(torch.int32).contiguous()
+    _check("hta_forward_paged", lib().hta_forward_paged(
+        ctypes.byref(shape), _ptr(q), _ptr(k_pool), _ptr(v_pool), num_pages, page_size, _ptr(bt), max_pages,
+        _ptr(cache_seqlens), _ptr(k_tree), _ptr(v_tree), _ptr(mask), mbs, _ptr(o), _ptr(lse_out), _ptr(ws),
+        ws.numel() * ws.element_size(), _stream(stream)))
     return o, lse_out
 
 
