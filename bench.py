@@ -203,6 +203,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-all-configs", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=60.0, help="seconds of oracle work for --impl reference")
+    ap.add_argument("--force-seqpar", action="store_true",
+                    help="run the sequence-parallel step (NCCL) even on one rank: checks the N > 1 code path "
+                         "on a single GPU")
     args = ap.parse_args()
     ws, rank, local = dist_env()
     cfg = dict(CONFIGS[args.workload])
@@ -216,10 +219,13 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
+    seqpar = ws > 1 or args.force_seqpar
+    if seqpar:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-    comm = hta.HtaComm(rank, ws) if ws > 1 else None
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=ws)
+    comm = hta.HtaComm(rank, ws) if seqpar else None
 
     # ---- inputs (seeded, synthetic, BASELINE.json workload shape); KV cache resident in HBM
     w = config_workload(args.workload, seed=0)
@@ -244,7 +250,7 @@ def main():
     o, path, plen, bonus = out["o"], out["path"], out["plen"], out["bonus"]
     lse = torch.empty(w.B, Hx, T, dtype=torch.float32, device=dev)
     shape = hta.make_shape(d_in["q"], k_cache=kc, k_tree=d_in["kt"])
-    if ws > 1:
+    if seqpar:
         wsb = torch.empty(comm.workspace_size(shape), dtype=torch.uint8, device=dev)
     else:
         wsb = hta.new_workspace(shape, dev)
@@ -262,17 +268,17 @@ def main():
             hta.hta_accept_greedy(x["parents"], x["draft"], x["tgt"], root=0, context_argmax=ctx,
                                   path=path, path_len=plen, bonus=bonus)                    # a6
         hta.hta_build_tree_mask(x["parents"], mask)                                         # a0
-        if ws > 1:                                                                          # a1-a5
+        if seqpar:                                                                          # a1-a5
             comm.forward(x["q"], kc, vc, x["kt"], x["vt"], mask, cache_seqlens_local=sl, o=o, lse_out=lse, ws=wsb)
         else:                                                                               # a1-a4
             hta.hta_forward(x["q"], kc, vc, x["kt"], x["vt"], mask, cache_seqlens=sl, o=o, lse_out=lse, ws=wsb,
                             events=events)
         cur.wait_stream(side)
 
-    launches_per_step = 4 if ws == 1 else 5
+    launches_per_step = 5 if seqpar else 4
 
     def barrier():
-        if ws > 1:
+        if seqpar:
             torch.distributed.barrier()
 
     # ---- warm-up
@@ -289,7 +295,7 @@ def main():
 
     e2e_buf, e2e_in = packed({k: (v.shape, v.dtype) for k, v in src.items()}, dev)
     graphs = {}
-    if ws == 1:  # (NCCL calls of the sequence-parallel step are issued eagerly)
+    if not seqpar:  # (NCCL calls of the sequence-parallel step are issued eagerly)
         for name, fn in (("step", lambda: step(d_in)), ("e2e", e2e_body)):
             cs = torch.cuda.Stream(device=dev)
             cs.wait_stream(torch.cuda.current_stream())
@@ -337,7 +343,7 @@ def main():
         # (1) device-resident step (graph replay)
         times = timed(lambda i: run_step(), args.steps)
         # (2) dominant kernel (prefix pass) timed on its own launch stream with CUDA events
-        if ws == 1:
+        if not seqpar:
             ev = created_events(2 * args.steps)
             pev = [(ev[2 * i], ev[2 * i + 1]) for i in range(args.steps)]
             timed(lambda i: step(d_in, events=pev[i]), args.steps)
@@ -394,7 +400,7 @@ def main():
                    "parallelism": f"seq{ws}",
                    "l2": "flushed before every timed step (512 MiB write, then a read of it; untimed)",
                    "step": ("a0 mask + hta_forward (a1-a4) | accept (a6) on a forked stream"
-                            + (" + NCCL exchange (a5)" if ws > 1 else "; CUDA graph replay"))},
+                            + (" + NCCL exchange (a5)" if seqpar else "; CUDA graph replay"))},
         "clocks": clocks,
         "gpu_launches": launches_per_step * args.steps,
         "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
@@ -407,7 +413,7 @@ def main():
     # ---- commit of the accepted path's K/V rows into the cache (device, after
     # a6), timed on its own (L2 flushed); measured after the step timings since it writes rows
     # of the (then no longer used) cache
-    if ws == 1:
+    if not seqpar:
         sl_commit = torch.full((w.B,), max(0, (hi - lo) - T), dtype=torch.int32, device=dev)
         out_sl = torch.empty_like(sl_commit)
         ct = []
@@ -452,7 +458,7 @@ def main():
             "us": statistics.mean(xt), "queries": 16, "roofline_us": t_roof * 1e6,
             "frac_of_roofline": t_roof * 1e6 / statistics.mean(xt), "bound": "hbm" if xb / pk["hbm_gbs"] > xf / (pk["bf16_tflops"] * 1e3) else "tensor",
             "note": "hta_prefix_attn over the step's KV cache (split-KV kernel + split merge), 16 frontier queries"}
-    if ws == 1 and (hi - lo) % 16 == 0:
+    if not seqpar and (hi - lo) % 16 == 0:
         # f3: the same forward over a paged cache (16-key pages, vLLM's default block size, pages
         # shuffled in the pool) -- hta_forward_paged, timed like the prefix kernel alone
         page = 16
@@ -494,7 +500,7 @@ def main():
         del kp, vp
 
     # ---- cpu baseline (rank 0, N = 1 only): the oracle as it stands, bounded sample
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not seqpar and not args.no_cpu_baseline:
         import oracle
         mask_np = np.stack([oracle.tree_mask(w.parents[b]) for b in range(w.B)])
         tps, dt, n, tot, cores = time_oracle(w, mask_np)
@@ -502,7 +508,7 @@ def main():
                                 "sample": f"{n} of {tot} query rows ({dt:.1f} s), extrapolated linearly"}
 
     # ---- the other BASELINE configs (N = 1): µs/step, device-resident, L2 flushed
-    if rank == 0 and ws == 1 and not args.no_all_configs:
+    if rank == 0 and not seqpar and not args.no_all_configs:
         others = {}
         for name in CONFIGS:
             if name == args.workload:
