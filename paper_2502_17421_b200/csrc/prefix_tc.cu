@@ -88,6 +88,9 @@ __device__ __forceinline__ uint64_t trace_globaltimer() {
 #define HTA_SKIP 0
 #endif
 // Pairs of every 8 whose exp2 runs on the FMA pipe (polynomial) instead of MUFU.
+#ifndef HTA_SPEC_MAX
+#define HTA_SPEC_MAX 1
+#endif
 #ifndef HTA_RING_KB
 #define HTA_RING_KB 192
 #endif
@@ -682,10 +685,27 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
                     return fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16)) * c;
                 };
+#if HTA_SPEC_MAX
+                // Speculative exponentials with the running max: no row-max reduction on the
+                // critical path.  Exact as long as no P exceeds 2^60 (bf16 P and the fp32 O / row
+                // sums have the range; floating point keeps the relative precision), which the row
+                // sum checks; otherwise (always on the first tile, where m_run = -inf) the warp
+                // redoes the tile with the true row max.
+                HTA_TR(11, sw, j);
+                lsum = exp_store(m_run);
+                mt = m_run;
+                if (__any_sync(0xffffffffu, !(lsum <= 0x1p60f))) {
+                    tmem_st_wait();  // the speculative P stores land before they are overwritten
+                    const float mx = row_max();
+                    mt = mx > m_run ? mx : m_run;
+                    lsum = exp_store(mt);
+                }
+#else
                 const float mx = row_max();
                 HTA_TR(11, sw, j);
                 mt = (mx > m_run + 8.0f) ? mx : m_run;  // stale max: rescale only on a jump > 2^8
                 lsum = exp_store(mt);
+#endif
             } else {
                 if (kDefer && j > 0) publish(j - 1);
                 mt = 0.f;
