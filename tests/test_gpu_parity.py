@@ -34,6 +34,9 @@ CASES = [
     (2, 7, 4, 2, 64, 129, "fp32", "V0", "roots"),            # fp32 d=64, self-only tree
     (1, 30, 6, 2, 128, 900, "bf16", "V1", "random"),         # G=3: Q staged by loads, one CTA
     (2, 9, 6, 2, 64, 700, "bf16", "V2", "beam"),             # G=3, d=64
+    (1, 256, 8, 2, 128, 600, "bf16", "V1", "beam"),          # T=256 (the maximum), M=1024: 4 pair groups
+    (1, 64, 32, 1, 128, 1000, "bf16", "V1", "beam"),         # MQA (H_kv=1, G=32), M=2048
+    (2, 33, 8, 8, 64, 2049, "bf16", "V2", "random"),         # MHA d=64, N just past a 192-key tile
 ]
 
 
@@ -206,3 +209,54 @@ def test_deterministic(cuda_device):
     o2, l2 = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask)
     torch.cuda.synchronize()
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+def test_step_in_cuda_graph_matches_eager(cuda_device):
+    """bench.py replays the step (mask -> forward, accept on a forked stream) from a CUDA graph;
+    the replay (with programmatic dependent launches as graph edges) must give the eager results."""
+    from workloads import accept_tokens
+    w = make_workload(1, 64, 32, 8, 128, 3000, "bf16", dist="V1", seed=17, tree="beam")
+    x = to_dev(w, cuda_device)
+    par = w.parents[0].to(cuda_device)
+    dr, tg, ctx = accept_tokens(w.parents[0], seed=1, vocab=1000, p_match=0.8)
+    dr, tg = dr.to(cuda_device), tg.to(cuda_device)
+    mask = torch.empty(64, 64, dtype=torch.uint8, device=cuda_device)
+    o = torch.empty_like(x["q"])
+    lse = torch.empty(1, 32, 64, dtype=torch.float32, device=cuda_device)
+    path = torch.empty(64, dtype=torch.int32, device=cuda_device)
+    plen = torch.empty(1, dtype=torch.int32, device=cuda_device)
+    bonus = torch.empty(1, dtype=torch.int32, device=cuda_device)
+    wsb = hta.new_workspace(hta.make_shape(x["q"], k_cache=x["kc"], k_tree=x["kt"]), cuda_device)
+    side = torch.cuda.Stream(device=cuda_device)
+
+    def step():
+        cur = torch.cuda.current_stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            hta.hta_accept_greedy(par, dr, tg, root=0, path=path, path_len=plen, bonus=bonus)
+        hta.hta_build_tree_mask(par, mask)
+        hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask, cache_seqlens=x["sl"], o=o, lse_out=lse,
+                        ws=wsb)
+        cur.wait_stream(side)
+
+    step()
+    torch.cuda.synchronize()
+    ref = [t.clone() for t in (o, lse, path, plen, bonus)]
+    for t in (o, lse, path, plen, bonus):
+        t.zero_()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream(device=cuda_device)
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    for t in (o, lse, path, plen, bonus):
+        t.zero_()
+    with torch.cuda.graph(g):
+        step()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip((o, lse, path, plen, bonus), ref):
+        assert torch.equal(a, b)
