@@ -94,9 +94,6 @@ __device__ __forceinline__ uint64_t trace_globaltimer() {
 #ifndef HTA_RING_KB
 #define HTA_RING_KB 192
 #endif
-#ifndef HTA_PHASE
-#define HTA_PHASE 0
-#endif
 #ifndef HTA_POLY
 #define HTA_POLY 3
 #endif

@@ -12,64 +12,29 @@ namespace hta {
 constexpr int kTmWarps = HTA_TM_WARPS;  // warps (= rows) per block
 // One warp per row; small blocks of at most 128 registers per thread, so that blocks fit beside
 // the prefix kernel's CTAs and start (programmatic dependent launch) during its epilogue.
-template <typename Tin, typename Tout, int D, int R>
+template <typename Tin, typename Tout, int D>
 __global__ void __launch_bounds__(32 * kTmWarps, 16 / kTmWarps) tree_merge_kernel(const TreeMergeParams p) {
     constexpr int E = D / 32;
-    const int nrows = p.B * p.T * p.Hr;
-    const int warp_id = blockIdx.x * kTmWarps + (threadIdx.x >> 5);
-    const int nwarps = gridDim.x * kTmWarps;
+    const int row = blockIdx.x * kTmWarps + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-
-    // ------------------------------------------------------------- tree pass
-    float ot[R][E], lse_t[R];
+    if (row >= p.B * p.T * p.Hr) return;
+    const int hl = row % p.Hr, t = (row / p.Hr) % p.T, b = row / (p.Hr * p.T);
+    // tree pass: before griddepcontrol.wait, so it overlaps the tail of the prefix kernel
+    float ot[E];
+    float lse_t = -INFINITY;
 #pragma unroll
-    for (int k = 0; k < R; ++k) {
-        const int row = warp_id + k * nwarps;
-        lse_t[k] = -INFINITY;
-#pragma unroll
-        for (int e = 0; e < E; ++e) ot[k][e] = 0.f;
-        if (row < nrows && p.do_tree) {
-            const int hl = row % p.Hr, t = (row / p.Hr) % p.T, b = row / (p.Hr * p.T);
-            lse_t[k] = tree_row<Tin, D>(p, b, t, p.h0 + hl, lane, ot[k]);
-        }
-    }
+    for (int e = 0; e < E; ++e) ot[e] = 0.f;
+    if (p.do_tree) lse_t = tree_row<Tin, D>(p, b, t, p.h0 + hl, lane, ot);
     if (p.n_parts > 0) pdl_wait_primary();  // the partials come from the preceding prefix kernel
-
-    // ------------------------------------------------------------- merge with prefix parts
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-        const int row = warp_id + k * nwarps;
-        if (row >= nrows) break;
-        const int hl = row % p.Hr, t = (row / p.Hr) % p.T, b = row / (p.Hr * p.T);
-        merge_row<Tout, D, false>(p, b, t, hl, lane, ot[k], lse_t[k]);
-    }
-}
-
-static int num_sms() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) !=
-                                                       cudaSuccess || n <= 0)
-            n = 148;
-    }
-    return n;
+    merge_row<Tout, D, false>(p, b, t, hl, lane, ot, lse_t);
 }
 
 template <typename Tin, typename Tout, int D>
 static cudaError_t launch_tm_d(const TreeMergeParams &p, bool pdl, cudaStream_t s) {
     const int rows = p.B * p.T * p.Hr;
     if (rows == 0) return cudaSuccess;
-    // with PDL the grid should fit beside the prefix kernel (one 4-warp block per SM): up to 8
-    // rows per warp; without PDL one row per warp spreads the latency-bound work widest
-#ifndef HTA_TM_RMAX
-#define HTA_TM_RMAX 1
-#endif
-    int R = 1;
-    if (pdl)
-        while (R < HTA_TM_RMAX && static_cast<int64_t>(num_sms()) * kTmWarps * R < rows) R *= 2;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((rows + kTmWarps * R - 1) / (kTmWarps * R));
+    cfg.gridDim = dim3((rows + kTmWarps - 1) / kTmWarps);
     cfg.blockDim = dim3(32 * kTmWarps);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
@@ -78,13 +43,7 @@ static cudaError_t launch_tm_d(const TreeMergeParams &p, bool pdl, cudaStream_t 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    cudaError_t e;
-    switch (R) {
-        case 1: e = cudaLaunchKernelEx(&cfg, tree_merge_kernel<Tin, Tout, D, 1>, p); break;
-        case 2: e = cudaLaunchKernelEx(&cfg, tree_merge_kernel<Tin, Tout, D, 2>, p); break;
-        case 4: e = cudaLaunchKernelEx(&cfg, tree_merge_kernel<Tin, Tout, D, 4>, p); break;
-        default: e = cudaLaunchKernelEx(&cfg, tree_merge_kernel<Tin, Tout, D, 8>, p); break;
-    }
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, tree_merge_kernel<Tin, Tout, D>, p);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

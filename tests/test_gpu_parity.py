@@ -239,6 +239,8 @@ def test_step_in_cuda_graph_matches_eager(cuda_device):
                         ws=wsb)
         cur.wait_stream(side)
 
+    for t in (o, lse, path, plen, bonus):  # (path is written up to path_len only)
+        t.zero_()
     step()
     torch.cuda.synchronize()
     ref = [t.clone() for t in (o, lse, path, plen, bonus)]
@@ -258,5 +260,5 @@ def test_step_in_cuda_graph_matches_eager(cuda_device):
     for _ in range(3):
         g.replay()
     torch.cuda.synchronize()
-    for a, b in zip((o, lse, path, plen, bonus), ref):
-        assert torch.equal(a, b)
+    for name, a, b in zip(("o", "lse", "path", "path_len", "bonus"), (o, lse, path, plen, bonus), ref):
+        assert torch.equal(a, b), f"{name}: max |diff| {(a.float() - b.float()).abs().max().item()}"
