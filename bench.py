@@ -61,7 +61,7 @@ def algorithmic_work(cfg, n_keys):
 class ClockSampler:
     """nvidia-smi clock / throttle sampling during the timed region (B200_PROFILING.md)."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
 
     def __init__(self, index: int):
         self.index = index
@@ -70,7 +70,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -89,15 +89,18 @@ class ClockSampler:
                 self.out = ""
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
+        """Median SM clock over the samples taken under load (GPU utilisation >= 50 %; all samples
+        if none), max clock, and every throttle reason seen active."""
+        sm, mx, util, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in (getattr(self, "out", "") or "").strip().splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 6:
+            if len(f) < 7:
                 continue
             try:
                 sm.append(float(f[0]))
                 mx.append(float(f[1]))
+                util.append(float(f[6]))
             except ValueError:
                 continue
             for n, v in zip(names, f[2:6]):
@@ -105,8 +108,9 @@ class ClockSampler:
                     reasons.add(n)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        loaded = [c for c, u in zip(sm, util) if u >= 50.0]
+        return {"sm_mhz": statistics.median(loaded or sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm), "samples_under_load": len(loaded)}
 
 
 def packed(specs, device):
