@@ -24,7 +24,9 @@ def sample_rows(B, T, H, n, seed):
     return sorted(rows)
 
 
-@pytest.mark.parametrize("name,dist", [(n, "V1") for n in CONFIGS] + [("llama8b_64k", "V2")])
+@pytest.mark.parametrize("name,dist", [(n, "V1") for n in CONFIGS] +
+                         [("llama8b_64k", "V2"), ("qwq32b_32k_b4", "V2"), ("longchat7b_16k", "V0"),
+                          ("llama8b_128k_t128", "V2")])
 def test_config_full_size_sampled(cuda_device, name, dist):
     w = config_workload(name, dist=dist, seed=0)
     mask = oracle_masks(w)
