@@ -58,13 +58,8 @@ def main():
         pro = [(r[1] - r[0]) / 1e3 for r in rows]
         ext = [(r[3] - t0) / 1e3 for r in rows]
         mhz = [r[2] / (r[3] - r[1]) * 1e3 for r in rows]
-        if all(r[4] for r in rows):
-            ep = [(r[4] - t0) / 1e3 for r in rows]
-            ms = [(r[5] - t0) / 1e3 for r in rows if r[5]]
-            md = [(r[6] - r[5]) / 1e3 for r in rows if r[6] and r[5]]
-            print(f"fused epilogue: main loop ends min {min(ep):.1f} median {statistics.median(ep):.1f} max {max(ep):.1f} us;"
-                  f" group wait ends median {statistics.median(ms):.1f} max {max(ms):.1f}; merge takes median "
-                  f"{statistics.median(md):.2f} max {max(md):.2f} us")
+        slow = sorted(range(len(rows)), key=lambda i: -ext[i])[:12]
+        print("slowest CTAs (blockIdx: exit us):", ", ".join(f"{i}:{ext[i]:.1f}" for i in slow))
         print(f"{len(rows)} CTAs: entry spread {max(ent):.1f} us; prologue {statistics.mean(pro):.1f} us "
               f"(max {max(pro):.1f}); exit min {min(ext):.1f} median {statistics.median(ext):.1f} max {max(ext):.1f} us; "
               f"SM clock {statistics.median(mhz):.0f} MHz")
