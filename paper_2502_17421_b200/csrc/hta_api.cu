@@ -119,7 +119,11 @@ PrefixPlan make_plan(const Shape &sh, int num_sms) {
         // 320 rows = 2.5 x 128 fill 3 single groups at 83 % but 2 pair groups at 63 %).
         auto layout = [&](int nt, int *S_out) {
             const int mg = (pl.M + 128 * nt - 1) / (128 * nt);
+#ifdef HTA_Q2
+            const int ctas = s.B * s.H_kv * mg;  // experiment: one CTA holds both 128-row tiles
+#else
             const int ctas = s.B * s.H_kv * mg * nt;  // CTAs per split (a pair is two CTAs, two SMs)
+#endif
             double cost = 0.0;
             *S_out = s.num_splits > 0 ? s.num_splits : best_splits(ctas, std::max(pl.n_tiles, 1), num_sms, &cost);
             return cost;
@@ -282,7 +286,11 @@ hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, co
             if ((r = make_pool_map(&tv, v, s, *pg)) != HTA_OK) return r;
         } else {
             // a CTA of a pair loads half of each K tile (96 keys) and half of each V tile (64 columns)
+#ifdef HTA_Q2
+            if ((r = make_kv_map(&tk, k, s, kBlockN)) != HTA_OK) return r;
+#else
             if ((r = make_kv_map(&tk, k, s, pl.nt == 2 ? kBlockN / 2 : kBlockN)) != HTA_OK) return r;
+#endif
             if ((r = make_kv_map(&tv, v, s, kBlockN)) != HTA_OK) return r;
         }
         CUtensorMap tq;

@@ -35,6 +35,7 @@
 // A split with no visible key writes the sentinel (O = 0, LSE = -inf).
 #include <cuda_bf16.h>
 #include <cstdio>
+#include <type_traits>
 
 #include "hta_internal.h"
 #include "ptx_sm100.cuh"
@@ -638,7 +639,12 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 // would co-limit the MMAs).  P packed (2 bf16 per column): keys [Ch, Ch + C) ->
                 // columns [Ch/2, Ch/2 + C/2) (C = kHalfCols, h = chalf), stored in 16-column
                 // chunks without waiting (one wait::st before P is published).
-                auto exp_store = [&](float m_use) {
+                // xmax_poly: max exponent argument of the polynomial slots (their 2^j would wrap
+                // past 2^127 instead of saturating like MUFU's ex2); tracked on the speculative
+                // pass only, where an argument above 60 forces the redo anyway.
+                float xmax_poly = -INFINITY;
+                auto exp_store = [&](float m_use, auto spec) {
+                    constexpr bool kSpec = decltype(spec)::value;
                     const float2 c2 = make_float2(c, c), neg2 = make_float2(-m_use, -m_use);
                     float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
                     const float2 *s2 = reinterpret_cast<const float2 *>(s);
@@ -648,7 +654,8 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                         const float2 x = __ffma2_rn(s2[i], c2, neg2);
                         float2 pp;
                         if ((i & 7) < HTA_POLY) {
-                            pp = exp2_poly2(x);
+                            if (kSpec) xmax_poly = max3f(xmax_poly, x.x, x.y);
+                            pp = exp2_poly2<!kSpec>(x);
                         } else {
                             pp.x = fast_exp2(x.x);
                             pp.y = fast_exp2(x.y);
@@ -689,19 +696,19 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 // sum checks; otherwise (always on the first tile, where m_run = -inf) the warp
                 // redoes the tile with the true row max.
                 HTA_TR(11, sw, j);
-                lsum = exp_store(m_run);
+                lsum = exp_store(m_run, std::true_type{});
                 mt = m_run;
-                if (__any_sync(0xffffffffu, !(lsum <= 0x1p60f))) {
+                if (__any_sync(0xffffffffu, !(lsum <= 0x1p60f) || xmax_poly > 60.f)) {
                     tmem_st_wait();  // the speculative P stores land before they are overwritten
                     const float mx = row_max();
                     mt = mx > m_run ? mx : m_run;
-                    lsum = exp_store(mt);
+                    lsum = exp_store(mt, std::false_type{});
                 }
 #else
                 const float mx = row_max();
                 HTA_TR(11, sw, j);
                 mt = (mx > m_run + 8.0f) ? mx : m_run;  // stale max: rescale only on a jump > 2^8
-                lsum = exp_store(mt);
+                lsum = exp_store(mt, std::false_type{});
 #endif
             } else {
                 if (kDefer && j > 0) publish(j - 1);

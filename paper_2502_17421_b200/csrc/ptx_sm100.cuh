@@ -595,6 +595,13 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return r;
 }
 
+// max of three floats in one FMNMX3
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+    float y;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(y) : "f"(a), "f"(b), "f"(c));
+    return y;
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -604,11 +611,20 @@ __device__ __forceinline__ float fast_exp2(float x) {
 // 2^x for a pair of floats on the FMA pipe (no MUFU): x = j + f with j = round(x) taken from
 // the mantissa of x + 1.5*2^23, f in [-0.5, 0.5], 2^f by a degree-3 polynomial (max relative
 // error 7.5e-5, far below the bf16 rounding of P), and 2^j added into the exponent field.
-// Inputs below -126 are clamped (their weight is < 2^-126, i.e. zero for the softmax).
+// Inputs are clamped to [-126, 126]: below, the weight is < 2^-126 (zero for the softmax);
+// above, 2^j would wrap the exponent field into the sign bit and turn an overflow into a tiny
+// negative P that the prefix kernel's speculative-max check (row sum > 2^60) cannot see -- with
+// the clamp an overflowing x gives 2^126, like the MUFU path's +inf caught by that check.
+template <bool kClampHigh = true>
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
     const float kMagic = 12582912.0f;  // 1.5 * 2^23
-    x.x = fmaxf(x.x, -126.0f);
-    x.y = fmaxf(x.y, -126.0f);
+    if (kClampHigh) {
+        x.x = fminf(fmaxf(x.x, -126.0f), 126.0f);
+        x.y = fminf(fmaxf(x.y, -126.0f), 126.0f);
+    } else {  // the caller detects x > 126 itself (max3 below) and discards the result
+        x.x = fmaxf(x.x, -126.0f);
+        x.y = fmaxf(x.y, -126.0f);
+    }
     const float2 t = __fadd2_rn(x, make_float2(kMagic, kMagic));
     const float2 r = __fadd2_rn(t, make_float2(-kMagic, -kMagic));
     const float2 f = __ffma2_rn(r, make_float2(-1.0f, -1.0f), x);

@@ -262,3 +262,29 @@ def test_step_in_cuda_graph_matches_eager(cuda_device):
     torch.cuda.synchronize()
     for name, a, b in zip(("o", "lse", "path", "path_len", "bonus"), (o, lse, path, plen, bonus), ref):
         assert torch.equal(a, b), f"{name}: max |diff| {(a.float() - b.float()).abs().max().item()}"
+
+
+@pytest.mark.parametrize("key", [192 + 2, 192 + 96 + 17, 192 + 9, 384 + 50, 3])
+@pytest.mark.parametrize("d", [128, 64])
+def test_logit_jump_past_exp_range(cuda_device, key, d):
+    """One prefix key whose logit exceeds the running max of the earlier tiles by ~150 (natural
+    units, 2^216 in P): the speculative exponentials overflow and the tile is redone with the
+    true max (prefix_tc.cu).  The key positions put the jump into polynomial and
+    MUFU exp slots of both column halves, in tiles 0-2 of one split (Z4 max-shifting: the result
+    must still equal the fp64 softmax)."""
+    B, T, H, Hkv, N = 1, 4, 4, 1, 576
+    gen = named_generator(11, f"jump:{key}:{d}")
+    u = torch.randn(d, generator=gen)
+    u = u / u.norm()
+    q = (40.0 * u + 0.5 * torch.randn(B, T, H, d, generator=gen)).to(torch.bfloat16)
+    kc = torch.randn(B, N, Hkv, d, generator=gen)
+    kc[:, key, :, :] = 42.5 * u + 0.1 * kc[:, key, :, :]  # logit ~150 (d=128) / ~205 (d=64)
+    kc = kc.to(torch.bfloat16)
+    vc = torch.randn(B, N, Hkv, d, generator=gen).to(torch.bfloat16)
+    kt = torch.zeros(B, T, Hkv, d, dtype=torch.bfloat16)
+    mask = np.ones((B, T, T), np.uint8)
+    oc_ref, lc_ref = oracle.attention(q, kc, vc, kt, kt, mask, part="cache")
+    for splits in (1, 2):
+        oc, lc = hta.hta_prefix_attn(q.to(cuda_device), kc.to(cuda_device), vc.to(cuda_device), num_splits=splits)
+        torch.cuda.synchronize()
+        compare(oc, lc, oc_ref, lc_ref, "bf16", f"prefix (S={splits})")
