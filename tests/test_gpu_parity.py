@@ -265,8 +265,8 @@ def test_step_in_cuda_graph_matches_eager(cuda_device):
 
 
 @pytest.mark.parametrize("key", [192 + 2, 192 + 96 + 17, 192 + 9, 384 + 50, 3])
-@pytest.mark.parametrize("d", [128, 64])
-def test_logit_jump_past_exp_range(cuda_device, key, d):
+@pytest.mark.parametrize("d,dtype", [(128, "bf16"), (64, "bf16"), (128, "fp32")])
+def test_logit_jump_past_exp_range(cuda_device, key, d, dtype):
     """One prefix key whose logit exceeds the running max of the earlier tiles by ~150 (natural
     units, 2^216 in P): the speculative exponentials overflow and the tile is redone with the
     true max (prefix_tc.cu).  The key positions put the jump into polynomial and
@@ -276,15 +276,43 @@ def test_logit_jump_past_exp_range(cuda_device, key, d):
     gen = named_generator(11, f"jump:{key}:{d}")
     u = torch.randn(d, generator=gen)
     u = u / u.norm()
-    q = (40.0 * u + 0.5 * torch.randn(B, T, H, d, generator=gen)).to(torch.bfloat16)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    q = (40.0 * u + 0.5 * torch.randn(B, T, H, d, generator=gen)).to(tdt)
     kc = torch.randn(B, N, Hkv, d, generator=gen)
     kc[:, key, :, :] = 42.5 * u + 0.1 * kc[:, key, :, :]  # logit ~150 (d=128) / ~205 (d=64)
-    kc = kc.to(torch.bfloat16)
-    vc = torch.randn(B, N, Hkv, d, generator=gen).to(torch.bfloat16)
-    kt = torch.zeros(B, T, Hkv, d, dtype=torch.bfloat16)
+    kc = kc.to(tdt)
+    vc = torch.randn(B, N, Hkv, d, generator=gen).to(tdt)
+    kt = torch.zeros(B, T, Hkv, d, dtype=tdt)
     mask = np.ones((B, T, T), np.uint8)
     oc_ref, lc_ref = oracle.attention(q, kc, vc, kt, kt, mask, part="cache")
     for splits in (1, 2):
         oc, lc = hta.hta_prefix_attn(q.to(cuda_device), kc.to(cuda_device), vc.to(cuda_device), num_splits=splits)
         torch.cuda.synchronize()
-        compare(oc, lc, oc_ref, lc_ref, "bf16", f"prefix (S={splits})")
+        compare(oc, lc, oc_ref, lc_ref, dtype, f"prefix (S={splits})")
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_tree_logit_far_above_prefix(cuda_device, dtype):
+    """A tree key whose logit exceeds every prefix logit by ~150 (and rows whose tree part is
+    far BELOW the prefix): the LSE merge must weight the parts by exp of LSE
+    differences far outside the fp32 exp range without overflow (Z4)."""
+    B, T, H, Hkv, d, N = 2, 6, 4, 2, 128, 700
+    gen = named_generator(12, f"treejump:{dtype}")
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    u = torch.randn(d, generator=gen)
+    u = u / u.norm()
+    q = (40.0 * u + 0.5 * torch.randn(B, T, H, d, generator=gen)).to(tdt)
+    kc = torch.randn(B, N, Hkv, d, generator=gen)
+    kt = torch.randn(B, T, Hkv, d, generator=gen)
+    kt[0, 2] = 42.5 * u          # batch 0: tree node 2 dominates the rows that see it
+    kc[1, 123] = 42.5 * u        # batch 1: a prefix key dominates, the tree part is ~150 below
+    q, kc, kt = q.to(tdt), kc.to(tdt), kt.to(tdt)
+    vc = torch.randn(B, N, Hkv, d, generator=gen).to(tdt)
+    vt = torch.randn(B, T, Hkv, d, generator=gen).to(tdt)
+    parents = torch.stack([torch.tensor([-1, 0, 0, 1, 2, 2], dtype=torch.int32)] * B)
+    mask = np.stack([oracle.tree_mask(parents[b]) for b in range(B)])
+    o_ref, l_ref = oracle.attention(q, kc, vc, kt, vt, mask)
+    x = [t.to(cuda_device) for t in (q, kc, vc, kt, vt)]
+    o, l = hta.hta_forward(*x, torch.from_numpy(mask).to(cuda_device))
+    torch.cuda.synchronize()
+    compare(o, l, o_ref, l_ref, dtype, "forward")
