@@ -1,3 +1,5 @@
+"""Diagnostics: per-row prefix errors vs the oracle for a few shapes and forced split counts (used
+to localise the polynomial-exp overflow; run against variant libraries via tools/lib_variants.sh)."""
 import sys; sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
 import numpy as np, torch
 import oracle
