@@ -92,6 +92,9 @@ __device__ __forceinline__ uint64_t trace_globaltimer() {
 #ifndef HTA_SPEC_MAX
 #define HTA_SPEC_MAX 1
 #endif
+#ifndef HTA_PAGED_SPEC
+#define HTA_PAGED_SPEC 0
+#endif
 #ifndef HTA_RING_KB
 #define HTA_RING_KB 192
 #endif
@@ -315,6 +318,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 const int slot = j % C::kSlotsK;
                 if (lane == 0) mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);
                 __syncwarp();
+                HTA_TR(30, 0, j);
                 uint8_t *dst = sK + slot * C::kKBytes;
                 if (lane == 0) {
                     if (PAIR) {
@@ -372,6 +376,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 const int slot = j % C::kSlotsV;
                 if (lane == 0) mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
                 __syncwarp();
+                HTA_TR(31, 0, j);
                 uint8_t *dst = sV + slot * C::kVBytes;
                 if (lane == 0) {
                     if (PAIR) {
@@ -689,27 +694,31 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
                     return fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16)) * c;
                 };
-#if HTA_SPEC_MAX
-                // Speculative exponentials with the running max: no row-max reduction on the
-                // critical path.  Exact as long as no P exceeds 2^60 (bf16 P and the fp32 O / row
-                // sums have the range; floating point keeps the relative precision), which the row
-                // sum checks; otherwise (always on the first tile, where m_run = -inf) the warp
-                // redoes the tile with the true row max.
-                HTA_TR(11, sw, j);
-                lsum = exp_store(m_run, std::true_type{});
-                mt = m_run;
-                if (__any_sync(0xffffffffu, !(lsum <= 0x1p60f) || xmax_poly > 60.f)) {
-                    tmem_st_wait();  // the speculative P stores land before they are overwritten
+                if (HTA_SPEC_MAX && (p.page_size == 0 || HTA_PAGED_SPEC)) {
+                    // Speculative exponentials with the running max: no row-max reduction on the
+                    // critical path.  Exact as long as no P exceeds 2^60 (bf16 P and the fp32 O /
+                    // row sums have the range; floating point keeps the relative precision), which
+                    // the row sum checks; otherwise (always on the first tile, where m_run = -inf)
+                    // the warp redoes the tile with the true row max.
+                    HTA_TR(11, sw, j);
+                    lsum = exp_store(m_run, std::true_type{});
+                    mt = m_run;
+                    if (__any_sync(0xffffffffu, !(lsum <= 0x1p60f) || xmax_poly > 60.f)) {
+                        tmem_st_wait();  // the speculative P stores land before they are overwritten
+                        const float mx = row_max();
+                        mt = mx > m_run ? mx : m_run;
+                        lsum = exp_store(mt, std::false_type{});
+                    }
+                } else {
+                    // Row max first, stale max (rescale only on a jump > 2^8).  The paged cache
+                    // uses this order: with 16-row TMA boxes the faster speculative softmax drove
+                    // the pipeline into V-starved tiles (163 vs 89 us on Llama-8B-64k, 16-key
+                    // pages; profiles/r01b/README.md).
                     const float mx = row_max();
-                    mt = mx > m_run ? mx : m_run;
+                    HTA_TR(11, sw, j);
+                    mt = (mx > m_run + 8.0f) ? mx : m_run;
                     lsum = exp_store(mt, std::false_type{});
                 }
-#else
-                const float mx = row_max();
-                HTA_TR(11, sw, j);
-                mt = (mx > m_run + 8.0f) ? mx : m_run;  // stale max: rescale only on a jump > 2^8
-                lsum = exp_store(mt, std::false_type{});
-#endif
             } else {
                 if (kDefer && j > 0) publish(j - 1);
                 mt = 0.f;

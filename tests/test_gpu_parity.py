@@ -269,7 +269,7 @@ def test_step_in_cuda_graph_matches_eager(cuda_device):
 def test_logit_jump_past_exp_range(cuda_device, key, d, dtype):
     """One prefix key whose logit exceeds the running max of the earlier tiles by ~150 (natural
     units, 2^216 in P): the speculative exponentials overflow and the tile is redone with the
-    true max (prefix_tc.cu, DESIGN.md §6.2).  The key positions put the jump into polynomial and
+    true max (prefix_tc.cu, DESIGN.md §6.1).  The key positions put the jump into polynomial and
     MUFU exp slots of both column halves, in tiles 0-2 of one split (Z4 max-shifting: the result
     must still equal the fp64 softmax)."""
     B, T, H, Hkv, N = 1, 4, 4, 1, 576

@@ -28,21 +28,29 @@ def main():
     w = config_workload(name, seed=0)
     x = [t.to(dev) for t in (w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree)]
     mask = hta.hta_build_tree_mask(w.parents[0].to(dev))
+    fwd = lambda: hta.hta_forward(*x, mask)  # noqa: E731
+    if os.environ.get("PAGED"):  # the paged forward over in-order 16-key pages
+        page = 16
+        maxp = w.N // page
+        kp = x[1].reshape(w.B * maxp, page, w.H_kv, w.d).contiguous()
+        vp = x[2].reshape(w.B * maxp, page, w.H_kv, w.d).contiguous()
+        bt = torch.arange(w.B * maxp, dtype=torch.int32, device=dev).view(w.B, maxp)
+        fwd = lambda: hta.hta_forward_paged(x[0], kp, vp, bt, x[3], x[4], mask)  # noqa: E731
     L = hta.lib()
     L.hta_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
     L.hta_debug_cta_times.argtypes = [ctypes.c_void_p]
     buf = torch.zeros(32 * 2048, dtype=torch.int64, device=dev)
-    hta.hta_forward(*x, mask)
+    fwd()
     torch.cuda.synchronize()
     assert L.hta_debug_set_trace(ctypes.c_void_p(buf.data_ptr()), cta) == 0
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     warm = int(os.environ.get("TRACE_WARM", "0"))  # back-to-back launches first (sustained load)
     for _ in range(3):
         for _ in range(warm):
-            hta.hta_forward(*x, mask)
+            fwd()
         buf.zero_()
         flush.zero_()  # cold L2, as in bench.py
-        hta.hta_forward(*x, mask)
+        fwd()
         torch.cuda.synchronize()
     times = (ctypes.c_uint64 * 8192)()
     if L.hta_debug_cta_times(times) == 0:
