@@ -159,9 +159,8 @@ hta_status_t hta_forward_timed(const hta_shape_t *shape, const void *q, const vo
  *                   block_table[b][k / page_size], row k % page_size.  Entries past the pages a
  *                   batch uses are not read for valid keys (negative ones read page 0, masked).
  *   shape->N_max    ignored (the logical capacity is max_pages * page_size); kv_strides ignored.
- * The result equals hta_forward on the gathered contiguous cache up to rounding: the same tiles
- * in the same order, but the softmax takes each tile's row max before its exponentials (the
- * contiguous pass speculates with the running max). */
+ * The result equals hta_forward on the gathered contiguous cache (the same tiles in the same
+ * order: bit-identical). */
 hta_status_t hta_forward_paged(const hta_shape_t *shape, const void *q, const void *k_pool,
                                const void *v_pool, int32_t num_pages, int32_t page_size,
                                const int32_t *block_table, int32_t max_pages,

@@ -92,8 +92,13 @@ __device__ __forceinline__ uint64_t trace_globaltimer() {
 #ifndef HTA_SPEC_MAX
 #define HTA_SPEC_MAX 1
 #endif
-#ifndef HTA_PAGED_SPEC
-#define HTA_PAGED_SPEC 0
+// Diagnostics: 1 = the contiguous-cache producers loop with the whole warp waiting on each
+// mbarrier (+2 us on Llama-8B-64k); 0 = lane 0 alone loops (the other lanes are parked at the
+// __syncwarp after the loop).  The paged producers always wait converged: their lanes take part
+// in every tile (block-table lookups, shuffles), and a lane-0-only wait with the other 31 lanes
+// at a per-tile __syncwarp made the paged pass 2x slower (profiles/r01b/README.md).
+#ifndef HTA_CONV
+#define HTA_CONV 0
 #endif
 #ifndef HTA_RING_KB
 #define HTA_RING_KB 192
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 const int n0 = static_cast<int>(key_lo) + j * kBlockN + (PAIR ? static_cast<int>(rank) * C::kKRows : 0);
                 const int prow = paged_row(p, b, n0 + 16 * (lane < kBoxes ? lane : 0));
                 const int slot = j % C::kSlotsK;
-                if (lane == 0) mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);
+                mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);  // the whole warp waits (converged)
                 __syncwarp();
                 HTA_TR(30, 0, j);
                 uint8_t *dst = sK + slot * C::kKBytes;
@@ -342,7 +347,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     }
                 }
             }
-        } else if (lane == 0 && HTA_SKIP < 3) {
+        } else if ((HTA_CONV || lane == 0) && HTA_SKIP < 3) {
             const uint32_t kfull0 = PAIR ? mapa_shared(smem_u32(&k_full[0]), 0) : 0u;
             for (int j = 0; j < n_tiles; ++j) {
                 const int n0 = static_cast<int>(key_lo) + j * kBlockN;
@@ -350,7 +355,8 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);
                 uint8_t *dst = sK + slot * C::kKBytes;
                 HTA_TR(30, 0, j);
-                if (PAIR) {
+                if (lane != 0) {
+                } else if (PAIR) {
                     if (leader) mbar_arrive_expect_tx(&k_full[slot], 2u * C::kKBytes);
 #pragma unroll
                     for (int kb = 0; kb < C::kKB; ++kb)
@@ -362,6 +368,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     for (int kb = 0; kb < C::kKB; ++kb)
                         tma_load_4d(dst + kb * (kBlockN * 128), &tmap_k, &k_full[slot], kb * 64, g, n0, b, kKvPolicy);
                 }
+                if (HTA_CONV) __syncwarp();
             }
         }
         __syncwarp();
@@ -374,7 +381,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 const int n0 = static_cast<int>(key_lo) + j * kBlockN;
                 const int prow = paged_row(p, b, n0 + 16 * (lane < kBoxes ? lane : 0));
                 const int slot = j % C::kSlotsV;
-                if (lane == 0) mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
+                mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
                 __syncwarp();
                 HTA_TR(31, 0, j);
                 uint8_t *dst = sV + slot * C::kVBytes;
@@ -401,7 +408,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     }
                 }
             }
-        } else if (lane == 0 && HTA_SKIP < 3) {
+        } else if ((HTA_CONV || lane == 0) && HTA_SKIP < 3) {
             const uint32_t vfull0 = PAIR ? mapa_shared(smem_u32(&v_full[0]), 0) : 0u;
             for (int j = 0; j < n_tiles; ++j) {
                 const int n0 = static_cast<int>(key_lo) + j * kBlockN;
@@ -409,7 +416,8 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
                 uint8_t *dst = sV + slot * C::kVBytes;
                 HTA_TR(31, 0, j);
-                if (PAIR) {
+                if (lane != 0) {
+                } else if (PAIR) {
                     if (leader) mbar_arrive_expect_tx(&v_full[slot], 2u * C::kVBytes);
                     tma_load_4d_pair(dst, &tmap_v, vfull0 + 8u * slot, static_cast<int>(rank) * 64, g, n0, b,
                                      kKvPolicy);
@@ -419,6 +427,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     for (int kb = 0; kb < C::kKB; ++kb)
                         tma_load_4d(dst + kb * (kBlockN * 128), &tmap_v, &v_full[slot], kb * 64, g, n0, b, kKvPolicy);
                 }
+                if (HTA_CONV) __syncwarp();
             }
         }
         __syncwarp();
@@ -694,7 +703,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
                     return fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16)) * c;
                 };
-                if (HTA_SPEC_MAX && (p.page_size == 0 || HTA_PAGED_SPEC)) {
+                if (HTA_SPEC_MAX) {
                     // Speculative exponentials with the running max: no row-max reduction on the
                     // critical path.  Exact as long as no P exceeds 2^60 (bf16 P and the fp32 O /
                     // row sums have the range; floating point keeps the relative precision), which
@@ -710,10 +719,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                         lsum = exp_store(mt, std::false_type{});
                     }
                 } else {
-                    // Row max first, stale max (rescale only on a jump > 2^8).  The paged cache
-                    // uses this order: with 16-row TMA boxes the faster speculative softmax drove
-                    // the pipeline into V-starved tiles (163 vs 89 us on Llama-8B-64k, 16-key
-                    // pages; profiles/r01b/README.md).
+                    // row max first, stale max (rescale only on a jump > 2^8): -DHTA_SPEC_MAX=0
                     const float mx = row_max();
                     HTA_TR(11, sw, j);
                     mt = (mx > m_run + 8.0f) ? mx : m_run;

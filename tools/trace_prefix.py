@@ -57,10 +57,10 @@ def main():
         n_cta = 0
         rows = []
         for i in range(1024):
-            e, ls, clk, x, ep, ms, me, _ = times[8 * i: 8 * i + 8]
+            e, ls, clk, x = times[4 * i: 4 * i + 4]  # g_cta_times[1024][4] (prefix_tc.cu)
             if e == 0 or x == 0:
                 break
-            rows.append((e, ls, clk, x, ep, ms, me))
+            rows.append((e, ls, clk, x))
         t0 = min(r[0] for r in rows)
         ent = [(r[0] - t0) / 1e3 for r in rows]
         pro = [(r[1] - r[0]) / 1e3 for r in rows]
@@ -71,6 +71,9 @@ def main():
         print(f"{len(rows)} CTAs: entry spread {max(ent):.1f} us; prologue {statistics.mean(pro):.1f} us "
               f"(max {max(pro):.1f}); exit min {min(ext):.1f} median {statistics.median(ext):.1f} max {max(ext):.1f} us; "
               f"SM clock {statistics.median(mhz):.0f} MHz")
+        q = sorted(ext)
+        print("exit quantiles (us): " + " ".join(f"p{p}={q[min(len(q) - 1, len(q) * p // 100)]:.1f}"
+                                               for p in (10, 25, 50, 75, 90, 100)))
     recs = []
     for warp, row in enumerate(buf.view(32, 2048).cpu().tolist()):
         for v in row:
