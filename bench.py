@@ -361,7 +361,15 @@ def main():
         # (3) end to end through the public API: per-step inputs H2D from pinned host memory,
         # result (O + accepted path) D2H; the KV cache is resident model state.
         e2e_times = timed(lambda i: run_e2e(), args.steps)
+        # The timed regions last a few ms, below the sampler's 20 ms period: replay the same step
+        # (untimed) for ~0.3 s so that clocks and throttle reasons are also sampled under load.
+        n_hold = max(1, int(0.3 / max(statistics.mean(times) * 1e-3, 1e-5)))
+        for _ in range(n_hold):
+            run_step()
+        torch.cuda.synchronize()
     clocks = clk.summary()
+    clocks["note"] = ("median SM clock over the samples under load (GPU utilisation >= 50 %); the sampler also "
+                      f"covers a {n_hold}-step untimed replay of the same step right after the timed regions")
 
     t_ms = max_over_ranks(statistics.mean(times))
     e2e_ms = max_over_ranks(statistics.mean(e2e_times))
