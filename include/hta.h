@@ -240,6 +240,19 @@ hta_status_t hta_comm_create(const void *unique_id_128, int32_t nranks, int32_t 
                              hta_comm_t *comm);
 hta_status_t hta_comm_destroy(hta_comm_t comm);
 
+/* Loopback communicator: `nranks` VIRTUAL ranks held by this one process on the current device
+ * (no NCCL).  It drives hta_forward_seqpar_loopback, which runs every rank's phases of the
+ * sequence-parallel step (local prefix pass into destination-major blocks, the all-to-all of
+ * head slices -- here device-to-device copies --, the P-way merge with the tree pass at rank r's
+ * head offset r*H/P, the optional all-gather) on one GPU.  It exists so that the P > 1 data
+ * path can be checked against the oracle where only one GPU is available.  1 <= nranks <= 64. */
+hta_status_t hta_comm_create_loopback(int32_t nranks, hta_comm_t *comm);
+
+/* HTA_OK, or HTA_ERR_NCCL if NCCL reported an asynchronous error on this communicator
+ * (ncclCommGetAsyncError; e.g. a peer failed during an earlier step).  hta_forward_seqpar checks
+ * it before enqueueing.  A loopback communicator always returns HTA_OK. */
+hta_status_t hta_comm_async_error(hta_comm_t comm);
+
 /* Workspace for hta_forward_seqpar: split partials + send/receive buffers. */
 size_t hta_workspace_size_seqpar(const hta_shape_t *shape_local, int32_t num_sms,
                                  int32_t nranks);
@@ -258,6 +271,27 @@ hta_status_t hta_forward_seqpar(hta_comm_t comm, const hta_shape_t *shape_local,
                                 int64_t mask_batch_stride, void *o, float *lse_out,
                                 int32_t gather_output, void *ws, size_t ws_bytes,
                                 hta_stream_t stream);
+
+/* hta_forward_seqpar for all ranks of a loopback communicator at once, on `stream` of the
+ * current device.  Per-rank arguments are HOST arrays of `nranks` DEVICE pointers:
+ *   k_cache_local[r], v_cache_local[r], cache_seqlens_local[r] (the array itself may be NULL:
+ *   full slices)   rank r's KV slice, as for hta_forward_seqpar on rank r
+ *   o[r], lse_out[r] (lse_out may be NULL)   rank r's outputs (head slice r, or all heads when
+ *   gather_output)
+ *   ws, ws_bytes   nranks x the 16-byte rounded hta_workspace_size_seqpar(shape_local, ...)
+ * q, k_tree, v_tree and mask are shared by the ranks (they are replicated in the real step).
+ * The per-rank computation is the same code as hta_forward_seqpar's; only the exchange is a
+ * local copy instead of NCCL.  Errors: as hta_forward_seqpar; HTA_ERR_INVALID_ARGUMENT for an
+ * NCCL communicator. */
+hta_status_t hta_forward_seqpar_loopback(hta_comm_t comm, const hta_shape_t *shape_local,
+                                         const void *q, const void *const *k_cache_local,
+                                         const void *const *v_cache_local,
+                                         const int32_t *const *cache_seqlens_local,
+                                         const void *k_tree, const void *v_tree,
+                                         const uint8_t *mask, int64_t mask_batch_stride,
+                                         void *const *o, float *const *lse_out,
+                                         int32_t gather_output, void *ws, size_t ws_bytes,
+                                         hta_stream_t stream);
 
 #ifdef __cplusplus
 }

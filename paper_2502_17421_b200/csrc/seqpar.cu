@@ -1,18 +1,27 @@
-// seqpar.cu -- sequence-parallel Hybrid Tree Attention over NCCL (one process per GPU).
+// seqpar.cu -- sequence-parallel Hybrid Tree Attention (one process per GPU, or P virtual ranks
+// of one process on one GPU: the loopback communicator).
 //
 // The prefix KV is sharded contiguously along the sequence; rank r computes the prefix pass on
 // its slice (split-KV on its own SMs), combines its splits into ONE partial per query row laid
-// out destination-major [P][B][T][H/P][d] (+ LSE), exchanges the head slices with a grouped
-// ncclSend/ncclRecv all-to-all (the only cross-device step), and merges the P received prefix
-// partials with the tree partial of its own H/P heads.  Exactness: Appendix C applied P+1 ways
-// (PAPER.md:662-671).  The paper runs on one GPU; this exchange is new here.
+// out destination-major [P][B][T][H/P][d] (+ LSE), exchanges the head slices all-to-all (the only
+// cross-rank step), and merges the P received prefix partials with the tree partial of its own
+// H/P heads.  Exactness: Appendix C applied P+1 ways.  The paper runs on one
+// GPU; this exchange is new here.
 //
-// NCCL is resolved at hta_comm_create time with dlopen("libnccl.so.2") so libhta has no
-// link-time NCCL dependency; inside a PyTorch process this finds the NCCL torch already loaded.
+// Every rank runs the same three per-rank phases (local parts -> exchange -> final merge, then
+// the optional all-gather + reassembly); only the transport of the exchange differs:
+//  * NCCL: a grouped ncclSend/ncclRecv all-to-all over NVLink (ncclAllGather for the output).
+//    NCCL is resolved with dlopen("libnccl.so.2") at hta_comm_create, so libhta has no link-time
+//    NCCL dependency; inside a PyTorch process this finds the NCCL torch already loaded.
+//  * loopback: all P ranks live in this process on the current device; the exchange is the
+//    same destination-major block copies done with cudaMemcpyAsync.  This runs the P > 1 code
+//    (destination-major send layout, rank > 0 head offsets, P-way final merge, reassembly) on
+//    one GPU, which is how the tests check it against the oracle.
 #include <dlfcn.h>
 
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "hta_internal.h"
 
@@ -32,6 +41,7 @@ struct NcclApi {
     nccl_result_t (*GetUniqueId)(nccl_uid_t *) = nullptr;
     nccl_result_t (*CommInitRank)(nccl_comm_t *, int, nccl_uid_t, int) = nullptr;
     nccl_result_t (*CommDestroy)(nccl_comm_t) = nullptr;
+    nccl_result_t (*CommGetAsyncError)(nccl_comm_t, nccl_result_t *) = nullptr;
     nccl_result_t (*GroupStart)() = nullptr;
     nccl_result_t (*GroupEnd)() = nullptr;
     nccl_result_t (*Send)(const void *, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
@@ -52,18 +62,22 @@ NcclApi &nccl() {
             HTA_SYM(GetUniqueId, "ncclGetUniqueId");
             HTA_SYM(CommInitRank, "ncclCommInitRank");
             HTA_SYM(CommDestroy, "ncclCommDestroy");
+            HTA_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
             HTA_SYM(GroupStart, "ncclGroupStart");
             HTA_SYM(GroupEnd, "ncclGroupEnd");
             HTA_SYM(Send, "ncclSend");
             HTA_SYM(Recv, "ncclRecv");
             HTA_SYM(AllGather, "ncclAllGather");
 #undef HTA_SYM
-            api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.GroupStart && api.GroupEnd &&
-                     api.Send && api.Recv && api.AllGather;
+            api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.CommGetAsyncError &&
+                     api.GroupStart && api.GroupEnd && api.Send && api.Recv && api.AllGather;
         }
     }
     return api;
 }
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+size_t round16(size_t x) { return (x + 15) & ~size_t(15); }
 
 // Per-rank exchange block: O [B][T][Hp][d] followed by LSE [B][Hp][T] (floats).
 size_t block_floats(const hta_shape_t &s, int P) {
@@ -71,14 +85,106 @@ size_t block_floats(const hta_shape_t &s, int P) {
     return size_t(s.B) * s.T * Hp * s.d + size_t(s.B) * Hp * s.T;
 }
 
-size_t round16(size_t x) { return (x + 15) & ~size_t(15); }
+// One rank's workspace, carved in this order (all 16-byte aligned):
+//   prefix split partials | send blocks [P][blk] | receive blocks [P][blk] |
+//   own output slice (O [B,T,Hp,d] dtype, LSE [B,Hp,T]) | gathered slices [P] (O) then [P] (LSE)
+struct RankWs {
+    float *parts;
+    size_t parts_bytes;
+    float *sendb, *recvb;
+    uint8_t *own_o;
+    float *own_l;
+    uint8_t *gat_o, *gat_l;
+};
+
+struct Geometry {
+    hta_shape_t s;
+    int P, Hp;
+    size_t es;        // bytes per output element
+    size_t blk;       // floats per exchange block
+    size_t o_slice;   // bytes of one rank's O head slice
+    size_t l_slice;   // bytes of one rank's LSE head slice
+    size_t ws_bytes;  // workspace per rank
+    int sms;
+};
+
+hta_status_t geometry(const hta_shape_t *shape, int P, int sms, Geometry *g) {
+    if (shape == nullptr || P < 1 || shape->H % P != 0) return HTA_ERR_INVALID_ARGUMENT;
+    const size_t base = hta_workspace_size(shape, sms);
+    if (base == size_t(-1)) return HTA_ERR_INVALID_ARGUMENT;
+    g->s = *shape;
+    g->P = P;
+    g->Hp = shape->H / P;
+    g->es = shape->dtype == HTA_BF16 ? 2 : 4;
+    g->blk = block_floats(*shape, P);
+    g->o_slice = size_t(shape->B) * shape->T * g->Hp * shape->d * g->es;
+    g->l_slice = size_t(shape->B) * g->Hp * shape->T * 4;
+    g->sms = sms;
+    g->ws_bytes = round16(base) + 2 * round16(P * g->blk * sizeof(float)) + round16(g->o_slice) +
+                  round16(g->l_slice) + round16(P * g->o_slice) + round16(P * g->l_slice);
+    return HTA_OK;
+}
+
+RankWs carve(const Geometry &g, void *ws) {
+    uint8_t *w = static_cast<uint8_t *>(ws);
+    RankWs r;
+    r.parts = reinterpret_cast<float *>(w);
+    r.parts_bytes = hta_workspace_size(&g.s, g.sms);
+    w += round16(r.parts_bytes);
+    r.sendb = reinterpret_cast<float *>(w);
+    w += round16(g.P * g.blk * sizeof(float));
+    r.recvb = reinterpret_cast<float *>(w);
+    w += round16(g.P * g.blk * sizeof(float));
+    r.own_o = w;
+    w += round16(g.o_slice);
+    r.own_l = reinterpret_cast<float *>(w);
+    w += round16(g.l_slice);
+    r.gat_o = w;
+    w += round16(g.P * g.o_slice);
+    r.gat_l = w;
+    return r;
+}
+
+// Phase 1 of rank r: prefix pass over its slice, splits combined into the destination-major
+// send blocks.
+hta_status_t phase_local(const Geometry &g, const RankWs &w, const void *q, const void *k, const void *v,
+                         const int32_t *seqlens, cudaStream_t st) {
+    return seqpar_local_parts(&g.s, q, k, v, seqlens, w.parts, w.parts_bytes, w.sendb, g.P, st);
+}
+
+// Phase 3 of rank r: the P received prefix partials + the tree pass of heads [r*Hp, (r+1)*Hp).
+hta_status_t phase_merge(const Geometry &g, const RankWs &w, int r, const void *q, const void *kt, const void *vt,
+                         const uint8_t *mask, int64_t mbs, void *o, float *lse, int gather, cudaStream_t st) {
+    void *o_local = gather ? static_cast<void *>(w.own_o) : o;
+    float *l_local = gather ? w.own_l : lse;
+    return seqpar_final_merge(&g.s, g.P, r, q, kt, vt, mask, mbs, w.recvb, g.blk, o_local, l_local, st);
+}
+
+// Phase 4 (gather_output): the P gathered head slices [P][B,T,Hp,d] -> o [B,T,H,d] (and LSE).
+hta_status_t phase_reassemble(const Geometry &g, const RankWs &w, void *o, float *lse, cudaStream_t st) {
+    const hta_shape_t &s = g.s;
+    const size_t row = size_t(g.Hp) * s.d * g.es;
+    for (int p = 0; p < g.P; ++p) {
+        if (cudaMemcpy2DAsync(static_cast<uint8_t *>(o) + p * row, size_t(s.H) * s.d * g.es, w.gat_o + p * g.o_slice,
+                              row, row, size_t(s.B) * s.T, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return HTA_ERR_CUDA;
+        if (lse != nullptr) {
+            const size_t lrow = size_t(g.Hp) * s.T * 4;
+            if (cudaMemcpy2DAsync(reinterpret_cast<uint8_t *>(lse) + p * lrow, size_t(s.H) * s.T * 4,
+                                  w.gat_l + p * g.l_slice, lrow, lrow, size_t(s.B), cudaMemcpyDeviceToDevice,
+                                  st) != cudaSuccess)
+                return HTA_ERR_CUDA;
+        }
+    }
+    return HTA_OK;
+}
 
 }  // namespace
 
 struct hta_comm_s {
-    nccl_comm_t comm;
+    nccl_comm_t comm;  // nullptr for a loopback communicator
     int nranks;
-    int rank;
+    int rank;          // -1 for a loopback communicator (it holds every rank)
 };
 
 extern "C" {
@@ -111,24 +217,39 @@ hta_status_t hta_comm_create(const void *unique_id_128, int32_t nranks, int32_t 
     return HTA_OK;
 }
 
+hta_status_t hta_comm_create_loopback(int32_t nranks, hta_comm_t *comm) {
+    if (comm == nullptr || nranks < 1 || nranks > 64) return HTA_ERR_INVALID_ARGUMENT;
+    hta_comm_s *h = new (std::nothrow) hta_comm_s{nullptr, nranks, -1};
+    if (h == nullptr) return HTA_ERR_INVALID_ARGUMENT;
+    *comm = h;
+    return HTA_OK;
+}
+
 hta_status_t hta_comm_destroy(hta_comm_t comm) {
     if (comm == nullptr) return HTA_ERR_INVALID_ARGUMENT;
-    NcclApi &api = nccl();
     hta_status_t r = HTA_OK;
-    if (api.ok && api.CommDestroy(comm->comm) != 0) r = HTA_ERR_NCCL;
+    if (comm->comm != nullptr) {
+        NcclApi &api = nccl();
+        if (api.ok && api.CommDestroy(comm->comm) != 0) r = HTA_ERR_NCCL;
+    }
     delete comm;
     return r;
 }
 
+hta_status_t hta_comm_async_error(hta_comm_t comm) {
+    if (comm == nullptr) return HTA_ERR_INVALID_ARGUMENT;
+    if (comm->comm == nullptr) return HTA_OK;  // loopback: no asynchronous transport
+    NcclApi &api = nccl();
+    if (!api.ok) return HTA_ERR_NCCL;
+    nccl_result_t async = 0;
+    if (api.CommGetAsyncError(comm->comm, &async) != 0 || async != 0) return HTA_ERR_NCCL;
+    return HTA_OK;
+}
+
 size_t hta_workspace_size_seqpar(const hta_shape_t *shape_local, int32_t num_sms, int32_t nranks) {
-    if (shape_local == nullptr || nranks < 1 || shape_local->H % nranks != 0) return size_t(-1);
-    const size_t base = hta_workspace_size(shape_local, num_sms);
-    if (base == size_t(-1)) return base;
-    const hta_shape_t &s = *shape_local;
-    const size_t blk = block_floats(s, nranks) * sizeof(float);
-    const size_t es = s.dtype == HTA_BF16 ? 2 : 4;
-    const size_t gat = round16(size_t(s.B) * s.T * s.H * s.d * es) + round16(size_t(s.B) * s.H * s.T * 4);
-    return round16(base) + 2 * round16(size_t(nranks) * blk) + 2 * gat;
+    Geometry g;
+    if (geometry(shape_local, nranks, num_sms > 0 ? num_sms : 148, &g) != HTA_OK) return size_t(-1);
+    return g.ws_bytes;
 }
 
 hta_status_t hta_forward_seqpar(hta_comm_t comm, const hta_shape_t *shape_local, const void *q,
@@ -137,50 +258,37 @@ hta_status_t hta_forward_seqpar(hta_comm_t comm, const hta_shape_t *shape_local,
                                 const uint8_t *mask, int64_t mask_batch_stride, void *o, float *lse_out,
                                 int32_t gather_output, void *ws, size_t ws_bytes, hta_stream_t stream) {
     if (comm == nullptr || shape_local == nullptr) return HTA_ERR_INVALID_ARGUMENT;
+    if (comm->comm == nullptr) return HTA_ERR_INVALID_ARGUMENT;  // loopback: hta_forward_seqpar_loopback
+    if (!q || !k_cache_local || !v_cache_local || !k_tree || !v_tree || !mask || !o) return HTA_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q) || !aligned16(k_cache_local) || !aligned16(v_cache_local) || !aligned16(k_tree) ||
+        !aligned16(v_tree) || !aligned16(o) || !aligned16(ws))
+        return HTA_ERR_INVALID_ARGUMENT;
     const int P = comm->nranks, r = comm->rank;
-    if (shape_local->H % P != 0) return HTA_ERR_INVALID_ARGUMENT;
-    const size_t need = hta_workspace_size_seqpar(shape_local, 0, P);
-    if (need == size_t(-1)) return HTA_ERR_INVALID_ARGUMENT;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t need_dev = hta_workspace_size_seqpar(shape_local, sms, P);
-    if (ws == nullptr || ws_bytes < need_dev) return HTA_ERR_WORKSPACE;
-    if (!q || !k_cache_local || !v_cache_local || !k_tree || !v_tree || !mask || !o) return HTA_ERR_INVALID_ARGUMENT;
+    Geometry g;
+    hta_status_t rc = geometry(shape_local, P, sms, &g);
+    if (rc != HTA_OK) return rc;
+    if (ws == nullptr || ws_bytes < g.ws_bytes) return HTA_ERR_WORKSPACE;
     NcclApi &api = nccl();
     if (!api.ok) return HTA_ERR_NCCL;
-
-    hta_shape_t s = *shape_local;
-    const int Hp = s.H / P;
-    const int d = s.d;
-    const size_t es = s.dtype == HTA_BF16 ? 2 : 4;
+    if ((rc = hta_comm_async_error(comm)) != HTA_OK) return rc;  // an earlier step's NCCL failure
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const RankWs w = carve(g, ws);
 
-    // carve the workspace
-    uint8_t *w = static_cast<uint8_t *>(ws);
-    const size_t base = round16(hta_workspace_size(&s, sms));
-    float *prefix_parts = reinterpret_cast<float *>(w);
-    const size_t blk = block_floats(s, P);
-    float *sendb = reinterpret_cast<float *>(w + base);
-    float *recvb = reinterpret_cast<float *>(w + base + round16(P * blk * sizeof(float)));
-    uint8_t *gsend = w + base + 2 * round16(P * blk * sizeof(float));
-    const size_t gat_o = round16(size_t(s.B) * s.T * s.H * d * es);
-    const size_t gat_l = round16(size_t(s.B) * s.H * s.T * 4);
-
-    // 1) local prefix pass -> split partials -> one destination-major partial per row
-    hta_status_t rc = seqpar_local_parts(&s, q, k_cache_local, v_cache_local, cache_seqlens_local, prefix_parts,
-                                         hta_workspace_size(&s, sms), sendb, P, st);
-    if (rc != HTA_OK) return rc;
-    // 2) all-to-all of head slices
-    const size_t own = size_t(r) * blk;
-    if (cudaMemcpyAsync(recvb + own, sendb + own, blk * sizeof(float), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    // 1) local prefix pass -> one destination-major partial per row
+    if ((rc = phase_local(g, w, q, k_cache_local, v_cache_local, cache_seqlens_local, st)) != HTA_OK) return rc;
+    // 2) all-to-all of head slices: block p of sendb goes to rank p, block p of recvb comes from p
+    if (cudaMemcpyAsync(w.recvb + size_t(r) * g.blk, w.sendb + size_t(r) * g.blk, g.blk * sizeof(float),
+                        cudaMemcpyDeviceToDevice, st) != cudaSuccess)
         return HTA_ERR_CUDA;
     if (P > 1) {
         if (api.GroupStart() != 0) return HTA_ERR_NCCL;
         for (int peer = 0; peer < P; ++peer) {
             if (peer == r) continue;
-            if (api.Send(sendb + size_t(peer) * blk, blk, kNcclFloat32, peer, comm->comm, st) != 0 ||
-                api.Recv(recvb + size_t(peer) * blk, blk, kNcclFloat32, peer, comm->comm, st) != 0) {
+            if (api.Send(w.sendb + size_t(peer) * g.blk, g.blk, kNcclFloat32, peer, comm->comm, st) != 0 ||
+                api.Recv(w.recvb + size_t(peer) * g.blk, g.blk, kNcclFloat32, peer, comm->comm, st) != 0) {
                 api.GroupEnd();
                 return HTA_ERR_NCCL;
             }
@@ -188,35 +296,75 @@ hta_status_t hta_forward_seqpar(hta_comm_t comm, const hta_shape_t *shape_local,
         if (api.GroupEnd() != 0) return HTA_ERR_NCCL;
     }
     // 3) merge the P prefix partials with the tree partial of heads [r*Hp, (r+1)*Hp)
-    void *o_local = gather_output ? static_cast<void *>(gsend) : o;
-    float *lse_local = gather_output ? reinterpret_cast<float *>(gsend + gat_o) : lse_out;
-    rc = seqpar_final_merge(&s, P, r, q, k_tree, v_tree, mask, mask_batch_stride, recvb, blk, o_local, lse_local,
-                                st);
-    if (rc != HTA_OK || !gather_output) return rc;
-    // 4) optional all-gather of the head slices, then [P][B,T,Hp,d] -> [B,T,H,d]
-    const size_t o_slice = size_t(s.B) * s.T * Hp * d * es;
-    const size_t l_slice = size_t(s.B) * Hp * s.T * 4;
-    uint8_t *gro = gsend + gat_o + gat_l;
-    uint8_t *grl = gro + round16(P * o_slice);
-    // LSE slice is packed right after the O slice inside gsend (o_local then lse_local).
+    if ((rc = phase_merge(g, w, r, q, k_tree, v_tree, mask, mask_batch_stride, o, lse_out, gather_output, st)) !=
+        HTA_OK)
+        return rc;
+    if (!gather_output) return HTA_OK;
+    // 4) all-gather of the head slices, then [P][B,T,Hp,d] -> [B,T,H,d]
     if (api.GroupStart() != 0) return HTA_ERR_NCCL;
-    if (api.AllGather(gsend, gro, o_slice, kNcclUint8, comm->comm, st) != 0 ||
-        (lse_out != nullptr && api.AllGather(gsend + gat_o, grl, l_slice, kNcclUint8, comm->comm, st) != 0)) {
+    if (api.AllGather(w.own_o, w.gat_o, g.o_slice, kNcclUint8, comm->comm, st) != 0 ||
+        (lse_out != nullptr && api.AllGather(w.own_l, w.gat_l, g.l_slice, kNcclUint8, comm->comm, st) != 0)) {
         api.GroupEnd();
         return HTA_ERR_NCCL;
     }
     if (api.GroupEnd() != 0) return HTA_ERR_NCCL;
-    for (int peer = 0; peer < P; ++peer) {
-        if (cudaMemcpy2DAsync(static_cast<uint8_t *>(o) + size_t(peer) * Hp * d * es, size_t(s.H) * d * es,
-                              gro + peer * o_slice, size_t(Hp) * d * es, size_t(Hp) * d * es, size_t(s.B) * s.T,
-                              cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-            return HTA_ERR_CUDA;
-        if (lse_out != nullptr &&
-            cudaMemcpy2DAsync(reinterpret_cast<uint8_t *>(lse_out) + size_t(peer) * Hp * s.T * 4,
-                              size_t(s.H) * s.T * 4, grl + peer * l_slice, size_t(Hp) * s.T * 4,
-                              size_t(Hp) * s.T * 4, size_t(s.B), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-            return HTA_ERR_CUDA;
+    return phase_reassemble(g, w, o, lse_out, st);
+}
+
+hta_status_t hta_forward_seqpar_loopback(hta_comm_t comm, const hta_shape_t *shape_local, const void *q,
+                                         const void *const *k_cache_local, const void *const *v_cache_local,
+                                         const int32_t *const *cache_seqlens_local, const void *k_tree,
+                                         const void *v_tree, const uint8_t *mask, int64_t mask_batch_stride,
+                                         void *const *o, float *const *lse_out, int32_t gather_output, void *ws,
+                                         size_t ws_bytes, hta_stream_t stream) {
+    if (comm == nullptr || comm->comm != nullptr || shape_local == nullptr) return HTA_ERR_INVALID_ARGUMENT;
+    if (!k_cache_local || !v_cache_local || !o || !q || !k_tree || !v_tree || !mask) return HTA_ERR_INVALID_ARGUMENT;
+    const int P = comm->nranks;
+    for (int r = 0; r < P; ++r) {
+        if (!k_cache_local[r] || !v_cache_local[r] || !o[r]) return HTA_ERR_INVALID_ARGUMENT;
+        if (!aligned16(k_cache_local[r]) || !aligned16(v_cache_local[r]) || !aligned16(o[r]))
+            return HTA_ERR_INVALID_ARGUMENT;
     }
+    if (!aligned16(q) || !aligned16(k_tree) || !aligned16(v_tree) || !aligned16(ws)) return HTA_ERR_INVALID_ARGUMENT;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    Geometry g;
+    hta_status_t rc = geometry(shape_local, P, sms, &g);
+    if (rc != HTA_OK) return rc;
+    const size_t per = round16(g.ws_bytes);
+    if (ws == nullptr || ws_bytes < per * P) return HTA_ERR_WORKSPACE;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    std::vector<RankWs> w(P);
+    for (int r = 0; r < P; ++r) w[r] = carve(g, static_cast<uint8_t *>(ws) + per * r);
+    auto sl = [&](int r) { return cache_seqlens_local ? cache_seqlens_local[r] : nullptr; };
+    auto lse = [&](int r) { return lse_out ? lse_out[r] : nullptr; };
+    for (int r = 0; r < P; ++r)
+        if ((rc = phase_local(g, w[r], q, k_cache_local[r], v_cache_local[r], sl(r), st)) != HTA_OK) return rc;
+    // the all-to-all: block dst of rank src's send buffer -> block src of rank dst's receive buffer
+    for (int dst = 0; dst < P; ++dst)
+        for (int src = 0; src < P; ++src)
+            if (cudaMemcpyAsync(w[dst].recvb + size_t(src) * g.blk, w[src].sendb + size_t(dst) * g.blk,
+                                g.blk * sizeof(float), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+                return HTA_ERR_CUDA;
+    for (int r = 0; r < P; ++r)
+        if ((rc = phase_merge(g, w[r], r, q, k_tree, v_tree, mask, mask_batch_stride, o[r], lse(r), gather_output,
+                              st)) != HTA_OK)
+            return rc;
+    if (!gather_output) return HTA_OK;
+    // the all-gather: rank src's own slice -> slot src of every rank's gather buffer
+    for (int dst = 0; dst < P; ++dst)
+        for (int src = 0; src < P; ++src) {
+            if (cudaMemcpyAsync(w[dst].gat_o + src * g.o_slice, w[src].own_o, g.o_slice, cudaMemcpyDeviceToDevice,
+                                st) != cudaSuccess)
+                return HTA_ERR_CUDA;
+            if (lse_out != nullptr &&
+                cudaMemcpyAsync(w[dst].gat_l + src * g.l_slice, w[src].own_l, g.l_slice, cudaMemcpyDeviceToDevice,
+                                st) != cudaSuccess)
+                return HTA_ERR_CUDA;
+        }
+    for (int r = 0; r < P; ++r)
+        if ((rc = phase_reassemble(g, w[r], o[r], lse(r), st)) != HTA_OK) return rc;
     return HTA_OK;
 }
 

@@ -58,9 +58,14 @@ _SIG = {
     "hta_comm_unique_id": (ctypes.c_int, [_P]),
     "hta_comm_create": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]),
     "hta_comm_destroy": (ctypes.c_int, [_P]),
+    "hta_comm_create_loopback": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]),
+    "hta_comm_async_error": (ctypes.c_int, [_P]),
     "hta_workspace_size_seqpar": (ctypes.c_size_t, [ctypes.POINTER(hta_shape_t), ctypes.c_int32, ctypes.c_int32]),
     "hta_forward_seqpar": (ctypes.c_int, [_P, ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, _P, _P, _P,
                                           ctypes.c_int64, _P, _P, ctypes.c_int32, _P, ctypes.c_size_t, _P]),
+    "hta_forward_seqpar_loopback": (ctypes.c_int, [_P, ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, _P, _P, _P,
+                                                   ctypes.c_int64, _P, _P, ctypes.c_int32, _P, ctypes.c_size_t,
+                                                   _P]),
 }
 
 
@@ -152,6 +157,17 @@ def _workspace(shape: hta_shape_t, device, ws: Optional[torch.Tensor]) -> torch.
     return new_workspace(shape, device) if ws is None else ws
 
 
+def _hold(stream, *temps):
+    """Temporaries created here whose pointers were enqueued on a caller-given `stream`: mark them
+    in use on that stream, so the caching allocator does not hand their memory to other work
+    before the kernels have run."""
+    if stream is None:
+        return
+    for t in temps:
+        if t is not None and t.is_cuda:
+            t.record_stream(stream)
+
+
 def _out_like_q(q: torch.Tensor, o: Optional[torch.Tensor]) -> torch.Tensor:
     """The ABI writes O with q's strides (hta_shape_t.q_strides): allocate it that way."""
     if o is None:
@@ -172,10 +188,12 @@ def hta_prefix_attn(q, k_cache, v_cache, cache_seqlens=None, o_part=None, lse_pa
         o_part = torch.empty(B, T, H, d, dtype=torch.float32, device=q.device)
     if lse_part is None:
         lse_part = torch.empty(B, H, T, dtype=torch.float32, device=q.device)
+    ws_given = ws
     ws = _workspace(shape, q.device, ws)
     _check("hta_prefix_attn", lib().hta_prefix_attn(ctypes.byref(shape), _ptr(q), _ptr(k_cache), _ptr(v_cache),
                                                     _ptr(cache_seqlens), _ptr(o_part), _ptr(lse_part), _ptr(ws),
                                                     ws.numel() * ws.element_size(), _stream(stream)))
+    _hold(stream, None if ws is ws_given else ws)
     return o_part, lse_part
 
 
@@ -203,9 +221,10 @@ def hta_merge_lse(o_parts, lse_parts, dtype=torch.bfloat16, o=None, lse_out=None
     shape = make_shape(o, H_kv=H_kv or H)
     if want_lse and lse_out is None:
         lse_out = torch.empty(B, H, T, dtype=torch.float32, device=o_parts.device)
-    _check("hta_merge_lse", lib().hta_merge_lse(ctypes.byref(shape), n, _ptr(o_parts.contiguous()),
-                                                _ptr(lse_parts.contiguous()), _ptr(o), _ptr(lse_out),
+    oc, lc = o_parts.contiguous(), lse_parts.contiguous()
+    _check("hta_merge_lse", lib().hta_merge_lse(ctypes.byref(shape), n, _ptr(oc), _ptr(lc), _ptr(o), _ptr(lse_out),
                                                 _stream(stream)))
+    _hold(stream, None if oc is o_parts else oc, None if lc is lse_parts else lc)
     return o, lse_out
 
 
@@ -221,6 +240,7 @@ def hta_forward(q, k_cache, v_cache, k_tree, v_tree, mask, cache_seqlens=None, o
     o = _out_like_q(q, o)
     if want_lse and lse_out is None:
         lse_out = torch.empty(B, H, T, dtype=torch.float32, device=q.device)
+    ws_given = ws
     ws = _workspace(shape, q.device, ws)
     if events is None:
         _check("hta_forward", lib().hta_forward(ctypes.byref(shape), _ptr(q), _ptr(k_cache), _ptr(v_cache),
@@ -231,6 +251,7 @@ def hta_forward(q, k_cache, v_cache, k_tree, v_tree, mask, cache_seqlens=None, o
         _check("hta_forward_timed", lib().hta_forward_timed(
             ctypes.byref(shape), _ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(cache_seqlens), _ptr(k_tree),
             _ptr(v_tree), _ptr(mask), mbs, _ptr(o), _ptr(lse_out), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream), ev0, ev1))
+    _hold(stream, None if ws is ws_given else ws)
     return o, lse_out
 
 
@@ -247,12 +268,14 @@ def hta_forward_paged(q, k_pool, v_pool, block_table, k_tree, v_tree, mask, cach
     o = _out_like_q(q, o)
     if want_lse and lse_out is None:
         lse_out = torch.empty(B, H, T, dtype=torch.float32, device=q.device)
+    ws_given = ws
     ws = _workspace(shape, q.device, ws)
     bt = block_table.to(torch.int32).contiguous()
     _check("hta_forward_paged", lib().hta_forward_paged(
         ctypes.byref(shape), _ptr(q), _ptr(k_pool), _ptr(v_pool), num_pages, page_size, _ptr(bt), max_pages,
         _ptr(cache_seqlens), _ptr(k_tree), _ptr(v_tree), _ptr(mask), mbs, _ptr(o), _ptr(lse_out), _ptr(ws),
         ws.numel() * ws.element_size(), _stream(stream)))
+    _hold(stream, None if ws is ws_given else ws, None if bt is block_table else bt)
     return o, lse_out
 
 
@@ -260,6 +283,7 @@ def hta_forward_paged(q, k_pool, v_pool, block_table, k_tree, v_tree, mask, cach
 
 def hta_build_tree_mask(parents: torch.Tensor, mask: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """uint8 [T,T] ancestor mask from int32 parents [T] (device if `parents` is on CUDA)."""
+    parents_in = parents
     parents = parents.to(torch.int32).contiguous()
     T = parents.numel()
     if mask is None:
@@ -267,6 +291,7 @@ def hta_build_tree_mask(parents: torch.Tensor, mask: Optional[torch.Tensor] = No
     on_dev = 1 if parents.is_cuda else 0
     _check("hta_build_tree_mask", lib().hta_build_tree_mask(_ptr(parents), T, _ptr(mask), on_dev,
                                                             _stream(stream) if on_dev else None))
+    _hold(stream, None if parents is parents_in else parents)
     return mask
 
 
@@ -282,6 +307,7 @@ def hta_accept_greedy(parents, draft_tokens, target_argmax, root: int = 0, conte
                       path=None, path_len=None, bonus=None, stream=None):
     """Greedy accepted path.  Host tensors -> (list path, int bonus); CUDA tensors -> device
     tensors (path int32 [T], path_len int32 [1], bonus int32 [1]) without synchronising."""
+    given = (parents, draft_tokens, target_argmax)
     parents = parents.to(torch.int32).contiguous()
     draft_tokens = draft_tokens.to(torch.int32).contiguous()
     target_argmax = target_argmax.to(torch.int32).contiguous()
@@ -295,6 +321,7 @@ def hta_accept_greedy(parents, draft_tokens, target_argmax, root: int = 0, conte
                                                         root, context_argmax, _ptr(path), _ptr(path_len), _ptr(bonus),
                                                         on_dev, _stream(stream) if on_dev else None))
     if on_dev:
+        _hold(stream, *(t for t, g in zip((parents, draft_tokens, target_argmax), given) if t is not g))
         return path, path_len, bonus
     n = int(path_len[0])
     return [int(x) for x in path[:n].tolist()], int(bonus[0])
@@ -317,12 +344,13 @@ def hta_commit_kv(path, path_len, k_tree, v_tree, k_cache, v_cache, cache_seqlen
     path = path.to(torch.int32).reshape(B, -1)
     if path.stride(-1) != 1:
         path = path.contiguous()
+    path_len = path_len.to(torch.int32).reshape(B)
     if seqlens_out is None:
         seqlens_out = torch.empty(B, dtype=torch.int32, device=k_cache.device)
-    _check("hta_commit_kv", lib().hta_commit_kv(ctypes.byref(s), _ptr(path), path.stride(0),
-                                                _ptr(path_len.to(torch.int32).reshape(B)), _ptr(k_tree), _ptr(v_tree),
-                                                _ptr(k_cache), _ptr(v_cache), _ptr(cache_seqlens), _ptr(seqlens_out),
-                                                _stream(stream)))
+    _check("hta_commit_kv", lib().hta_commit_kv(ctypes.byref(s), _ptr(path), path.stride(0), _ptr(path_len),
+                                                _ptr(k_tree), _ptr(v_tree), _ptr(k_cache), _ptr(v_cache),
+                                                _ptr(cache_seqlens), _ptr(seqlens_out), _stream(stream)))
+    _hold(stream, path, path_len)
     return seqlens_out
 
 
@@ -371,6 +399,7 @@ class HtaComm:
         if want_lse and lse_out is None:
             lse_out = torch.empty(B, Hx, T, dtype=torch.float32, device=q.device)
         n = self.workspace_size(shape)
+        ws_given = ws
         if ws is None or ws.numel() < n:
             ws = torch.empty(n, dtype=torch.uint8, device=q.device)
         mbs = 0 if mask.dim() == 2 else mask.stride(0)
@@ -378,7 +407,57 @@ class HtaComm:
             self.handle, ctypes.byref(shape), _ptr(q), _ptr(k_cache_local), _ptr(v_cache_local),
             _ptr(cache_seqlens_local), _ptr(k_tree), _ptr(v_tree), _ptr(mask), mbs, _ptr(o), _ptr(lse_out),
             1 if gather_output else 0, _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
+        _hold(stream, None if ws is ws_given else ws)
         return o, lse_out
+
+    def async_error(self) -> bool:
+        """True if NCCL reported an asynchronous error on this communicator."""
+        return lib().hta_comm_async_error(self.handle) != 0
+
+
+class LoopbackComm:
+    """`world_size` virtual ranks of the sequence-parallel step in this process, on the current
+    device (hta_comm_create_loopback): every rank's phases run through libhta on one GPU, the
+    exchange being device copies.  Used to check the P > 1 data path against the oracle."""
+
+    def __init__(self, world_size: int):
+        h = ctypes.c_void_p()
+        _check("hta_comm_create_loopback", lib().hta_comm_create_loopback(world_size, ctypes.byref(h)))
+        self.handle, self.world_size = h, world_size
+
+    def close(self):
+        if self.handle:
+            lib().hta_comm_destroy(self.handle)
+            self.handle = None
+
+    def workspace_size(self, shape: hta_shape_t) -> int:
+        n = lib().hta_workspace_size_seqpar(ctypes.byref(shape), _num_sms(torch.cuda.current_device()),
+                                            self.world_size)
+        if n == ctypes.c_size_t(-1).value:
+            raise HtaError("hta_workspace_size_seqpar", 1)
+        return self.world_size * ((n + 15) // 16 * 16)
+
+    def forward(self, q, k_slices, v_slices, k_tree, v_tree, mask, seqlens_slices=None, gather_output=False,
+                want_lse=True, scale=None, num_splits=0, stream=None):
+        """k_slices / v_slices: per-rank KV slices [B, N_r, H_kv, d] (same N_r capacity);
+        returns per-rank lists (o, lse) as hta_forward_seqpar would on each rank."""
+        P = self.world_size
+        assert len(k_slices) == P and len(v_slices) == P
+        shape = make_shape(q, k_cache=k_slices[0], k_tree=k_tree, scale=scale, num_splits=num_splits)
+        B, T, H, d = q.shape
+        Hx = H if gather_output else H // P
+        os_ = [torch.empty(B, T, Hx, d, dtype=q.dtype, device=q.device) for _ in range(P)]
+        ls = [torch.empty(B, Hx, T, dtype=torch.float32, device=q.device) for _ in range(P)] if want_lse else None
+        ws = torch.empty(self.workspace_size(shape), dtype=torch.uint8, device=q.device)
+        arr = lambda ts: (ctypes.c_void_p * P)(*[t.data_ptr() for t in ts])
+        mbs = 0 if mask.dim() == 2 else mask.stride(0)
+        _check("hta_forward_seqpar_loopback", lib().hta_forward_seqpar_loopback(
+            self.handle, ctypes.byref(shape), _ptr(q), arr(k_slices), arr(v_slices),
+            arr(seqlens_slices) if seqlens_slices is not None else None, _ptr(k_tree), _ptr(v_tree), _ptr(mask),
+            mbs, arr(os_), arr(ls) if ls is not None else None, 1 if gather_output else 0, _ptr(ws),
+            ws.numel(), _stream(stream)))
+        _hold(stream, ws)
+        return os_, ls
 
 
 def shard_bounds(N: int, world_size: int, rank: int) -> Tuple[int, int]:

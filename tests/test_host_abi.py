@@ -161,3 +161,42 @@ def test_shard_bounds_cover_sequence():
             assert b[0][0] == 0 and b[-1][1] == N
             assert all(b[i][1] == b[i + 1][0] for i in range(P - 1))
             assert max(hi - lo for lo, hi in b) - min(hi - lo for lo, hi in b) <= 1
+
+
+def test_loopback_communicator_host_checks(L):
+    """Loopback communicator (P virtual ranks, no NCCL): host-side creation and argument checks."""
+    h = ctypes.c_void_p()
+    assert L.hta_comm_create_loopback(0, ctypes.byref(h)) == 1
+    assert L.hta_comm_create_loopback(65, ctypes.byref(h)) == 1
+    assert L.hta_comm_create_loopback(4, ctypes.byref(h)) == 0
+    try:
+        assert L.hta_comm_async_error(h) == 0
+        s = _shape(N=2048)
+        # a loopback communicator is not an NCCL one: hta_forward_seqpar refuses it
+        rc = L.hta_forward_seqpar(h, ctypes.byref(s), *([ctypes.c_void_p(16)] * 7), 0, ctypes.c_void_p(16), None,
+                                  0, ctypes.c_void_p(16), 1 << 30, None)
+        assert rc == 1
+        # NULL per-rank pointer arrays are rejected before any device work
+        rc = L.hta_forward_seqpar_loopback(h, ctypes.byref(s), ctypes.c_void_p(16), None, None, None,
+                                           ctypes.c_void_p(16), ctypes.c_void_p(16), ctypes.c_void_p(16), 0, None,
+                                           None, 0, ctypes.c_void_p(16), 1 << 30, None)
+        assert rc == 1
+        # H not divisible by the rank count
+        s = _shape(H=12, H_kv=4, N=2048)
+        assert L.hta_workspace_size_seqpar(ctypes.byref(s), 148, 8) == ctypes.c_size_t(-1).value
+    finally:
+        assert L.hta_comm_destroy(h) == 0
+
+
+def test_seqpar_workspace_layout(L):
+    """hta_workspace_size_seqpar = split partials + send and receive blocks [P][blk] + own output
+    slice + the gathered slices (16-byte rounded pieces)."""
+    r16 = lambda x: (x + 15) // 16 * 16
+    for P in (1, 2, 4, 8):
+        s = _shape(N=16384)
+        blk = (s.B * s.T * (s.H // P) * s.d + s.B * (s.H // P) * s.T) * 4
+        o_sl = s.B * s.T * (s.H // P) * s.d * 2
+        l_sl = s.B * (s.H // P) * s.T * 4
+        want = r16(L.hta_workspace_size(ctypes.byref(s), 148)) + 2 * r16(P * blk) + r16(o_sl) + r16(l_sl) + \
+            r16(P * o_sl) + r16(P * l_sl)
+        assert L.hta_workspace_size_seqpar(ctypes.byref(s), 148, P) == want
