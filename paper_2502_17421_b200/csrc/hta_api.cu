@@ -629,7 +629,7 @@ hta_status_t seqpar_local_parts(const hta_shape_t *shape, const void *q, const v
     r = run_prefix(sh, pl, q, k, v, seqlens, parts_ws, lse_ws, ostride, lstride, st);
     if (r != HTA_OK) return r;
     const int Hp = s.H / P;
-    const int64_t blk = int64_t(s.B) * s.T * Hp * s.d + int64_t(s.B) * Hp * s.T;
+    const int64_t blk = static_cast<int64_t>(seqpar_block_floats(s.B, s.T, Hp, s.d));
     TreeMergeParams p = base_tm(sh);
     p.do_tree = 0;
     p.n_parts = pl.splits;

@@ -107,6 +107,14 @@ int host_build_mask(const int32_t *parents, int T, uint8_t *mask);  // 0 ok, -1 
 int host_accept(const int32_t *parents, const int32_t *draft, const int32_t *tgt, int T, int root, int ctx,
                 int32_t *path, int32_t *path_len, int32_t *bonus);  // 0 ok, -1 invalid
 
+// Floats of one destination-major exchange block of the sequence-parallel step: O [B][T][Hp][d]
+// then LSE [B][Hp][T], rounded up to a multiple of 4 floats so that every block (and the
+// vectorised O rows in it) stays 16-byte aligned.
+inline size_t seqpar_block_floats(int B, int T, int Hp, int d) {
+    const size_t n = size_t(B) * T * Hp * d + size_t(B) * Hp * T;
+    return (n + 3) & ~size_t(3);
+}
+
 // Sequence-parallel building blocks (implemented in hta_api.cu, used by seqpar.cu).
 // Local prefix pass over this rank's KV slice, combined into one partial per row laid out
 // destination-major: block p (for rank p) = O [B][T][H/P][d] then LSE [B][H/P][T].

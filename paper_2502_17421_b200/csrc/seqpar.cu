@@ -79,11 +79,8 @@ NcclApi &nccl() {
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 size_t round16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// Per-rank exchange block: O [B][T][Hp][d] followed by LSE [B][Hp][T] (floats).
-size_t block_floats(const hta_shape_t &s, int P) {
-    const size_t Hp = size_t(s.H / P);
-    return size_t(s.B) * s.T * Hp * s.d + size_t(s.B) * Hp * s.T;
-}
+// Per-rank exchange block: O [B][T][Hp][d] followed by LSE [B][Hp][T] (floats, 16-byte rounded).
+size_t block_floats(const hta_shape_t &s, int P) { return seqpar_block_floats(s.B, s.T, s.H / P, s.d); }
 
 // One rank's workspace, carved in this order (all 16-byte aligned):
 //   prefix split partials | send blocks [P][blk] | receive blocks [P][blk] |

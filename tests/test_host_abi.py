@@ -192,9 +192,9 @@ def test_seqpar_workspace_layout(L):
     """hta_workspace_size_seqpar = split partials + send and receive blocks [P][blk] + own output
     slice + the gathered slices (16-byte rounded pieces)."""
     r16 = lambda x: (x + 15) // 16 * 16
-    for P in (1, 2, 4, 8):
-        s = _shape(N=16384)
-        blk = (s.B * s.T * (s.H // P) * s.d + s.B * (s.H // P) * s.T) * 4
+    for P, B, T in ((1, 1, 64), (2, 1, 64), (4, 1, 64), (8, 1, 64), (8, 2, 13)):
+        s = _shape(B=B, T=T, N=16384)
+        blk = (s.B * s.T * (s.H // P) * s.d + s.B * (s.H // P) * s.T + 3) // 4 * 16
         o_sl = s.B * s.T * (s.H // P) * s.d * 2
         l_sl = s.B * (s.H // P) * s.T * 4
         want = r16(L.hta_workspace_size(ctypes.byref(s), 148)) + 2 * r16(P * blk) + r16(o_sl) + r16(l_sl) + \
