@@ -9,13 +9,9 @@
 
 namespace hta {
 
-#ifndef HTA_BLOCK_N
-#define HTA_BLOCK_N 192
-#endif
-// Keys per KV tile of the prefix pass: TMEM holds 384 / kBlockN S/P buffers (2 x 192 or
-// 3 x 128 columns) and the 128-column O accumulator (512 columns in all).
-constexpr int kBlockN = HTA_BLOCK_N;
-static_assert(kBlockN == 96 || kBlockN == 128 || kBlockN == 192, "KV tile of 96, 128 or 192 keys");
+// Keys per KV tile of the prefix pass: TMEM holds three 128-column S/P buffers and the
+// 128-column O accumulator (512 columns in all).
+constexpr int kBlockN = 128;
 constexpr int kSimtBlock = 16;   // key block (split granularity) of the fp32 SIMT prefix pass
 constexpr int kRowsPerTile = 128;  // rows of one tcgen05 M=128 tile
 

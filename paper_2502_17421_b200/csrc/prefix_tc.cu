@@ -5,33 +5,34 @@
 // 199-201: "the queries and the cached key-value pairs {K_cache, V_cache} do not require
 // additional masks"), producing a normalised partial O and its LSE.  The
 // paper calls FlashDecoding for this step (PAPER.md:108 footnote); this kernel is the B200-native
-// replacement (DESIGN.md "Prefix kernel"):
+// replacement (DESIGN.md §6.1):
 //
 //  * rows: the T tree tokens x the G query heads of one KV head form the M dimension
 //    (row r = t*G + j, head h = g*G + j).  Each CTA owns 128 rows (one TMEM lane per row).
-//  * KV tiles of kBlockN = 192 keys: TMEM holds two S/P buffers of 192 fp32 columns and the
-//    128-column O accumulator (512 columns), and the fixed per-tile costs of the softmax warps
-//    (barrier checks, publication, reduction latency) are spread over 192 keys.
 //  * PAIR (M > 128, d = 128): a cluster of two CTAs on one TPC runs tcgen05.mma.cta_group::2
-//    with M = 256: each CTA holds its 128 Q rows, HALF of every K tile (96 keys) and HALF of
-//    every V tile (64 head-dim columns), so each KV byte is read from HBM once for 256 rows and
-//    each SM streams only half of the operand bytes through shared memory.
-//  * warp 0 (one lane) streams K and V tiles with TMA into two rings of smem slots (128B
-//    swizzle, the canonical UMMA layout) so K tiles can run ahead of V tiles; in a pair both
-//    CTAs' bytes are counted on the leader's barriers.
-//  * warp 1 of the leader CTA issues the MMAs in a fixed order with suspended barrier waits, one
-//    elected lane issuing each group (descriptors are warp-uniform and advanced by constants):
-//    S = Q K^T into one of two TMEM buffers (fp32) once a K tile and a buffer are free, and
-//    O += P V with A = P read from TMEM (the "TS" form) and B = V from smem (MN-major) once P and
-//    the V tile are ready.
-//  * warps 2-9 (softmax): the two warps that share a TMEM lane quarter own disjoint 16-row halves
-//    of it, and each row is shared by a pair of threads (lanes t and t+16) that each hold 96 of
-//    its 192 S values (tcgen05.ld .16x32bx2).  Per tile: row max (one shuffle between the pair),
-//    exp2 (3/8 of the pairs on the FMA pipe by polynomial, the rest on MUFU), row sum, P -> bf16
-//    -> tcgen05.st over S.  No two warps ever exchange data, so they drift freely and overlap
-//    each other's latency.  O is rescaled in TMEM only when the running max grows by more than
-//    2^8 (exact: the final normalisation uses the same, possibly stale, max).
-//  * the epilogue divides O by the row sum and writes fp32 partials + natural-log LSE.
+//    with M = 256: each CTA holds its 128 Q rows, HALF of every K tile (64 keys) and HALF of
+//    every V tile (64 head-dim columns), so each KV byte is read from HBM once for 256 rows.
+//  * KV tiles of kBlockN = 128 keys; TMEM = three S/P buffers of 128 fp32 columns + the
+//    128-column O accumulator (512 columns).  The MMA warp issues S_0, S_1, S_2, then per tile j
+//    PV_j (A = P_j from TMEM, "TS" form) and S_{j+3} into P_j's buffer, so a tile's softmax has
+//    two tile periods between its S being ready and its P being needed.
+//  * softmax: TWO groups of 8 warps take alternate tiles (group j % 2), so one group's TMEM loads
+//    and P publication overlap the other group's exponentials.  In a group, the two warps that
+//    share a TMEM lane quarter own disjoint 16-row halves of it and each row is shared by a pair
+//    of threads (lanes t, t+16) holding 64 of its 128 S values.  Per tile: exp2 of S*c - m with
+//    m the row's running max (3/8 of the pairs on the FMA pipe by polynomial, the rest on MUFU),
+//    row sum, P -> bf16 -> tcgen05.st over S, publish.
+//  * running max across the groups (speculative): a tile's exponentials use the running max m
+//    known to its group; no row-max reduction is on the critical path.  The row sum checks that
+//    no P exceeded 2^60 (bf16 P and the fp32 O / sums have the range, so the result is exact up
+//    to rounding); otherwise the tile is redone with its true row max.  The decision of tile j
+//    (the row's m after it) is handed to the other group through shared memory and a per-warp
+//    mbarrier ("token"); the group of tile j+1 reads it only after its own exponentials (it is
+//    long available by then) and redoes the tile if m moved.  Whoever raises m rescales O in TMEM
+//    after PV_{j-1} and before publishing P_j, so every PV accumulates in one scale.
+//  * warps 0-3 (K/Q TMA, MMA issue + TMEM allocation, V TMA, spare) give registers to the
+//    softmax warps (setmaxnreg).
+//  * epilogue (both groups: half of the head dim each): O / row sum -> fp32 partial + LSE.
 // A split with no visible key writes the sentinel (O = 0, LSE = -inf).
 #include <cuda_bf16.h>
 #include <cstdio>
@@ -42,79 +43,64 @@
 
 namespace hta {
 
-// Optional pipeline timeline (build with -DHTA_TRACE, tools/trace_prefix.py): lane 0 of each
-// traced warp of CTA g_trace_cta appends (event, tag, j, clock) records.
+// Pipeline timeline (diagnostics only: built into libhta_trace.so with -DHTA_TRACE, read by
+// tools/trace_prefix.py).  Lane 0 of every warp of CTA g_trace_cta records (event, tile, clock).
 #ifdef HTA_TRACE
 __device__ unsigned long long *g_trace = nullptr;
 __device__ int g_trace_cta = 0;
-__device__ unsigned long long g_cta_times[1024][4];  // per CTA: entry ns, loop start ns/clk, exit ns, exit clk
-constexpr int kTraceRecs = 2048;  // per warp, written straight to g_trace (traced CTA only)
-#define HTA_TR(ev, tag, jj)                                                                              \
-    do {                                                                                                 \
-        if (lane == 0 && tr_on && tr_n < kTraceRecs)                                                     \
-            tr_buf[warp * kTraceRecs + tr_n++] = (static_cast<unsigned long long>(ev) << 56) |              \
-                                                 (static_cast<unsigned long long>(tag) << 52) |           \
-                                                 (static_cast<unsigned long long>((jj) & 0xFFFFF) << 32) |\
-                                                 static_cast<unsigned long long>(static_cast<uint32_t>(clock64())); \
+constexpr int kTraceRecs = 1024;  // per warp
+#define HTA_TR(ev, jj)                                                                                     \
+    do {                                                                                                   \
+        if (tr_on && lane == 0 && tr_n < kTraceRecs)                                                       \
+            tr_buf[warp * kTraceRecs + tr_n++] = (static_cast<unsigned long long>(ev) << 56) |             \
+                                                  (static_cast<unsigned long long>((jj) & 0xFFFFFF) << 32) | \
+                                                  static_cast<uint32_t>(clock64());                        \
     } while (0)
-__device__ __forceinline__ uint64_t trace_globaltimer() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-// clock and wall time (ns) side by side: the SM clock the kernel actually ran at
-#define HTA_TR_CLK(ev)                                                                                   \
-    do {                                                                                                 \
-        const uint32_t c_ = static_cast<uint32_t>(clock64());                                            \
-        const uint32_t t_ = static_cast<uint32_t>(trace_globaltimer());                                  \
-        if (lane == 0 && tr_on && tr_n + 1 < kTraceRecs) {                                               \
-            tr_buf[warp * kTraceRecs + tr_n++] = (static_cast<unsigned long long>(ev) << 56) | c_;       \
-            tr_buf[warp * kTraceRecs + tr_n++] = (static_cast<unsigned long long>(ev + 1) << 56) | t_;   \
-        }                                                                                                \
+// Softmax warps stamp their per-tile events into registers and write them after publishing the
+// tile: a global store before a release-semantics mbarrier arrive would make that arrive wait
+// for the store (and distort the timeline it is meant to measure).
+#define HTA_TRS(k) tr_c[k] = static_cast<uint32_t>(clock64())
+#define HTA_TRFLUSH(jj)                                                                                    \
+    do {                                                                                                   \
+        const int ev_[6] = {10, 11, 12, 13, 15, 14};                                                       \
+        for (int k_ = 0; k_ < 6; ++k_)                                                                     \
+            if (tr_on && lane == 0 && tr_n < kTraceRecs)                                                   \
+                tr_buf[warp * kTraceRecs + tr_n++] = (static_cast<unsigned long long>(ev_[k_]) << 56) |    \
+                                                     (static_cast<unsigned long long>((jj) & 0xFFFFFF) << 32) | tr_c[k_]; \
     } while (0)
 #else
-#define HTA_TR(ev, tag, jj) do { } while (0)
-#define HTA_TR_CLK(ev) do { } while (0)
+#define HTA_TR(ev, jj) \
+    do {               \
+    } while (0)
+#define HTA_TRS(k) \
+    do {           \
+    } while (0)
+#define HTA_TRFLUSH(jj) \
+    do {                \
+    } while (0)
 #endif
 
-// Diagnostics only (tools/): HTA_SKIP=1 skips the softmax math, HTA_SKIP=2 also the MMAs,
-// leaving the TMA stream and the barrier protocol; HTA_SKIP=3 runs the MMAs with no TMA traffic
-// (operands are whatever sits in smem) and no softmax; HTA_SKIP=4 = 3 with the softmax.
-// Product builds use 0.
-// Publish P_j at the start of tile j+1 (see the softmax loop).
-#ifndef HTA_DEFER
-#define HTA_DEFER 1
-#endif
-#ifndef HTA_SKIP
-#define HTA_SKIP 0
-#endif
-// Pairs of every 8 whose exp2 runs on the FMA pipe (polynomial) instead of MUFU.
-#ifndef HTA_SPEC_MAX
-#define HTA_SPEC_MAX 1
-#endif
-// Diagnostics: 1 = the contiguous-cache producers loop with the whole warp waiting on each
-// mbarrier (+2 us on Llama-8B-64k); 0 = lane 0 alone loops (the other lanes are parked at the
-// __syncwarp after the loop).  The paged producers always wait converged: their lanes take part
-// in every tile (block-table lookups, shuffles), and a lane-0-only wait with the other 31 lanes
-// at a per-tile __syncwarp made the paged pass 2x slower (profiles/r01b/README.md).
-#ifndef HTA_CONV
-#define HTA_CONV 0
-#endif
-#ifndef HTA_RING_KB
-#define HTA_RING_KB 192
-#endif
-#ifndef HTA_POLY
-#define HTA_POLY 3
+// Timing diagnostics only (tools/lib_variants.sh; results are wrong): HTA_DIAG bit 1 = no P
+// stores to TMEM, bit 2 = no exponentials (P = x), bit 4 = no wait for the row-max hand-over.
+#ifndef HTA_DIAG
+#define HTA_DIAG 0
 #endif
 
-#ifndef HTA_KV_POLICY
-#define HTA_KV_POLICY kPolicyEvictFirst
-#endif
-constexpr uint64_t kKvPolicy = HTA_KV_POLICY;  // L2 policy of the streamed K/V tiles (read once)
+constexpr uint64_t kKvPolicy = kPolicyEvictFirst;  // L2 policy of the streamed K/V tiles (read once)
+constexpr int kPolyPairs = 3;                      // pairs of every 8 whose exp2 runs on the FMA pipe
+constexpr float kSpecLimit = 0x1p60f;              // largest P the speculative pass may produce
+
+// The running max after a tile whose requirement is rho (its row max, or -inf when the tile
+// fits under m): raised only when some exponent argument would exceed 60 (P > 2^60).
+__device__ __forceinline__ float fold_max(float m, float rho) { return rho > m + 60.f ? rho : m; }
+
+__device__ __forceinline__ void setmaxnreg_dec(void) { asm volatile("setmaxnreg.dec.sync.aligned.u32 32;"); }
+__device__ __forceinline__ void setmaxnreg_inc(void) { asm volatile("setmaxnreg.inc.sync.aligned.u32 112;"); }
 
 template <int D, bool PAIR>
 struct TcCfg {
     static_assert(!PAIR || D == 128, "CTA pairs split the 128-column V tile in two 64-column halves");
+    static_assert(kBlockN == 128, "three 128-column S/P buffers + O fill the 512 TMEM columns");
     static constexpr int kKB = D / 64;                          // 128-byte K-blocks of the head dim
     static constexpr int kRegionBytes = 128 * 128;              // 128 rows x 128 B
     static constexpr int kQBytes = kRowsPerTile * D * 2;        // this CTA's 128 Q rows
@@ -122,41 +108,26 @@ struct TcCfg {
     static constexpr int kVCols = PAIR ? D / 2 : D;             // head-dim columns of a V tile held here
     static constexpr int kKBytes = kKRows * D * 2;
     static constexpr int kVBytes = kBlockN * kVCols * 2;
-    static constexpr int kRingBytes = (PAIR || D == 64 ? HTA_RING_KB : 192) * 1024;
-#ifdef HTA_KRING_PCT  // diagnostics: share of the ring given to K tiles (percent)
-    static constexpr int kSlotsK = (kRingBytes * HTA_KRING_PCT / 100) / kKBytes;
-    static constexpr int kSlotsV = (kRingBytes - kSlotsK * kKBytes) / kVBytes;
-#else
+    static constexpr int kRingBytes = 192 * 1024;
     static constexpr int kSlotsK = (kRingBytes / 2) / kKBytes;
     static constexpr int kSlotsV = (kRingBytes / 2) / kVBytes;
-#endif
-    static constexpr int kSBufs = 384 / kBlockN;                // S/P buffers in TMEM (2 x 192 or 3 x 128)
-    static constexpr int kSoftmaxWarps = 8;                     // two per SM sub-partition
-    static constexpr int kFirstSoftmaxWarp = 3;                 // warp 0 K TMA, 1 MMA + TMEM, 2 V TMA
-    static constexpr int kThreads = 32 * (kFirstSoftmaxWarp + kSoftmaxWarps);
+    static constexpr int kSBufs = 3;
+    static constexpr int kGroupWarps = 8;                       // softmax warps per group (two per SMSP)
+    static constexpr int kFirstSoftmaxWarp = 4;                 // warps 0-3: K TMA, MMA, V TMA, spare
+    static constexpr int kThreads = 32 * (kFirstSoftmaxWarp + 2 * kGroupWarps);
     static constexpr int kVOff = kQBytes + kSlotsK * kKBytes;   // start of the V ring
     static constexpr int kBarOff = kVOff + kSlotsV * kVBytes;
-    static constexpr int kSmemBytes = kBarOff + 512;  // base is 1024-aligned (__align__ below)
+    static constexpr int kNumBars = 2 * kSlotsK + 2 * kSlotsV + 3 * kSBufs + 4;
+    static constexpr int kMaxOff = kBarOff + 8 * kNumBars + 8;  // row-max hand-over rho[3][128]
+    static constexpr int kSmemBytes = kMaxOff + 3 * 128 * 4;    // base is 1024-aligned (__align__ below)
     static_assert(kSlotsK >= 2 && kSlotsV >= 2, "need at least 2 slots per ring");
     static_assert(kSmemBytes <= 232448, "shared memory budget");
+    static_assert(8 * 128 * 4 <= kSlotsK * kKBytes, "the epilogue exchange reuses the K ring");
 };
 
 // TMEM column map: S/P buffer b at 128*b (b = 0, 1, 2), O at 384.
 __device__ __forceinline__ uint32_t s_col(int buf) { return static_cast<uint32_t>(kBlockN * buf); }
-constexpr uint32_t kOCol = 384u;  // O: 128 fp32 columns after the S buffers (384 + 128 = 512)
-
-// this thread's N S values (N = 64 or 96; the other half of the warp at +N columns) and the wait
-template <int N>
-__device__ __forceinline__ void tmem_ld_S(uint32_t taddr, float *v) {
-    if constexpr (N == 96) {
-        tmem_ld_x96<96>(taddr, v);
-    } else if constexpr (N == 48) {
-        tmem_ld_x48<48>(taddr, v);
-    } else {
-        tmem_ld_x64_nowait<64>(taddr, v);
-        tmem_ld_wait_fence<64>(v);
-    }
-}
+constexpr uint32_t kOCol = 384u;
 
 // Pool row of logical key k of batch b (paged KV); pages past the table or negative entries read
 // page 0 (such keys are past cache_seqlens: masked, and their V rows zeroed).
@@ -187,20 +158,26 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     uint64_t *pv_done = p_full + C::kSBufs;        // [kSBufs]   PV_j arrives on pv_done[j % kSBufs]
     uint64_t *o_final = pv_done + C::kSBufs;       // [1]
     uint64_t *q_full = o_final + 1;                // [1]       Q staged (the leader's copy is the one used)
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_full + 1);
+    uint64_t *v_tail_land = q_full + 1;            // [1]       this CTA's part of the last V tile landed
+    uint64_t *v_tail_ready = v_tail_land + 1;      // [1]       ... and sanitised (the leader's copy is used)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(v_tail_ready + 1);
+    // row-max hand-over of tile j in slot j % 3: one 32-bit word per row, rho_j with the
+    // generation parity (j / 3) & 1 in its lowest mantissa bit, written once by the group of tile j
+    // and read by polling (no barrier) by the group of tile j+1, which is also the next writer of
+    // the slot (tile j+3) -- so a slot is never overwritten before it is read.  The 1-ulp tag
+    // leaves a P of 1 at the row max exactly 1 after rounding to bf16.
+    uint32_t *m_sh = reinterpret_cast<uint32_t *>(smem + C::kMaxOff);  // [3][128] tagged rho_j
 
     const int warp = threadIdx.x >> 5;
-#ifdef HTA_TRACE
-    if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_times[blockIdx.x][0] = trace_globaltimer();
-#endif
     const int lane = threadIdx.x & 31;
-#ifdef HTA_TRACE
-    int tr_n = 0;
-    unsigned long long *tr_buf = g_trace;
-    const bool tr_on = g_trace != nullptr && static_cast<int>(blockIdx.x) == g_trace_cta;
-#endif
     const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
+#ifdef HTA_TRACE
+    unsigned long long *const tr_buf = g_trace;  // read once: a global load per record would stall
+    const bool tr_on = tr_buf != nullptr && static_cast<int>(blockIdx.x) == g_trace_cta;
+    int tr_n = 0;
+#endif
+    HTA_TR(0, 0);
 
     // ---- work item: (b, g, split, row group); a pair shares one work item
     int rest = PAIR ? (blockIdx.x >> 1) : blockIdx.x;
@@ -229,13 +206,17 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         }
         for (int i = 0; i < C::kSBufs; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], C::kSoftmaxWarps * (PAIR ? 2 : 1));
+            mbar_init(&p_full[i], C::kGroupWarps * (PAIR ? 2 : 1));
             mbar_init(&pv_done[i], 1);
         }
         mbar_init(o_final, 1);
-        mbar_init(q_full, p.q_tma ? 1 : C::kSoftmaxWarps * (PAIR ? 2 : 1));
+        mbar_init(q_full, p.q_tma ? 1 : C::kGroupWarps * (PAIR ? 2 : 1));
+        mbar_init(v_tail_land, 1);
+        mbar_init(v_tail_ready, PAIR ? 2 : 1);
         fence_mbar_init();
     }
+    for (int i = threadIdx.x; i < 3 * 128; i += blockDim.x)  // generation -1 (parity 1): never read
+        m_sh[i] = 0xFF7FFFFFu;
     if (warp == 1) {
         if (PAIR) {
             tmem_alloc2(tmem_slot, 512);
@@ -252,8 +233,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     // Inputs (q, K/V, seqlens) may come from the kernel before this one on the stream: wait for it
-    // (griddepcontrol.wait; a no-op unless it triggered this grid's launch early, as the tree-mask
-    // kernel does).  The tree/merge kernel after this one reads the mask after its own wait.
+    // (griddepcontrol.wait; a no-op unless it triggered this grid's launch early).
     pdl_wait_primary();
 
     int64_t n_b = p.N_max;
@@ -273,14 +253,6 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     float *o_base = p.o_out + static_cast<int64_t>(split) * p.o_split_stride;
     float *lse_base = p.lse_out + static_cast<int64_t>(split) * p.lse_split_stride;
 
-
-    if (warp == 0) HTA_TR_CLK(50);
-#ifdef HTA_TRACE
-    if (threadIdx.x == 0 && blockIdx.x < 1024) {
-        g_cta_times[blockIdx.x][1] = trace_globaltimer();
-        g_cta_times[blockIdx.x][2] = clock64();
-    }
-#endif
     if (n_tiles == 0) {  // empty split: sentinel rows (both CTAs of a pair take this branch)
         for (int r = threadIdx.x; r < kRowsPerTile; r += blockDim.x) {
             const int grow = row0 + r;
@@ -291,239 +263,245 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);
             lse_base[(static_cast<int64_t>(b) * p.H + h) * p.T + t] = -INFINITY;
         }
-    } else if (warp == 0) {
-        // ================= TMA producer of Q and the K ring (K_j is consumed by S_j).  K and V
-        // have producers of their own, so K tiles run ahead of V tiles by as many slots as the
-        // K ring has (S_j frees K_j long before PV_j frees V_j).
-        if (lane == 0 && p.q_tma) {  // Q first: it gates S_0 and must not queue behind K/V
-            const int t0 = row0 / p.G;
-            if (PAIR) {
-                if (leader) mbar_arrive_expect_tx(q_full, 2u * C::kQBytes);
-                const uint32_t qfull0 = mapa_shared(smem_u32(q_full), 0);
-#pragma unroll
-                for (int kb = 0; kb < C::kKB; ++kb)
-                    tma_load_4d_pair(sQ + kb * C::kRegionBytes, &tmap_q, qfull0, kb * 64, g * p.G, t0, b,
-                                     kPolicyEvictNormal);  // re-read by every split
-            } else {
-                mbar_arrive_expect_tx(q_full, C::kQBytes);
-#pragma unroll
-                for (int kb = 0; kb < C::kKB; ++kb)
-                    tma_load_4d(sQ + kb * C::kRegionBytes, &tmap_q, q_full, kb * 64, g * p.G, t0, b,
-                                kPolicyEvictNormal);
-            }
-        }
-        if (p.page_size > 0 && HTA_SKIP < 3) {
-            // paged KV: the whole warp runs the loop; lane i translates box i (16 keys) of the
-            // tile through the block table, lane 0 issues the TMA boxes
-            const uint32_t kfull0 = PAIR ? mapa_shared(smem_u32(&k_full[0]), 0) : 0u;
-            constexpr int kBoxes = C::kKRows / 16;
-            for (int j = 0; j < n_tiles; ++j) {
-                const int n0 = static_cast<int>(key_lo) + j * kBlockN + (PAIR ? static_cast<int>(rank) * C::kKRows : 0);
-                const int prow = paged_row(p, b, n0 + 16 * (lane < kBoxes ? lane : 0));
-                const int slot = j % C::kSlotsK;
-                mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);  // the whole warp waits (converged)
-                __syncwarp();
-                HTA_TR(30, 0, j);
-                uint8_t *dst = sK + slot * C::kKBytes;
-                if (lane == 0) {
-                    if (PAIR) {
-                        if (leader) mbar_arrive_expect_tx(&k_full[slot], 2u * C::kKBytes);
-                    } else {
-                        mbar_arrive_expect_tx(&k_full[slot], C::kKBytes);
-                    }
-                }
-#pragma unroll
-                for (int i = 0; i < kBoxes; ++i) {
-                    const int r = __shfl_sync(0xffffffffu, prow, i);
-                    if (lane == 0) {
-#pragma unroll
-                        for (int kb = 0; kb < C::kKB; ++kb) {
-                            uint8_t *dd = dst + kb * (C::kKRows * 128) + i * 2048;
-                            if (PAIR)
-                                tma_load_4d_pair(dd, &tmap_k, kfull0 + 8u * slot, kb * 64, g, r, 0, kKvPolicy);
-                            else
-                                tma_load_4d(dd, &tmap_k, &k_full[slot], kb * 64, g, r, 0, kKvPolicy);
-                        }
-                    }
-                }
-            }
-        } else if ((HTA_CONV || lane == 0) && HTA_SKIP < 3) {
-            const uint32_t kfull0 = PAIR ? mapa_shared(smem_u32(&k_full[0]), 0) : 0u;
-            for (int j = 0; j < n_tiles; ++j) {
-                const int n0 = static_cast<int>(key_lo) + j * kBlockN;
-                const int slot = j % C::kSlotsK;
-                mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);
-                uint8_t *dst = sK + slot * C::kKBytes;
-                HTA_TR(30, 0, j);
-                if (lane != 0) {
-                } else if (PAIR) {
-                    if (leader) mbar_arrive_expect_tx(&k_full[slot], 2u * C::kKBytes);
+    } else if (warp < C::kFirstSoftmaxWarp) {
+        setmaxnreg_dec();
+        if (warp == 0) {
+            // ================= TMA producer of Q and the K ring (K_j is consumed by S_j).  K and V
+            // have producers of their own, so K tiles run ahead of V tiles by as many slots as the
+            // K ring has (S_j frees K_j long before PV_j frees V_j).
+            if (lane == 0 && p.q_tma) {  // Q first: it gates S_0 and must not queue behind K/V
+                const int t0 = row0 / p.G;
+                if (PAIR) {
+                    if (leader) mbar_arrive_expect_tx(q_full, 2u * C::kQBytes);
+                    const uint32_t qfull0 = mapa_shared(smem_u32(q_full), 0);
 #pragma unroll
                     for (int kb = 0; kb < C::kKB; ++kb)
-                        tma_load_4d_pair(dst + kb * (C::kKRows * 128), &tmap_k, kfull0 + 8u * slot, kb * 64, g,
-                                         n0 + static_cast<int>(rank) * C::kKRows, b, kKvPolicy);
+                        tma_load_4d_pair(sQ + kb * C::kRegionBytes, &tmap_q, qfull0, kb * 64, g * p.G, t0, b,
+                                         kPolicyEvictNormal);  // re-read by every split
                 } else {
-                    mbar_arrive_expect_tx(&k_full[slot], C::kKBytes);
+                    mbar_arrive_expect_tx(q_full, C::kQBytes);
 #pragma unroll
                     for (int kb = 0; kb < C::kKB; ++kb)
-                        tma_load_4d(dst + kb * (kBlockN * 128), &tmap_k, &k_full[slot], kb * 64, g, n0, b, kKvPolicy);
+                        tma_load_4d(sQ + kb * C::kRegionBytes, &tmap_q, q_full, kb * 64, g * p.G, t0, b,
+                                    kPolicyEvictNormal);
                 }
-                if (HTA_CONV) __syncwarp();
             }
-        }
-        __syncwarp();
-    } else if (warp == 2) {
-        // ================= TMA producer of the V ring (V_j is consumed by PV_j)
-        if (p.page_size > 0 && HTA_SKIP < 3) {
-            const uint32_t vfull0 = PAIR ? mapa_shared(smem_u32(&v_full[0]), 0) : 0u;
-            constexpr int kBoxes = kBlockN / 16;
-            for (int j = 0; j < n_tiles; ++j) {
-                const int n0 = static_cast<int>(key_lo) + j * kBlockN;
-                const int prow = paged_row(p, b, n0 + 16 * (lane < kBoxes ? lane : 0));
-                const int slot = j % C::kSlotsV;
-                mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
-                __syncwarp();
-                HTA_TR(31, 0, j);
-                uint8_t *dst = sV + slot * C::kVBytes;
-                if (lane == 0) {
-                    if (PAIR) {
-                        if (leader) mbar_arrive_expect_tx(&v_full[slot], 2u * C::kVBytes);
-                    } else {
-                        mbar_arrive_expect_tx(&v_full[slot], C::kVBytes);
-                    }
-                }
-#pragma unroll
-                for (int i = 0; i < kBoxes; ++i) {
-                    const int r = __shfl_sync(0xffffffffu, prow, i);
+            const uint32_t kfull0 = PAIR ? mapa_shared(smem_u32(&k_full[0]), 0) : 0u;
+            if (p.page_size > 0) {
+                // paged KV: the whole warp runs the loop (waits converged); lane i translates box i
+                // (16 keys) of the tile through the block table, lane 0 issues the TMA boxes
+                constexpr int kBoxes = C::kKRows / 16;
+                for (int j = 0; j < n_tiles; ++j) {
+                    const int n0 = static_cast<int>(key_lo) + j * kBlockN +
+                                   (PAIR ? static_cast<int>(rank) * C::kKRows : 0);
+                    const int prow = paged_row(p, b, n0 + 16 * (lane < kBoxes ? lane : 0));
+                    const int slot = j % C::kSlotsK;
+                    mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);
+                    __syncwarp();
+                    uint8_t *dst = sK + slot * C::kKBytes;
                     if (lane == 0) {
                         if (PAIR) {
-                            tma_load_4d_pair(dst + i * 2048, &tmap_v, vfull0 + 8u * slot, static_cast<int>(rank) * 64,
-                                             g, r, 0, kKvPolicy);
+                            if (leader) mbar_arrive_expect_tx(&k_full[slot], 2u * C::kKBytes);
                         } else {
+                            mbar_arrive_expect_tx(&k_full[slot], C::kKBytes);
+                        }
+                    }
 #pragma unroll
-                            for (int kb = 0; kb < C::kKB; ++kb)
-                                tma_load_4d(dst + kb * (kBlockN * 128) + i * 2048, &tmap_v, &v_full[slot], kb * 64, g,
-                                            r, 0, kKvPolicy);
+                    for (int i = 0; i < kBoxes; ++i) {
+                        const int r = __shfl_sync(0xffffffffu, prow, i);
+                        if (lane == 0) {
+#pragma unroll
+                            for (int kb = 0; kb < C::kKB; ++kb) {
+                                uint8_t *dd = dst + kb * (C::kKRows * 128) + i * 2048;
+                                if (PAIR)
+                                    tma_load_4d_pair(dd, &tmap_k, kfull0 + 8u * slot, kb * 64, g, r, 0, kKvPolicy);
+                                else
+                                    tma_load_4d(dd, &tmap_k, &k_full[slot], kb * 64, g, r, 0, kKvPolicy);
+                            }
                         }
                     }
                 }
+            } else if (lane == 0) {
+                // contiguous cache: lane 0 alone loops (the other lanes wait at the __syncwarp below)
+                for (int j = 0; j < n_tiles; ++j) {
+                    const int n0 = static_cast<int>(key_lo) + j * kBlockN;
+                    const int slot = j % C::kSlotsK;
+                    mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);
+                    HTA_TR(30, j);
+                    uint8_t *dst = sK + slot * C::kKBytes;
+                    if (PAIR) {
+                        if (leader) mbar_arrive_expect_tx(&k_full[slot], 2u * C::kKBytes);
+#pragma unroll
+                        for (int kb = 0; kb < C::kKB; ++kb)
+                            tma_load_4d_pair(dst + kb * (C::kKRows * 128), &tmap_k, kfull0 + 8u * slot, kb * 64, g,
+                                             n0 + static_cast<int>(rank) * C::kKRows, b, kKvPolicy);
+                    } else {
+                        mbar_arrive_expect_tx(&k_full[slot], C::kKBytes);
+#pragma unroll
+                        for (int kb = 0; kb < C::kKB; ++kb)
+                            tma_load_4d(dst + kb * (kBlockN * 128), &tmap_k, &k_full[slot], kb * 64, g, n0, b,
+                                        kKvPolicy);
+                    }
+                }
             }
-        } else if ((HTA_CONV || lane == 0) && HTA_SKIP < 3) {
+            __syncwarp();
+        } else if (warp == 2) {
+            // ================= TMA producer of the V ring (V_j is consumed by PV_j).  The last
+            // tile of a split that ends at the sequence end may hold garbage (even NaN) rows past
+            // cache_seqlens (Z13): P is 0 there, but 0 x NaN is NaN in the MMA, so this warp zeroes
+            // those V rows in smem before the MMA may read them.  That tile's TMA completes on a
+            // barrier of this CTA (v_tail_land); the MMA warp then waits on v_tail_ready (both CTAs
+            // of a pair arrive) instead of v_full.
             const uint32_t vfull0 = PAIR ? mapa_shared(smem_u32(&v_full[0]), 0) : 0u;
-            for (int j = 0; j < n_tiles; ++j) {
-                const int n0 = static_cast<int>(key_lo) + j * kBlockN;
-                const int slot = j % C::kSlotsV;
-                mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
-                uint8_t *dst = sV + slot * C::kVBytes;
-                HTA_TR(31, 0, j);
-                if (lane != 0) {
-                } else if (PAIR) {
-                    if (leader) mbar_arrive_expect_tx(&v_full[slot], 2u * C::kVBytes);
-                    tma_load_4d_pair(dst, &tmap_v, vfull0 + 8u * slot, static_cast<int>(rank) * 64, g, n0, b,
-                                     kKvPolicy);
-                } else {
+            auto v_bar = [&](int j, int slot, bool tail) -> uint32_t {  // barrier the tile's TMA signals
+                if (tail) return smem_u32(v_tail_land);
+                return PAIR ? vfull0 + 8u * slot : smem_u32(&v_full[slot]);
+            };
+            auto v_expect = [&](int slot, bool tail) {
+                if (tail)
+                    mbar_arrive_expect_tx(v_tail_land, C::kVBytes);
+                else if (!PAIR)
                     mbar_arrive_expect_tx(&v_full[slot], C::kVBytes);
+                else if (leader)
+                    mbar_arrive_expect_tx(&v_full[slot], 2u * C::kVBytes);
+            };
+            // one 16-row box (paged) or the whole tile (box_rows = kBlockN) at key row r
+            auto v_load = [&](uint8_t *dst, uint32_t bar, bool tail, int r, int bb) {
+                if (PAIR && !tail)
+                    tma_load_4d_pair(dst, &tmap_v, bar, static_cast<int>(rank) * 64, g, r, bb, kKvPolicy);
+                else if (PAIR)
+                    tma_load_4d(dst, &tmap_v, v_tail_land, static_cast<int>(rank) * 64, g, r, bb, kKvPolicy);
+                else
 #pragma unroll
                     for (int kb = 0; kb < C::kKB; ++kb)
-                        tma_load_4d(dst + kb * (kBlockN * 128), &tmap_v, &v_full[slot], kb * 64, g, n0, b, kKvPolicy);
+                        tma_load_4d_bar(dst + kb * (kBlockN * 128), &tmap_v, bar, kb * 64, g, r, bb, kKvPolicy);
+            };
+            if (p.page_size > 0) {
+                constexpr int kBoxes = kBlockN / 16;
+                for (int j = 0; j < n_tiles; ++j) {
+                    const int n0 = static_cast<int>(key_lo) + j * kBlockN;
+                    const int prow = paged_row(p, b, n0 + 16 * (lane < kBoxes ? lane : 0));
+                    const int slot = j % C::kSlotsV;
+                    const bool tail = tail_zero && j == n_tiles - 1;
+                    mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
+                    __syncwarp();
+                    uint8_t *dst = sV + slot * C::kVBytes;
+                    if (lane == 0) v_expect(slot, tail);
+#pragma unroll
+                    for (int i = 0; i < kBoxes; ++i) {
+                        const int r = __shfl_sync(0xffffffffu, prow, i);
+                        if (lane == 0) v_load(dst + i * 2048, v_bar(j, slot, tail), tail, r, 0);
+                    }
                 }
-                if (HTA_CONV) __syncwarp();
+            } else if (lane == 0) {
+                for (int j = 0; j < n_tiles; ++j) {
+                    const int n0 = static_cast<int>(key_lo) + j * kBlockN;
+                    const int slot = j % C::kSlotsV;
+                    const bool tail = tail_zero && j == n_tiles - 1;
+                    mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
+                    HTA_TR(31, j);
+                    v_expect(slot, tail);
+                    v_load(sV + slot * C::kVBytes, v_bar(j, slot, tail), tail, n0, b);
+                }
             }
-        }
-        __syncwarp();
-    } else if (warp == 1) {
-        // ================= MMA issuer: the whole warp of the leader CTA runs this loop with
-        // warp-uniform values and elect.sync issues each tcgen05 op (one lane, no waterfall);
-        // descriptors are built once and advanced by constants, so the tensor pipe is never
-        // starved by issue overhead (a single divergent lane issues at half the N=128 MMA rate).
-        if (leader) {
+            __syncwarp();
+            if (tail_zero) {
+                mbar_wait(v_tail_land, 0);
+                __syncwarp();
+                uint8_t *vt = sV + ((n_tiles - 1) % C::kSlotsV) * C::kVBytes;
+                constexpr int kAtoms = C::kVCols / 64;  // 128-byte column atoms per key row
+                const int n_chunks = (kBlockN - tail_valid) * kAtoms * 8;  // 16-byte chunks to zero
+                for (int i = lane; i < n_chunks; i += 32) {
+                    const int row = tail_valid + i / (kAtoms * 8);
+                    const int atom = (i / 8) % kAtoms;
+                    *reinterpret_cast<uint4 *>(vt + atom * (kBlockN * 128) + row * 128 + (i % 8) * 16) =
+                        make_uint4(0u, 0u, 0u, 0u);
+                }
+                fence_proxy_async_smem();  // generic-proxy zeros -> read by the tensor core
+                __syncwarp();
+                if (lane == 0) {
+                    if (PAIR)
+                        mbar_arrive_remote_release_cluster(mapa_shared(smem_u32(v_tail_ready), 0));
+                    else
+                        mbar_arrive(v_tail_ready);
+                }
+            }
+        } else if (warp == 1 && leader) {
+            // ================= MMA issuer: the whole warp of the leader CTA runs this loop with
+            // warp-uniform values and elect.sync issues each tcgen05 op (one lane, no waterfall);
+            // descriptors are built once and advanced by constants.  Fixed order with suspended
+            // barrier waits: S_0, S_1, S_2, then per tile j: PV_j (needs V_j and P_j), S_{j+3}
+            // (needs K_{j+3}; its buffer was last read by PV_j, issued just before).
             constexpr int kM = PAIR ? 256 : 128;
             const uint32_t idesc_qk = idesc_bf16_f32(kM, kBlockN, 0);
             const uint32_t idesc_pv = idesc_bf16_f32(kM, D, 1);
             const uint64_t qd0 = sdesc_sw128(smem_u32(sQ), 16, 1024);
             const uint64_t kd0 = sdesc_sw128(smem_u32(sK), 16, 1024);
             const uint64_t vd0 = sdesc_sw128(smem_u32(sV), kBlockN * 128, 1024);
-            // One elected lane issues each group of MMAs; the descriptors are warp-uniform values
-            // computed outside the elected branch, so ptxas keeps them in uniform registers and
-            // each tcgen05.mma costs a few instructions (issue must stay well under 64 cycles per
-            // N=128 MMA, and this warp shares its sub-partition with two softmax warps).
             auto commit = [](uint64_t *bar) {
                 if (PAIR)
                     tc_commit2_mc(bar);
                 else
                     tc_commit(bar);
             };
-            auto issue_S = [&](int buf, int slot) {
-                if (HTA_SKIP == 1 || HTA_SKIP == 2) return;
-                const uint32_t d_t = tmem + s_col(buf);
-                const uint64_t kd = kd0 + static_cast<uint32_t>((slot * C::kKBytes) >> 4);
-#pragma unroll
-                for (int k = 0; k < D / 16; ++k) {
-                    // K-major SW128: +32 B per K step inside a 128-B atom, next atom = next region
-                    const uint32_t qo = ((k / 4) * C::kRegionBytes + (k % 4) * 32) >> 4;
-                    const uint32_t ko = ((k / 4) * (C::kKRows * 128) + (k % 4) * 32) >> 4;
-                    if (PAIR)
-                        mma2_bf16_ss(d_t, qd0 + qo, kd + ko, idesc_qk, k > 0 ? 1u : 0u);
-                    else
-                        mma_bf16_ss(d_t, qd0 + qo, kd + ko, idesc_qk, k > 0 ? 1u : 0u);
-                }
-            };
-            auto issue_PV = [&](int buf, int slot, bool acc) {
-                if (HTA_SKIP == 1 || HTA_SKIP == 2) return;
-                const uint32_t a_t = tmem + s_col(buf);
-                const uint64_t vd = vd0 + static_cast<uint32_t>((slot * C::kVBytes) >> 4);
-#pragma unroll
-                for (int k = 0; k < kBlockN / 16; ++k) {
-                    // MN-major SW128: 16 keys = two 8-row groups = +2048 B per K step
-                    if (PAIR)
-                        mma2_bf16_ts(tmem + kOCol, a_t + k * 8, vd + static_cast<uint32_t>(k * 128), idesc_pv,
-                                     (acc || k > 0) ? 1u : 0u);
-                    else
-                        mma_bf16_ts(tmem + kOCol, a_t + k * 8, vd + static_cast<uint32_t>(k * 128), idesc_pv,
-                                    (acc || k > 0) ? 1u : 0u);
-                }
-            };
             const bool issuer = elect_one() != 0;
-            // Fixed order with hardware-suspended waits (no polling: a spinning issuer would take
-            // issue slots from the softmax warps sharing its SM sub-partition):
-            //   S_0, S_1, then for every j: PV_j (needs V_j and P_j), S_{j+2} (needs K_{j+2}; its
-            //   buffer was last read by PV_j, issued just before).
-            constexpr bool kNoMem = HTA_SKIP >= 3;
-            auto wait_all = [](uint64_t *bar, uint32_t parity) {
-                mbar_wait(bar, parity);
-                __syncwarp();
-            };
             auto start_S = [&](int jj) {
-                if (!kNoMem) {
-                    wait_all(&k_full[jj % C::kSlotsK], (jj / C::kSlotsK) & 1);
-                    HTA_TR(23, 0, jj);
-                    if (tail_zero && jj == n_tiles - 1)  // the softmax warps sanitise V of this tile
-                        wait_all(&v_full[jj % C::kSlotsV], (jj / C::kSlotsV) & 1);
-                }
+                mbar_wait(&k_full[jj % C::kSlotsK], (jj / C::kSlotsK) & 1);
+                __syncwarp();
+                HTA_TR(2, jj);
                 tc_fence_after();
                 if (issuer) {
-                    issue_S(jj % C::kSBufs, jj % C::kSlotsK);
+                    const uint32_t d_t = tmem + s_col(jj % C::kSBufs);
+                    const uint64_t kd = kd0 + static_cast<uint32_t>(((jj % C::kSlotsK) * C::kKBytes) >> 4);
+#pragma unroll
+                    for (int k = 0; k < D / 16; ++k) {
+                        // K-major SW128: +32 B per K step inside a 128-B atom, next atom = next region
+                        const uint32_t qo = ((k / 4) * C::kRegionBytes + (k % 4) * 32) >> 4;
+                        const uint32_t ko = ((k / 4) * (C::kKRows * 128) + (k % 4) * 32) >> 4;
+                        if (PAIR)
+                            mma2_bf16_ss(d_t, qd0 + qo, kd + ko, idesc_qk, k > 0 ? 1u : 0u);
+                        else
+                            mma_bf16_ss(d_t, qd0 + qo, kd + ko, idesc_qk, k > 0 ? 1u : 0u);
+                    }
                     commit(&s_full[jj % C::kSBufs]);
                     commit(&k_empty[jj % C::kSlotsK]);
                 }
                 __syncwarp();
-                HTA_TR(21, 0, jj);
             };
             if (PAIR && !p.q_tma)
                 mbar_wait_cluster(q_full, 0);  // staged by both CTAs' threads (generic proxy)
             else
                 mbar_wait(q_full, 0);
             __syncwarp();
-            HTA_TR(22, 0, 0);
             for (int jj = 0; jj < C::kSBufs && jj < n_tiles; ++jj) start_S(jj);
             for (int j = 0; j < n_tiles; ++j) {
-                if (!kNoMem) wait_all(&v_full[j % C::kSlotsV], (j / C::kSlotsV) & 1);
-                HTA_TR(24, 0, j);
-                wait_all(&p_full[j % C::kSBufs], (j / C::kSBufs) & 1);
-                HTA_TR(1, 0, j);
+                if (tail_zero && j == n_tiles - 1) {  // the V producers sanitised this tile
+                    if (PAIR)
+                        mbar_wait_cluster(v_tail_ready, 0);
+                    else
+                        mbar_wait(v_tail_ready, 0);
+                } else {
+                    mbar_wait(&v_full[j % C::kSlotsV], (j / C::kSlotsV) & 1);
+                }
+                __syncwarp();
+                HTA_TR(3, j);
+                mbar_wait(&p_full[j % C::kSBufs], (j / C::kSBufs) & 1);
+                __syncwarp();
+                HTA_TR(1, j);
                 tc_fence_after();
                 if (issuer) {
-                    issue_PV(j % C::kSBufs, j % C::kSlotsV, j > 0);
+                    const uint32_t a_t = tmem + s_col(j % C::kSBufs);
+                    const uint64_t vd = vd0 + static_cast<uint32_t>(((j % C::kSlotsV) * C::kVBytes) >> 4);
+#pragma unroll
+                    for (int k = 0; k < kBlockN / 16; ++k) {
+                        // MN-major SW128: 16 keys = two 8-row groups = +2048 B per K step
+                        if (PAIR)
+                            mma2_bf16_ts(tmem + kOCol, a_t + k * 8, vd + static_cast<uint32_t>(k * 128), idesc_pv,
+                                         (j > 0 || k > 0) ? 1u : 0u);
+                        else
+                            mma_bf16_ts(tmem + kOCol, a_t + k * 8, vd + static_cast<uint32_t>(k * 128), idesc_pv,
+                                        (j > 0 || k > 0) ? 1u : 0u);
+                    }
                     commit(&pv_done[j % C::kSBufs]);
                     commit(&v_empty[j % C::kSlotsV]);
                 }
@@ -531,21 +509,23 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 if (j + C::kSBufs < n_tiles) start_S(j + C::kSBufs);
             }
             if (issuer) commit(o_final);
+            __syncwarp();
         }
-        __syncwarp();
     } else {
-        // ================= softmax: warp w owns rows 32*(w%4) + 16*rh .. +15 of the tile (rh =
-        // (w-3)/4); lane t holds row (t & 15) of them, keys [96*(t>>4), 96*(t>>4) + 96)
+        setmaxnreg_inc();
+        // ================= softmax: group grp takes tiles j = grp, grp + 2, ...; warp gw of a
+        // group owns rows 32*(gw%4) + 16*(gw/4) .. +15 of the tile (TMEM lane quarter gw % 4 =
+        // warp % 4); lane t holds row (t & 15) of them, keys [64*(t>>4), +64) of each tile.
         const int sw = warp - C::kFirstSoftmaxWarp;
-        if (!p.q_tma) {  // this CTA's 128 Q rows -> smem in the canonical K-major SWIZZLE_128B
-            // layout (G does not divide 128: no TMA box), staged by the softmax warps
+        const int grp = sw / C::kGroupWarps;
+        const int gw = sw % C::kGroupWarps;
+        if (!p.q_tma && grp == 0) {  // this CTA's 128 Q rows -> smem in the canonical K-major
+            // SWIZZLE_128B layout (G does not divide 128: no TMA box), staged by group 0
             const __nv_bfloat16 *q = static_cast<const __nv_bfloat16 *>(p.q);
-            constexpr int kQThreads = 32 * C::kSoftmaxWarps;
+            constexpr int kQThreads = 32 * C::kGroupWarps;
             constexpr int kChunks = D / 8;  // 16-byte chunks per row
             constexpr int kPer = (kRowsPerTile * kChunks + kQThreads - 1) / kQThreads;
             const int qt = threadIdx.x - 32 * C::kFirstSoftmaxWarp;
-            // all loads of a thread in flight at once (a load/store loop would serialise kPer cold
-            // HBM latencies)
             uint4 val[kPer];
 #pragma unroll
             for (int i = 0; i < kPer; ++i) {
@@ -568,7 +548,6 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             }
             fence_proxy_async_smem();  // generic-proxy stores -> read by the tensor core
             __syncwarp();
-            HTA_TR(14, sw, 0);
             if (lane == 0) {
                 if (PAIR)
                     mbar_arrive_remote_release_cluster(mapa_shared(smem_u32(q_full), 0));
@@ -577,7 +556,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             }
         }
         const int quarter = warp & 3;
-        const int rh = sw >> 2;
+        const int rh = gw >> 2;
         const int chalf = lane >> 4;
         const int r = quarter * 32 + rh * 16 + (lane & 15);
         const int grow = row0 + r;
@@ -585,89 +564,81 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32 + rh * 16) << 16;
         const float c = p.scale_log2;
         const uint32_t pfull0 = PAIR ? mapa_shared(smem_u32(&p_full[0]), 0) : 0u;
-        constexpr int kHalfCols = kBlockN / 2;
-        float m_run = -INFINITY, l_run = 0.f;  // l_run: this thread's 64 columns only
-        // Publish P_jp (stored to TMEM without waiting): wait for the stores (and any O rescale
-        // of that tile), sanitise the garbage V rows of the last tile, signal the MMA warp.
+        constexpr int kHalf = kBlockN / 2;  // S columns per thread
+        // m_run: the row's running max (log2 units) as last known to this group; the group's row
+        // sum l_run (this thread's columns of the group's tiles) is expressed in the scale m_run.
+        float m_run = -INFINITY, l_run = 0.f;
+#ifdef HTA_TRACE
+        uint32_t tr_c[6] = {0, 0, 0, 0, 0, 0};
+#endif
+        // Publish P_j: wait for its TMEM stores, sanitise the garbage V rows of the last tile,
+        // signal the MMA warp.
         auto publish = [&](int jp) {
             tmem_st_wait();
-            if (jp == n_tiles - 1 && tail_zero) {
-                // V rows (keys) past the sequence end: zero this CTA's part of key row r (may be
-                // NaN); the thread pair of row r splits the row's 16-byte chunks
-                for (int kr = r; kr < kBlockN; kr += kRowsPerTile) {  // key rows r and r + 128
-                    if (kr < tail_valid) continue;
-                    uint8_t *vrow = sV + ((n_tiles - 1) % C::kSlotsV) * C::kVBytes + kr * 128;
-                    constexpr int kChunks16 = C::kVCols * 2 / 16;  // 16-byte chunks in this CTA's row
-#pragma unroll
-                    for (int cch = chalf * (kChunks16 / 2); cch < (chalf + 1) * (kChunks16 / 2); ++cch)
-                        *reinterpret_cast<uint4 *>(vrow + (cch / 8) * (kBlockN * 128) + (cch % 8) * 16) =
-                            make_uint4(0u, 0u, 0u, 0u);
-                }
-                fence_proxy_async_smem();
-            }
+            HTA_TRS(4);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                const int pb = jp % C::kSBufs;
-                if (!PAIR)
-                    mbar_arrive(&p_full[pb]);
-                else if (jp == n_tiles - 1 && tail_zero)
-                    mbar_arrive_remote_release_cluster(pfull0 + 8u * pb);  // publishes zeroed V rows
+                if (PAIR)
+                    mbar_arrive_remote(pfull0 + 8u * (jp % C::kSBufs));
                 else
-                    mbar_arrive_remote(pfull0 + 8u * pb);
+                    mbar_arrive(&p_full[jp % C::kSBufs]);
             }
-            HTA_TR(13, sw, jp);
         };
-        // Deferred publication: P_{j-1} is published once S_j is ready, just before S_j is loaded,
-        // so the completion of P_{j-1}'s stores is waited for a tile later (long done) instead of
-        // right after the exponentials, on each tile's critical path.  No deadlock: S_j needs only
-        // P_{j-2}, published at the start of tile j-1.
-        constexpr bool kDefer = HTA_DEFER != 0;
-        for (int j = 0; j < n_tiles; ++j) {
+        for (int j = grp; j < n_tiles; j += 2) {
             const int buf = j % C::kSBufs;
             mbar_wait(&s_full[buf], static_cast<uint32_t>((j / C::kSBufs) & 1));
-            HTA_TR(10, sw, j);
             tc_fence_after();
-            const bool last = j == n_tiles - 1;
-            float mt = 0.f, lsum = 0.f;
+            HTA_TRS(0);
             if (pad_warp) {
                 // all 16 rows of this warp are padding (row >= M, e.g. M = 64 for MHA with T = 64):
                 // no softmax -- their P (and O) rows are never used -- only the protocol
-                if (kDefer && j > 0) publish(j - 1);
-                mt = m_run;
-            } else if (HTA_SKIP < 1 || HTA_SKIP == 4) {
-                float s[kHalfCols];  // this thread's S values: keys [kHalfCols*chalf, +kHalfCols)
-                if (kDefer && j > 0) publish(j - 1);
-                tmem_ld_S<kHalfCols>(tmem + lane_off + s_col(buf), s);
+                publish(j);
+                continue;
+            }
+            const bool last = j == n_tiles - 1;
+            // S_j of this thread in two chunks of 32 columns (keys [kHalf*chalf + 32*ch, +32)): the
+            // chunk's values are loaded, turned into packed P and dead before the next chunk
+            // loads, so the softmax fits its register budget without spills.  Keys past the split
+            // end -> -inf (last tile only; the empty asm keeps that a real branch).
+            constexpr int kChunk = 32;
+            float s[kChunk];
+            auto load_s = [&](int ch) {
+                tmem_ld_x32_nowait<kHalf>(tmem + lane_off + s_col(buf) + ch * kChunk, s);
+                tmem_ld_wait_fence<kChunk>(s);
                 if (last && tail_valid < kBlockN) {
-                    // keys past the split end -> -inf (last tile only; the empty asm keeps this a
-                    // real branch instead of per-element selects on every tile)
                     asm volatile("" ::: "memory");
-                    const int lim = tail_valid - chalf * kHalfCols;  // this thread's first invalid column
+                    const int lim = tail_valid - chalf * kHalf - ch * kChunk;  // first invalid column
 #pragma unroll
-                    for (int cc = 0; cc < kHalfCols; ++cc)
+                    for (int cc = 0; cc < kChunk; ++cc)
                         if (cc >= lim) s[cc] = -INFINITY;
                 }
-                // P = exp2(S*c - m) -> bf16 over S in TMEM; returns this thread's row sum.  3 of
-                // every 8 column pairs use the FMA-pipe polynomial, the rest MUFU ex2 (MUFU alone
-                // would co-limit the MMAs).  P packed (2 bf16 per column): keys [Ch, Ch + C) ->
-                // columns [Ch/2, Ch/2 + C/2) (C = kHalfCols, h = chalf), stored in 16-column
-                // chunks without waiting (one wait::st before P is published).
-                // xmax_poly: max exponent argument of the polynomial slots (their 2^j would wrap
-                // past 2^127 instead of saturating like MUFU's ex2); tracked on the speculative
-                // pass only, where an argument above 60 forces the redo anyway.
-                float xmax_poly = -INFINITY;
-                auto exp_store = [&](float m_use, auto spec) {
-                    constexpr bool kSpec = decltype(spec)::value;
-                    const float2 c2 = make_float2(c, c), neg2 = make_float2(-m_use, -m_use);
-                    float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-                    const float2 *s2 = reinterpret_cast<const float2 *>(s);
-                    uint32_t pk[16];
+            };
+            HTA_TRS(1);
+            // P = exp2(S*c - m) packed to bf16 in registers (2 per word: keys [Ch + 2i, Ch + 2i + 2)
+            // -> pk[i], h = chalf); returns this thread's row sum.  3 of every 8 column pairs on
+            // the FMA-pipe polynomial, the rest on MUFU.  xmax_poly: max exponent argument of the
+            // polynomial slots (their 2^j would wrap past 2^127 instead of saturating like MUFU's
+            // ex2), tracked on the speculative pass only, where an argument above 60 forces the
+            // redo anyway.  Nothing is stored to TMEM until the tile's running max is settled:
+            // S stays intact for a redo, and the hand-over below needs no TMEM traffic first.
+            float xmax_poly = -INFINITY;
+            uint32_t pk[kHalf / 2];
+            auto exp_pack = [&](float m_use, auto spec) {
+                constexpr bool kSpec = decltype(spec)::value;
+                const float2 c2 = make_float2(c, c), neg2 = make_float2(-m_use, -m_use);
+                float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int i = 0; i < kHalfCols / 2; ++i) {
+                for (int ch = 0; ch < kHalf / kChunk; ++ch) {
+                    load_s(ch);
+                    const float2 *s2 = reinterpret_cast<const float2 *>(s);
+#pragma unroll
+                    for (int i = 0; i < kChunk / 2; ++i) {
                         const float2 x = __ffma2_rn(s2[i], c2, neg2);
                         float2 pp;
-                        if ((i & 7) < HTA_POLY) {
+                        if (HTA_DIAG & 2) {
+                            pp = x;
+                        } else if ((i & 7) < kPolyPairs) {
                             if (kSpec) xmax_poly = max3f(xmax_poly, x.x, x.y);
                             pp = exp2_poly2<!kSpec>(x);
                         } else {
@@ -678,67 +649,63 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                             acc1 = __fadd2_rn(acc1, pp);
                         else
                             acc0 = __fadd2_rn(acc0, pp);
-                        pk[i & 15] = pack_bf16x2(pp.x, pp.y);
-                        if ((i & 15) == 15)
-                            tmem_st_16x16_split_nowait<kHalfCols / 2>(tmem + lane_off + s_col(buf) + (i - 15), pk);
-                        else if (i == kHalfCols / 2 - 1)  // a last chunk of 8 columns (48-column halves)
-                            tmem_st_16x8_split_nowait<kHalfCols / 2>(tmem + lane_off + s_col(buf) + (i & ~15), pk);
+                        pk[ch * (kChunk / 2) + i] = pack_bf16x2(pp.x, pp.y);
                     }
-                    return (acc0.x + acc1.x) + (acc0.y + acc1.y);
-                };
-                auto row_max = [&]() {  // max over the row (this thread's values and its pair's)
-                    float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
-#pragma unroll
-                    for (int cc = 4; cc + 8 <= kHalfCols; cc += 8) {
-                        mx0 = fmaxf(mx0, fmaxf(s[cc], s[cc + 4]));
-                        mx1 = fmaxf(mx1, fmaxf(s[cc + 1], s[cc + 5]));
-                        mx2 = fmaxf(mx2, fmaxf(s[cc + 2], s[cc + 6]));
-                        mx3 = fmaxf(mx3, fmaxf(s[cc + 3], s[cc + 7]));
-                    }
-                    static_assert(kHalfCols % 8 == 0, "4 + 8k + 4 columns");
-                    mx0 = fmaxf(mx0, s[kHalfCols - 4]);
-                    mx1 = fmaxf(mx1, s[kHalfCols - 3]);
-                    mx2 = fmaxf(mx2, s[kHalfCols - 2]);
-                    mx3 = fmaxf(mx3, s[kHalfCols - 1]);
-                    const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-                    return fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16)) * c;
-                };
-                if (HTA_SPEC_MAX) {
-                    // Speculative exponentials with the running max: no row-max reduction on the
-                    // critical path.  Exact as long as no P exceeds 2^60 (bf16 P and the fp32 O /
-                    // row sums have the range; floating point keeps the relative precision), which
-                    // the row sum checks; otherwise (always on the first tile, where m_run = -inf)
-                    // the warp redoes the tile with the true row max.
-                    HTA_TR(11, sw, j);
-                    lsum = exp_store(m_run, std::true_type{});
-                    mt = m_run;
-                    if (__any_sync(0xffffffffu, !(lsum <= 0x1p60f) || xmax_poly > 60.f)) {
-                        tmem_st_wait();  // the speculative P stores land before they are overwritten
-                        const float mx = row_max();
-                        mt = mx > m_run ? mx : m_run;
-                        lsum = exp_store(mt, std::false_type{});
-                    }
-                } else {
-                    // row max first, stale max (rescale only on a jump > 2^8): -DHTA_SPEC_MAX=0
-                    const float mx = row_max();
-                    HTA_TR(11, sw, j);
-                    mt = (mx > m_run + 8.0f) ? mx : m_run;
-                    lsum = exp_store(mt, std::false_type{});
                 }
-            } else {
-                if (kDefer && j > 0) publish(j - 1);
-                mt = 0.f;
-                lsum = 1.f;
+                return (acc0.x + acc1.x) + (acc0.y + acc1.y);
+            };
+            auto row_max = [&]() {  // max over the row (this thread's values and its pair's), x c
+                float mx = -INFINITY;
+#pragma unroll
+                for (int ch = 0; ch < kHalf / kChunk; ++ch) {
+                    load_s(ch);
+#pragma unroll
+                    for (int cc = 0; cc < kChunk; cc += 2) mx = max3f(mx, s[cc], s[cc + 1]);
+                }
+                return fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16)) * c;
+            };
+            // Speculative exponentials with m_run, the row's running max after tile j-2 (this
+            // group's last fold; tile j-1 is folded in below).
+            const float m_spec = m_run;
+            float lsum = exp_pack(m_spec, std::true_type{});
+            const bool ovf = __any_sync(0xffffffffu, !(lsum <= kSpecLimit) || xmax_poly > 60.f);
+            // rho_j: this tile's row max if the speculative pass overflowed, else -inf (the tile
+            // needs no larger running max than the row already has).  Handed to the group of tile
+            // j+1 at once: no group waits on the other before its own hand-over.
+            float rho = -INFINITY;
+            if (ovf) rho = row_max();  // (rare: a group's first tile, or a jump of the logits)
+            HTA_TRS(2);
+            // hand rho_j over ("no requirement" is -FLT_MAX rather than -inf, so the tagged word
+            // stays a finite float); both groups fold the same tagged values
+            const uint32_t gen = static_cast<uint32_t>((j / 3) & 1);
+            if (ovf) rho = __uint_as_float((__float_as_uint(rho) & ~1u) | gen);
+            if (chalf == 0) st_volatile_shared(&m_sh[(j % 3) * 128 + r], ovf ? __float_as_uint(rho) : (0xFF7FFFFEu | gen));
+            // the running max after tile j-1 (fold of rho_{j-1}), then after tile j; both groups
+            // fold the same sequence rho_0, rho_1, ... and agree on every tile's max
+            float m_prev = m_run;
+            if (j > 0 && !(HTA_DIAG & 4)) {
+                const uint32_t *src = &m_sh[((j - 1) % 3) * 128 + r];
+                const uint32_t want = static_cast<uint32_t>(((j - 1) / 3) & 1);
+                uint32_t wv = ld_volatile_shared(src);
+                if ((wv & 1u) != want) {
+                    const uint64_t t0 = global_ns();
+                    while (((wv = ld_volatile_shared(src)) & 1u) != want)
+                        if (global_ns() - t0 > kWatchdogNs) __trap();
+                }
+                m_prev = fold_max(m_prev, __uint_as_float(wv));
             }
-            HTA_TR(12, sw, j);
-            // Rescale O only when the running max moved.  O must then hold P_{j-1} V_{j-1} first:
-            // wait for PV_{j-1} on its own barrier pv_done[(j-1) % 2].  That barrier cannot run a
-            // phase ahead (PV_{j+1} needs P_{j+1}, not yet published), so the parity wait is exact
-            // although most tiles never wait.
-            const bool need = (j > 0) && (mt != m_run);
-            const float f = need ? fast_exp2(m_run - mt) : 1.0f;
-            l_run = l_run * f + lsum;
+            HTA_TRS(3);
+            const float m_fin = fold_max(m_prev, rho);
+            if (__any_sync(0xffffffffu, ovf || m_fin != m_spec)) lsum = exp_pack(m_fin, std::false_type{});
+            // P_j over S_j in TMEM (columns [Ch/2, Ch/2 + 32)), without waiting
+            if (!(HTA_DIAG & 1)) {
+                tmem_st_16x16_split_nowait<kHalf / 2>(tmem + lane_off + s_col(buf), pk);
+                tmem_st_16x16_split_nowait<kHalf / 2>(tmem + lane_off + s_col(buf) + 16, pk + 16);
+            }
+            // O holds the tiles before j in scale m_prev; raise it to m_fin (after PV_{j-1})
+            const bool need = j > 0 && m_fin != m_prev;
             if (__any_sync(0xffffffffu, need)) {
+                const float f = need ? fast_exp2(m_prev - m_fin) : 1.0f;
                 mbar_wait(&pv_done[(j - 1) % C::kSBufs], static_cast<uint32_t>(((j - 1) / C::kSBufs) & 1));
                 tc_fence_after();
 #pragma unroll 1
@@ -750,45 +717,66 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     tmem_st_16x32_split<D / 2>(tmem + lane_off + kOCol + ch, *reinterpret_cast<uint32_t(*)[32]>(o));
                 }
             }
-            m_run = mt;
-            if (!kDefer) publish(j);
+            l_run = (m_fin == m_run ? l_run : l_run * fast_exp2(m_run - m_fin)) + lsum;
+            m_run = m_fin;
+            publish(j);
+            HTA_TRS(5);
+            HTA_TRFLUSH(j);
         }
-        if (kDefer && n_tiles > 0) publish(n_tiles - 1);
-        // ---- epilogue: the thread pair of a row adds its two partial row sums
+        // ---- epilogue: the row sum over both groups and both column halves; each group writes
+        // half of the head dim.  The exchange reuses the K ring (every MMA has completed).
         mbar_wait(o_final, 0);
         tc_fence_after();
         pdl_launch_dependents();
-        const float l_tot = l_run + __shfl_xor_sync(0xffffffffu, l_run, 16);
+        float *x_m = reinterpret_cast<float *>(sK);   // [2 groups][128 rows][2 halves]
+        float *x_l = x_m + 2 * 128 * 2;
+        x_m[(grp * 128 + r) * 2 + chalf] = m_run;
+        x_l[(grp * 128 + r) * 2 + chalf] = l_run;
+        named_bar_sync(1, 32 * 2 * C::kGroupWarps);
+        float m_tot = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) m_tot = fmaxf(m_tot, x_m[((i >> 1) * 128 + r) * 2 + (i & 1)]);
+        float l_tot = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float mi = x_m[((i >> 1) * 128 + r) * 2 + (i & 1)];
+            const float li = x_l[((i >> 1) * 128 + r) * 2 + (i & 1)];
+            if (li > 0.f) l_tot += li * fast_exp2(mi - m_tot);
+        }
         const float inv = 1.0f / l_tot;
-        const bool row_ok = grow < p.M;
+        const bool row_ok = grow < p.M && !pad_warp;
         int t = 0, h = 0;
         if (row_ok) {
             t = grow / p.G;
             h = g * p.G + grow % p.G;
         }
-        float *dst = o_base + ((static_cast<int64_t>(b) * p.T + t) * p.H + h) * D + chalf * (D / 2);
-#pragma unroll
-        for (int ch = 0; ch < D / 2; ch += 32) {
+        // thread (row, chalf) of group grp: O columns [chalf*D/2 + grp*D/4, +D/4)
+        constexpr int kQ = D / 4;
+        float *dst = o_base + ((static_cast<int64_t>(b) * p.T + t) * p.H + h) * D + chalf * (D / 2) + grp * kQ;
+        if constexpr (kQ == 32) {
             float o[32];
-            tmem_ld_16x32_split<D / 2>(tmem + lane_off + kOCol + ch, o);
+            tmem_ld_16x32_split<D / 2>(tmem + lane_off + kOCol + grp * kQ, o);
             if (row_ok) {
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
-                    reinterpret_cast<float4 *>(dst + ch)[e] =
+                    reinterpret_cast<float4 *>(dst)[e] =
+                        make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
+            }
+        } else {
+            float o[16];
+            tmem_ld_16x16_split<D / 2>(tmem + lane_off + kOCol + grp * kQ, o);
+            if (row_ok) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    reinterpret_cast<float4 *>(dst)[e] =
                         make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
             }
         }
-        if (row_ok && chalf == 0)
-            lse_base[(static_cast<int64_t>(b) * p.H + h) * p.T + t] = (m_run + log2f(l_tot)) * 0.69314718055994530942f;
+        if (row_ok && chalf == 0 && grp == 0)
+            lse_base[(static_cast<int64_t>(b) * p.H + h) * p.T + t] = (m_tot + log2f(l_tot)) * 0.69314718055994530942f;
     }
 
-#ifdef HTA_TRACE
-    if (warp == 3) HTA_TR_CLK(52);
-    if (threadIdx.x == 96 && blockIdx.x < 1024) {
-        g_cta_times[blockIdx.x][3] = trace_globaltimer();
-        g_cta_times[blockIdx.x][2] = clock64() - g_cta_times[blockIdx.x][2];
-    }
-#endif
+    HTA_TR(63, 0);
     tc_fence_before();
     __syncthreads();
     if (PAIR) cluster_sync();  // no CTA of the pair leaves while the peer may still signal it
@@ -805,9 +793,6 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
 extern "C" __attribute__((visibility("default"))) int hta_debug_set_trace(void *buf, int cta) {
     if (cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf)) != cudaSuccess) return -1;
     return cudaMemcpyToSymbol(g_trace_cta, &cta, sizeof(cta)) == cudaSuccess ? 0 : -1;
-}
-extern "C" __attribute__((visibility("default"))) int hta_debug_cta_times(void *host_out) {
-    return cudaMemcpyFromSymbol(host_out, g_cta_times, sizeof(g_cta_times)) == cudaSuccess ? 0 : -1;
 }
 #endif
 

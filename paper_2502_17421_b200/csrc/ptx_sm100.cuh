@@ -57,6 +57,15 @@ __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// Shared-memory word read/written with volatile semantics (flag hand-over between warps).
+__device__ __forceinline__ uint32_t ld_volatile_shared(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile_shared(uint32_t *p, uint32_t v) {
+    asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
 // Named barrier among `nthreads` threads (ids 1..15; 0 is __syncthreads).
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -72,7 +81,7 @@ __device__ __forceinline__ uint64_t global_ns() {
     return t;
 }
 // Watchdog of the waits below: a wait that has not completed after kWatchdogNs of wall time is a
-// protocol bug; trap (a reported kernel fault) instead of hanging the GPU.
+// protocol bug; trap (a reported kernel fault, cudaErrorLaunchFailure) instead of hanging the GPU.
 constexpr uint64_t kWatchdogNs = 2000000000ull;  // 2 s (the longest kernel runs well under 1 ms)
 
 // Wait for the phase with the given parity to complete.
@@ -81,10 +90,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     if (mbar_try_wait(a, parity)) return;
     const uint64_t t0 = global_ns();
     while (!mbar_try_wait(a, parity)) {
-        if (global_ns() - t0 > kWatchdogNs) {
-            printf("hta: mbarrier wait timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
-            __trap();
-        }
+        if (global_ns() - t0 > kWatchdogNs) __trap();
     }
 }
 
@@ -105,10 +111,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity
     if (mbar_try_wait_cluster(a, parity)) return;
     const uint64_t t0 = global_ns();
     while (!mbar_try_wait_cluster(a, parity)) {
-        if (global_ns() - t0 > kWatchdogNs) {
-            printf("hta: cluster mbarrier wait timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
-            __trap();
-        }
+        if (global_ns() - t0 > kWatchdogNs) __trap();
     }
 }
 
@@ -154,6 +157,15 @@ __device__ __forceinline__ void tma_load_4d(void *smem_dst, const void *map, uin
         "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(smem_dst)),
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
+        : "memory");
+}
+// The same with the completion barrier given as a shared::cta address.
+__device__ __forceinline__ void tma_load_4d_bar(void *smem_dst, const void *map, uint32_t bar, int c0, int c1, int c2,
+                                                int c3, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(smem_dst)),
+        "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
         : "memory");
 }
 // Pair TMA: data lands in this CTA's smem, completion bytes are counted on `bar_cluster`
@@ -485,6 +497,18 @@ __device__ __forceinline__ void tmem_ld_16x32_split(uint32_t taddr, float (&v)[3
         "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], %33;\n\t"
         "tcgen05.wait::ld.sync.aligned;"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr), "n"(SPLIT)
+        : "memory");
+}
+// 16 columns per half (half offset SPLIT) with the wait.
+template <int SPLIT>
+__device__ __forceinline__ void tmem_ld_16x16_split(uint32_t taddr, float (&v)[16]) {
+    uint32_t *r = reinterpret_cast<uint32_t *>(v);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x32bx2.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16], %17;\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr), "n"(SPLIT)
         : "memory");
 }

@@ -59,16 +59,17 @@ def test_workspace_size_matches_split_plan(L):
     # split, 9 splits = 144 CTAs
     s = _shape()
     assert L.hta_workspace_size(ctypes.byref(s), 148) == 9 * part(s)
-    # forced splits are capped by the number of 192-key tiles
+    # forced splits are capped by the number of 128-key tiles (and rounded to whole tiles per
+    # split: 8 tiles in 7 splits = 2 tiles per split = 4 splits)
     s = _shape(N=300, splits=7)
-    assert L.hta_workspace_size(ctypes.byref(s), 148) == 2 * part(s)
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == 3 * part(s)
     s = _shape(N=1000, splits=7)
-    assert L.hta_workspace_size(ctypes.byref(s), 148) == 6 * part(s)
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == 4 * part(s)
     s = _shape(N=0)
     assert L.hta_workspace_size(ctypes.byref(s), 148) == 1 * part(s)
     # QwQ-like: M = 320 rows.  Pairs: 2 row groups x 8 kv heads x B=4 = 128 CTAs per split, best
-    # 1 split (one wave of 171 tiles).  Single CTAs: 3 row groups = 96 CTAs per split, 3 splits =
-    # 288 CTAs = 2 waves of 57 tiles -> the planner takes single CTAs with 3 splits
+    # 1 split (one wave of 256 tiles).  Single CTAs: 3 row groups = 96 CTAs per split, 3 splits =
+    # 288 CTAs = 2 waves of 86 tiles -> the planner takes single CTAs with 3 splits
     s = _shape(B=4, H=40, N=32768)
     assert L.hta_workspace_size(ctypes.byref(s), 148) == 3 * part(s)
 

@@ -1,15 +1,20 @@
 """Pipeline timeline of one CTA of the prefix kernel (diagnostics; needs libhta_trace.so).
 
     python -m paper_2502_17421_b200.build --trace
-    HTA_LIB=paper_2502_17421_b200/libhta_trace.so python tools/trace_prefix.py [workload]
+    HTA_LIB=paper_2502_17421_b200/libhta_trace.so python tools/trace_prefix.py [workload] [cta]
 
-Events (see HTA_TR in csrc/prefix_tc.cu): MMA warp 1 = p_full satisfied (PV about to issue);
-softmax warp: 10 = S ready, 11 = S loaded + row max, 12 = exp loop done, 13 = P published.
+Events (HTA_TR in csrc/prefix_tc.cu), per warp, clock64 cycles:
+  MMA warp 1:  2 = K_j landed, S_j issue   3 = V_j landed   1 = P_j published, PV_j issue
+  producers:   30 = K slot j free, TMA issued (warp 0)   31 = V slot j (warp 2)
+  softmax:     10 = S_j ready   11 = S_j loaded   12 = exponentials done   13 = hand-over of
+               tile j-1 read   15 = P_j stores landed   14 = P_j published
+  all warps:   0 = kernel entry   63 = exit
 """
 import ctypes
 import os
 import statistics
 import sys
+from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -20,6 +25,8 @@ import torch  # noqa: E402
 from paper_2502_17421_b200 import hta  # noqa: E402
 from workloads.generators import config_workload  # noqa: E402
 
+RECS = 1024
+
 
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "llama8b_64k"
@@ -28,105 +35,88 @@ def main():
     w = config_workload(name, seed=0)
     x = [t.to(dev) for t in (w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree)]
     mask = hta.hta_build_tree_mask(w.parents[0].to(dev))
-    fwd = lambda: hta.hta_forward(*x, mask)  # noqa: E731
-    if os.environ.get("PAGED"):  # the paged forward over in-order 16-key pages
-        page = 16
-        maxp = w.N // page
-        kp = x[1].reshape(w.B * maxp, page, w.H_kv, w.d).contiguous()
-        vp = x[2].reshape(w.B * maxp, page, w.H_kv, w.d).contiguous()
-        bt = torch.arange(w.B * maxp, dtype=torch.int32, device=dev).view(w.B, maxp)
-        fwd = lambda: hta.hta_forward_paged(x[0], kp, vp, bt, x[3], x[4], mask)  # noqa: E731
     L = hta.lib()
     L.hta_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    L.hta_debug_cta_times.argtypes = [ctypes.c_void_p]
-    buf = torch.zeros(32 * 2048, dtype=torch.int64, device=dev)
-    fwd()
+    buf = torch.zeros(32 * RECS, dtype=torch.int64, device=dev)
+    hta.hta_forward(*x, mask)
     torch.cuda.synchronize()
     assert L.hta_debug_set_trace(ctypes.c_void_p(buf.data_ptr()), cta) == 0
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    warm = int(os.environ.get("TRACE_WARM", "0"))  # back-to-back launches first (sustained load)
     for _ in range(3):
-        for _ in range(warm):
-            fwd()
         buf.zero_()
-        flush.zero_()  # cold L2, as in bench.py
-        fwd()
+        flush.zero_()
+        flush.view(torch.float32).sum()
+        hta.hta_forward(*x, mask)
         torch.cuda.synchronize()
-    times = (ctypes.c_uint64 * 8192)()
-    if L.hta_debug_cta_times(times) == 0:
-        n_cta = 0
+    L.hta_debug_set_trace(None, -1)
+    raw = buf.cpu().view(32, RECS).tolist()
+    ev = defaultdict(dict)  # (warp, event) -> {tile: clock}
+    t0 = None
+    for wi in range(32):
+        last = 0
+        hi = 0
+        for r in raw[wi]:
+            if r == 0:
+                break
+            r &= (1 << 64) - 1
+            e, j, c = r >> 56, (r >> 32) & 0xFFFFFF, r & 0xFFFFFFFF
+            c += hi
+            if c < last:  # 32-bit wrap
+                hi += 1 << 32
+                c += 1 << 32
+            last = c
+            ev[(wi, e)][j] = c
+            if e == 0:
+                t0 = c if t0 is None else min(t0, c)
+    if t0 is None:
+        print("no trace records")
+        return
+    rel = lambda c: c - t0  # noqa: E731
+    exit_t = max(rel(v[0]) for (wi, e), v in ev.items() if e == 63)
+    print(f"{name} CTA {cta}: exit at {exit_t} cycles after the first entry")
+    mma = {e: ev.get((1, e), {}) for e in (1, 2, 3)}
+    tiles = sorted(mma[1])
+    if tiles:
+        pv = [rel(mma[1][j]) for j in tiles]
+        per = [b - a for a, b in zip(pv, pv[1:])]
+        print(f"MMA: {len(tiles)} PV issues, first at {pv[0]}, last at {pv[-1]}; period median "
+              f"{statistics.median(per) if per else 0:.0f} (p10 {sorted(per)[len(per) // 10] if per else 0}, "
+              f"p90 {sorted(per)[9 * len(per) // 10] if per else 0})")
+        # what gates PV_j: V landed (3) or P published (1 fires after 3)
+        gate_v = [rel(mma[3][j]) for j in tiles if j in mma[3]]
+        print(f"     V_j landed -> PV_j issued gap median {statistics.median([a - b for a, b in zip(pv, gate_v)]):.0f}")
+        if mma[2]:
+            s_is = [rel(mma[2][j]) for j in sorted(mma[2])]
+            print(f"     S issues: first {s_is[0]}, K_0..2 landed at {s_is[:3]}")
+    for wi in range(4, 20):
+        ten = ev.get((wi, 10), {})
+        if not ten:
+            continue
         rows = []
-        for i in range(1024):
-            e, ls, clk, x = times[4 * i: 4 * i + 4]  # g_cta_times[1024][4] (prefix_tc.cu)
-            if e == 0 or x == 0:
-                break
-            rows.append((e, ls, clk, x))
-        t0 = min(r[0] for r in rows)
-        ent = [(r[0] - t0) / 1e3 for r in rows]
-        pro = [(r[1] - r[0]) / 1e3 for r in rows]
-        ext = [(r[3] - t0) / 1e3 for r in rows]
-        mhz = [r[2] / (r[3] - r[1]) * 1e3 for r in rows]
-        slow = sorted(range(len(rows)), key=lambda i: -ext[i])[:12]
-        print("slowest CTAs (blockIdx: exit us):", ", ".join(f"{i}:{ext[i]:.1f}" for i in slow))
-        print(f"{len(rows)} CTAs: entry spread {max(ent):.1f} us; prologue {statistics.mean(pro):.1f} us "
-              f"(max {max(pro):.1f}); exit min {min(ext):.1f} median {statistics.median(ext):.1f} max {max(ext):.1f} us; "
-              f"SM clock {statistics.median(mhz):.0f} MHz")
-        q = sorted(ext)
-        print("exit quantiles (us): " + " ".join(f"p{p}={q[min(len(q) - 1, len(q) * p // 100)]:.1f}"
-                                               for p in (10, 25, 50, 75, 90, 100)))
-    recs = []
-    for warp, row in enumerate(buf.view(32, 2048).cpu().tolist()):
-        for v in row:
-            if v == 0:
-                break
-            v &= (1 << 64) - 1
-            recs.append((v & 0xFFFFFFFF, v >> 56, (v >> 52) & 0xF, (v >> 32) & 0xFFFFF, warp))
-    raw = {r[1]: r[0] for r in recs if r[1] in (50, 51, 52, 53)}
-    if len(raw) == 4:
-        cyc = (raw[52] - raw[50]) & 0xFFFFFFFF
-        ns = (raw[53] - raw[51]) & 0xFFFFFFFF
-        print(f"kernel body: {cyc} cycles in {ns / 1e3:.1f} us -> SM clock {cyc / ns * 1e3:.0f} MHz")
-    recs = [r for r in recs if r[1] < 50]
-    t0 = min(r[0] for r in recs)
-    ev = {}
-    for c, e, wg, j, warp in recs:
-        ev[(e, wg, j)] = c - t0
-    js = sorted({k[2] for k in ev})
-    print(f"{name} cta {cta}: {len(js)} KV tiles")
-    print("   j | K issued  K landed  S issued | S ready  max   exp | P all pub | V issued  V landed  P seen(PV) | K lat  V lat")
-    rows = []
-    for j in js:
-        g = lambda e, w=0: ev.get((e, w, j), -1)
-        pub = [ev[(13, w, j)] for w in range(16) if (13, w, j) in ev]
-        pm = max(pub) if pub else -1
-        rows.append((j, g(30), g(23), g(21), g(10), g(11), g(12), pm, g(31), g(24), g(1)))
-        print(f"{j:4d} | {g(30):8d} {g(23):8d} {g(21):8d} | {g(10):8d} {g(11)-g(10):5d} {g(12)-g(11):5d} | {pm:8d} | "
-              f"{g(31):8d} {g(24):8d} {g(1):8d} | {g(23)-g(30):5d} {g(24)-g(31):5d}")
-    mid = rows[3:-3] if len(rows) > 8 else rows
-    if len(mid) > 2:
-        per = (mid[-1][4] - mid[0][4]) / (len(mid) - 1)
-        print(f"period (S ready to S ready, middle tiles): {per:.0f} cycles")
-        wait_k = statistics.mean(max(0, r[2] - r[7 - 0] if False else 0) for r in mid)
-        kl = statistics.mean(r[2] - r[1] for r in mid)
-        vl = statistics.mean(r[9] - r[8] for r in mid)
-        print(f"mean TMA latency (issue -> MMA warp sees full): K {kl:.0f}  V {vl:.0f} cycles")
-        # what gated each PV issue: the later of V landed and P published
-        gate_p = sum(1 for r in mid if r[10] - r[9] > 50)
-        print(f"PV gated by P publication on {gate_p} of {len(mid)} tiles (else by V data)")
-        print(" warp sm  SMSP  S->max  max->exp  exp->pub(next tile)  pub lag vs earliest warp")
-        jm = [r[0] for r in mid]
-        for w in range(16):
-            a = [ev[(11, w, j)] - ev[(10, w, j)] for j in jm if (11, w, j) in ev and (10, w, j) in ev]
-            b = [ev[(12, w, j)] - ev[(11, w, j)] for j in jm if (12, w, j) in ev and (11, w, j) in ev]
-            c = [ev[(13, w, j)] - ev[(12, w, j)] for j in jm if (13, w, j) in ev and (12, w, j) in ev]
-            lag = [ev[(13, w, j)] - min(ev[(13, x, j)] for x in range(16) if (13, x, j) in ev) for j in jm
-                   if (13, w, j) in ev]
-            if a:
-                print(f"  {w:3d}  {(w + 3) % 4:3d}  {statistics.mean(a):6.0f}  {statistics.mean(b):7.0f}  "
-                      f"{statistics.mean(c) if c else 0:10.0f}  {statistics.mean(lag) if lag else 0:10.0f}")
-        sm = statistics.mean(r[5] - r[4] for r in mid)
-        se = statistics.mean(r[6] - r[5] for r in mid)
-        print(f"softmax warp 0: S ready -> max {sm:.0f}, max -> exp done {se:.0f}")
+        for j in sorted(ten):
+            r = [ev.get((wi, e), {}).get(j) for e in (10, 11, 12, 13, 15, 14)]
+            if None in r:
+                continue
+            rows.append([r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[5] - r[4]])
+        if not rows:
+            continue
+        med = [statistics.median(c[i] for c in rows) for i in range(5)]
+        starts = sorted(ten)
+        gaps = [ten[b] - ev[(wi, 14)][a] for a, b in zip(starts, starts[1:]) if a in ev[(wi, 14)]]
+        print(f"softmax warp {wi:2d} (group {(wi - 4) // 8}): {len(rows)} tiles; median S ready->loaded "
+              f"{med[0]:.0f}, exps {med[1]:.0f}, ->token {med[2]:.0f}, ->P stored {med[3]:.0f}, ->published {med[4]:.0f}; "
+              f"idle waiting for S {statistics.median(gaps) if gaps else 0:.0f}")
+    # timeline of a window of tiles: group warp 4 (even tiles) and 12 (odd tiles), MMA warp 1
+    print("tile: S_j issued | S_j ready | loaded | exps done | token read | published | PV_j issued   (cycles)")
+    mid = len(tiles) // 2 if tiles else 0
+    for j in range(max(0, mid - 4), mid + 4):
+        wi = 4 if j % 2 == 0 else 12
+        get = lambda w, e: ev.get((w, e), {}).get(j)  # noqa: E731
+        vals = [get(1, 2), get(wi, 10), get(wi, 11), get(wi, 12), get(wi, 13), get(wi, 14), get(1, 1)]
+        print(f"{j:4d}: " + " | ".join("-" if v is None else str(rel(v)) for v in vals))
+    if "--raw" in sys.argv:
+        for (wi, e), v in sorted(ev.items()):
+            print(wi, e, [(j, rel(c)) for j, c in sorted(v.items())][:12])
 
 
 if __name__ == "__main__":
