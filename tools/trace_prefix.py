@@ -74,7 +74,14 @@ def main():
     rel = lambda c: c - t0  # noqa: E731
     exit_t = max(rel(v[0]) for (wi, e), v in ev.items() if e == 63)
     print(f"{name} CTA {cta}: exit at {exit_t} cycles after the first entry")
-    mma = {e: ev.get((1, e), {}) for e in (1, 2, 3)}
+    # roles from the records: the MMA warp logs events 1-3, softmax warps event 10 (group = tile parity)
+    mw = next((w for w in range(32) if (w, 1) in ev), 1)
+    sm = [w for w in range(32) if (w, 10) in ev]
+    grp = {w: min(ev[(w, 10)]) % 2 for w in sm}
+    g0 = [w for w in sm if grp[w] == 0]
+    g1 = [w for w in sm if grp[w] == 1]
+    print(f"MMA warp {mw}; group 0 warps {g0}; group 1 warps {g1}")
+    mma = {e: ev.get((mw, e), {}) for e in (1, 2, 3)}
     tiles = sorted(mma[1])
     if tiles:
         pv = [rel(mma[1][j]) for j in tiles]
@@ -88,7 +95,7 @@ def main():
         if mma[2]:
             s_is = [rel(mma[2][j]) for j in sorted(mma[2])]
             print(f"     S issues: first {s_is[0]}, K_0..2 landed at {s_is[:3]}")
-    for wi in range(4, 20):
+    for wi in sm:
         ten = ev.get((wi, 10), {})
         if not ten:
             continue
@@ -103,17 +110,47 @@ def main():
         med = [statistics.median(c[i] for c in rows) for i in range(5)]
         starts = sorted(ten)
         gaps = [ten[b] - ev[(wi, 14)][a] for a, b in zip(starts, starts[1:]) if a in ev[(wi, 14)]]
-        print(f"softmax warp {wi:2d} (group {(wi - 4) // 8}): {len(rows)} tiles; median S ready->loaded "
+        print(f"softmax warp {wi:2d} (group {grp[wi]}): {len(rows)} tiles; median S ready->loaded "
               f"{med[0]:.0f}, exps {med[1]:.0f}, ->token {med[2]:.0f}, ->P stored {med[3]:.0f}, ->published {med[4]:.0f}; "
               f"idle waiting for S {statistics.median(gaps) if gaps else 0:.0f}")
     # timeline of a window of tiles: group warp 4 (even tiles) and 12 (odd tiles), MMA warp 1
     print("tile: S_j issued | S_j ready | loaded | exps done | token read | published | PV_j issued   (cycles)")
     mid = len(tiles) // 2 if tiles else 0
     for j in range(max(0, mid - 4), mid + 4):
-        wi = 4 if j % 2 == 0 else 12
+        wi = g0[0] if j % 2 == 0 else g1[0]
         get = lambda w, e: ev.get((w, e), {}).get(j)  # noqa: E731
-        vals = [get(1, 2), get(wi, 10), get(wi, 11), get(wi, 12), get(wi, 13), get(wi, 14), get(1, 1)]
+        vals = [get(mw, 2), get(wi, 10), get(wi, 11), get(wi, 12), get(wi, 13), get(wi, 14), get(mw, 1)]
         print(f"{j:4d}: " + " | ".join("-" if v is None else str(rel(v)) for v in vals))
+    # critical chain per tile: S_j ready (first warp of its group) -> last warp of the group
+    # published P_j -> PV_j issued -> S_{j+3} issued (by the MMA warp)
+    print("tile: S ready(first) | P published (first..last warp) | PV_j issued | S_j+3 issued | S_j+3 ready")
+    for j in range(max(0, mid - 6), mid + 6):
+        ws = g0 if j % 2 == 0 else g1
+        r10 = [ev.get((w, 10), {}).get(j) for w in ws]
+        r14 = [ev.get((w, 14), {}).get(j) for w in ws]
+        r10 = [rel(x) for x in r10 if x is not None]
+        r14 = [rel(x) for x in r14 if x is not None]
+        pv = ev.get((mw, 1), {}).get(j)
+        s3 = ev.get((mw, 2), {}).get(j + 3)
+        ws3 = g0 if (j + 3) % 2 == 0 else g1
+        r3 = [ev.get((w, 10), {}).get(j + 3) for w in ws3]
+        r3 = [rel(x) for x in r3 if x is not None]
+        if r10 and r14:
+            print(f"{j:4d}: {min(r10)} | {min(r14)}..{max(r14)} (+{max(r14) - min(r10)}) | "
+                  f"{rel(pv) if pv else '-'} (+{rel(pv) - max(r14) if pv else 0}) | {rel(s3) if s3 else '-'} | "
+                  f"{min(r3) if r3 else '-'} (+{min(r3) - rel(s3) if r3 and s3 else 0})")
+    # per warp: median lag of its publish behind the first warp of its group
+    lags = defaultdict(list)
+    for j in range(2, len(tiles) - 2):
+        ws = list(g0 if j % 2 == 0 else g1)
+        t = {w: ev.get((w, 14), {}).get(j) for w in ws}
+        if None in t.values():
+            continue
+        t0 = min(t.values())
+        for w in ws:
+            lags[w].append(t[w] - t0)
+    print("publish lag behind the group's first warp (median):",
+          {w: int(statistics.median(v)) for w, v in sorted(lags.items())})
     if "--raw" in sys.argv:
         for (wi, e), v in sorted(ev.items()):
             print(wi, e, [(j, rel(c)) for j, c in sorted(v.items())][:12])
