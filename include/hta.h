@@ -203,6 +203,17 @@ hta_status_t hta_accept_greedy(const int32_t *parents, const int32_t *draft_toke
                                int32_t context_argmax, int32_t *path, int32_t *path_len,
                                int32_t *bonus, int32_t on_device, hta_stream_t stream);
 
+/* The per-step tree work of a verification step in ONE launch on `stream` (device pointers):
+ * the tree mask of `parents` (as hta_build_tree_mask with on_device = 1; mask may be NULL to skip
+ * it) and the greedy accepted path (as hta_accept_greedy with on_device = 1).  Invalid parent
+ * entries give all-zero mask rows and path_len = -1.  The kernel lets the next kernel on the
+ * stream start its prologue at once (programmatic dependent launch), so a following hta_forward,
+ * which needs the mask only in its tree pass, is barely delayed by it. */
+hta_status_t hta_tree_step(const int32_t *parents, int32_t T, uint8_t *mask,
+                           const int32_t *draft_tokens, const int32_t *target_argmax, int32_t root,
+                           int32_t context_argmax, int32_t *path, int32_t *path_len,
+                           int32_t *bonus, hta_stream_t stream);
+
 /* commit_kv ("the large model only updates its KV cache upon
  * verification completion"): append the accepted tree nodes' K/V rows to the cache, in path
  * order, on the device (no host round trip between acceptance and the next step).

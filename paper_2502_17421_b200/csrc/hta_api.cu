@@ -539,6 +539,19 @@ hta_status_t hta_build_tree_mask(const int32_t *parents, int32_t T, uint8_t *mas
                                                                                                     : HTA_ERR_CUDA;
 }
 
+hta_status_t hta_tree_step(const int32_t *parents, int32_t T, uint8_t *mask, const int32_t *draft_tokens,
+                           const int32_t *target_argmax, int32_t root, int32_t context_argmax, int32_t *path,
+                           int32_t *path_len, int32_t *bonus, hta_stream_t stream) {
+    if (T < 1 || T > 256 || root < -1 || root >= T) return HTA_ERR_INVALID_ARGUMENT;
+    if (!parents || !draft_tokens || !target_argmax || !path || !path_len || !bonus) return HTA_ERR_INVALID_ARGUMENT;
+    hta_status_t r = check_device();
+    if (r != HTA_OK) return r;
+    return launch_tree_step(parents, T, mask, draft_tokens, target_argmax, root, context_argmax, path, path_len,
+                            bonus, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? HTA_OK
+               : HTA_ERR_CUDA;
+}
+
 hta_status_t hta_validate_tree_mask(const uint8_t *mask, int32_t T) {
     if (mask == nullptr || T < 1 || T > 256) return HTA_ERR_INVALID_ARGUMENT;
     for (int i = 0; i < T; ++i) {

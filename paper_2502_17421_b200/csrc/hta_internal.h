@@ -95,6 +95,9 @@ cudaError_t launch_commit_kv(const int32_t *path, int64_t path_stride, const int
                              const void *vt, void *kc, void *vc, const int32_t *seqlens, int32_t *seqlens_out,
                              const CommitGeom &gm, int B, cudaStream_t s);
 cudaError_t launch_build_mask(const int32_t *parents, int T, uint8_t *mask, cudaStream_t s);
+// Mask (if mask != nullptr) and greedy accepted path (if draft != nullptr) in one launch.
+cudaError_t launch_tree_step(const int32_t *parents, int T, uint8_t *mask, const int32_t *draft, const int32_t *tgt,
+                             int root, int ctx, int32_t *path, int32_t *path_len, int32_t *bonus, cudaStream_t s);
 cudaError_t launch_accept(const int32_t *parents, const int32_t *draft, const int32_t *tgt, int T, int root,
                           int ctx, int32_t *path, int32_t *path_len, int32_t *bonus, cudaStream_t s);
 

@@ -321,6 +321,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     const int slot = j % C::kSlotsK;
                     mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);
                     __syncwarp();
+                    HTA_TR(30, j);
                     uint8_t *dst = sK + slot * C::kKBytes;
                     if (lane == 0) {
                         if (PAIR) {
@@ -408,6 +409,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     const bool tail = tail_zero && j == n_tiles - 1;
                     mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
                     __syncwarp();
+                    HTA_TR(31, j);
                     uint8_t *dst = sV + slot * C::kVBytes;
                     if (lane == 0) v_expect(slot, tail);
 #pragma unroll

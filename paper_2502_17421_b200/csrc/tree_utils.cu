@@ -32,46 +32,8 @@ int host_build_mask(const int32_t *parents, int T, uint8_t *mask) {
     return 0;
 }
 
-__global__ void __launch_bounds__(256) build_mask_kernel(const int32_t *__restrict__ parents, int T,
-                                                         uint8_t *__restrict__ mask) {
-    __shared__ int32_t par[256];
-    const int i = threadIdx.x;
-    // the next kernel (hta_forward's prefix pass, which needs no mask) may start its prologue now;
-    // whoever reads the mask does so after griddepcontrol.wait
-    pdl_launch_dependents();
-    if (i < T) par[i] = parents[i];  // one coalesced load; the chain walks below hit smem
-    __syncthreads();
-    if (i >= T) return;
-    uint32_t bits[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-    bool ok = true;
-    int a = i;
-    while (a >= 0) {  // parent indices strictly decrease, so this terminates
-        bits[a >> 5] |= 1u << (a & 31);
-        const int pa = par[a];
-        if (pa < -1 || pa >= a) {
-            ok = false;
-            break;
-        }
-        a = pa;
-    }
-    uint8_t *row = mask + static_cast<int64_t>(i) * T;
-    if (!ok)
-        for (int w = 0; w < 8; ++w) bits[w] = 0u;
-    if ((T & 3) == 0) {  // rows are 4-byte aligned: store 4 mask bytes at a time
-        for (int j = 0; j < T; j += 4) {
-            const uint32_t nib = (bits[j >> 5] >> (j & 31)) & 0xFu;
-            const uint32_t word = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
-            *reinterpret_cast<uint32_t *>(row + j) = word;
-        }
-    } else {
-        for (int j = 0; j < T; ++j) row[j] = static_cast<uint8_t>((bits[j >> 5] >> (j & 31)) & 1u);
-    }
-}
-
 cudaError_t launch_build_mask(const int32_t *parents, int T, uint8_t *mask, cudaStream_t s) {
-    if (T <= 0 || T > 256) return cudaErrorInvalidValue;
-    build_mask_kernel<<<1, 256, 0, s>>>(parents, T, mask);
-    return cudaGetLastError();
+    return launch_tree_step(parents, T, mask, nullptr, nullptr, 0, 0, nullptr, nullptr, nullptr, s);
 }
 
 // ----------------------------------------------------------------------------- accept
@@ -138,129 +100,191 @@ int host_accept(const int32_t *parents, const int32_t *draft, const int32_t *tgt
     return accept_impl(parents, draft, tgt, T, root, ctx, path, path_len, bonus, acc, height);
 }
 
-// Device version: one block, thread v = node v.  Pointer jumping over the parent chains gives,
-// for every node, whether its whole root path matches (AND of the per-node match bits) and its
-// depth, in ceil(log2 T) rounds; the maximal accepted depth is a block max; the nodes on some
-// maximal accepted path are marked by walking up from the maximal endpoints; the walk from
-// the root then takes the smallest marked child at each level (lexicographically smallest).
-__global__ void __launch_bounds__(256) accept_kernel(const int32_t *parents, const int32_t *draft,
-                                                     const int32_t *tgt, int T, int root, int ctx, int32_t *path,
-                                                     int32_t *path_len, int32_t *bonus) {
-    __shared__ int32_t par[256], tg[256], anc[256], dep[256];
-    __shared__ uint8_t ok[256], good[256];
-    __shared__ int s_err, s_L, s_next;
+// Device version of both utilities: one block, thread v = node v (T <= 256), no loop over the
+// tree depth other than the ancestor walk.
+//  * Mask: thread v walks its parent chain in shared memory and collects its ancestor set (itself
+//    included) as a 256-bit mask anc(v) = row v of the tree mask (Z4).
+//  * Accept (Z12), bit-parallel: with match(u) = draft[u] == target[parent(u)] (context_argmax for
+//    a node without parent; the root always matches in root mode) as a 256-bit set M, the path of
+//    node v is P(v) = anc(v) (minus the ancestors of the root in root mode, where v must lie in
+//    the root's subtree) and v is accepted iff P(v) is inside M.  Its length is popcount P(v).
+//    Among the longest accepted paths the lexicographically smallest node sequence is the one
+//    whose lowest differing node is its own, i.e. the largest mask when bit 0 of word 0 is the
+//    most significant bit: a block-wide max over the bit-reversed masks.  The path is then the
+//    winner's set bits in ascending order (one thread per node writes its position).
+// The kernel lets the next kernel on the stream launch at once (programmatic dependent launch:
+// hta_forward's prefix pass, which reads neither the mask nor the path, overlaps its prologue);
+// a kernel that reads these outputs does so after its griddepcontrol.wait.
+__global__ void __launch_bounds__(256) tree_step_kernel(const int32_t *__restrict__ parents, int T,
+                                                        uint8_t *__restrict__ mask, const int32_t *__restrict__ draft,
+                                                        const int32_t *__restrict__ tgt, int root, int ctx,
+                                                        int32_t *path, int32_t *path_len, int32_t *bonus) {
+    __shared__ int32_t par[256], tg[256];
+    __shared__ uint32_t match_w[8], err_w[8], root_anc[8];
+    __shared__ uint32_t best_key[8][9];  // per warp: its best (depth, 8 words of bit-reversed mask)
+    __shared__ int best_node[8];
     const int v = threadIdx.x;
+    const int lane = v & 31, warp = v >> 5;
+    pdl_launch_dependents();
     const bool in = v < T;
-    if (v == 0) {
-        s_err = 0;
-        s_L = 0;
-    }
+    const bool do_acc = draft != nullptr;
+    // every input load at once (one round trip)
     int pa = -1, dr = 0;
     if (in) {
         pa = parents[v];
-        dr = draft[v];
-        tg[v] = tgt[v];
+        if (do_acc) {
+            dr = draft[v];
+            tg[v] = tgt[v];
+        }
         par[v] = pa;
     }
+    const bool bad = in && (pa < -1 || pa >= v);
     __syncthreads();
-    if (in && (pa < -1 || pa >= v)) atomicOr(&s_err, 1);
-    if (v == 0 && (root < -1 || root >= T)) atomicOr(&s_err, 1);
-    // match bit and first jump target of every node
-    int my_anc = -1, my_dep = 0;
-    uint8_t my_ok = 0;
-    if (in) {
-        my_dep = 1;
-        pa = (pa >= -1 && pa < v) ? pa : -1;  // invalid input is reported below; never index with it
-        if (root >= 0) {
-            my_ok = (v == root) ? 1 : (pa >= 0 && dr == tg[pa]);
-            my_anc = (v == root) ? -1 : pa;
-        } else {
-            my_ok = pa < 0 ? (dr == ctx) : (dr == tg[pa]);
-            my_anc = pa;
-        }
-        anc[v] = my_anc;
-        dep[v] = my_dep;
-        ok[v] = my_ok;
+    // match bit of every node (its draft token vs the target's argmax at its parent)
+    const int tgt_par = (do_acc && in && !bad) ? (pa >= 0 ? tg[pa] : ctx) : 0;
+    const bool mt = do_acc && in && !bad && (root >= 0 ? (v == root || (pa >= 0 && dr == tgt_par)) : dr == tgt_par);
+    const uint32_t mw = __ballot_sync(0xffffffffu, mt);
+    const uint32_t ew = __ballot_sync(0xffffffffu, bad);
+    if (lane == 0) {
+        match_w[warp] = mw;
+        err_w[warp] = ew;
     }
-    __syncthreads();
-    if (s_err) {
+    if (do_acc) __syncthreads();
+    uint32_t bits[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    bool ok = in && !bad;
+    if (ok) {
+        int a = v;
+        while (a >= 0) {  // parent indices strictly decrease, so this terminates
+            bits[a >> 5] |= 1u << (a & 31);
+            const int pp = par[a];
+            if (pp < -1 || pp >= a) {
+                ok = false;
+                break;
+            }
+            a = pp;
+        }
+        if (!ok)
+#pragma unroll
+            for (int w = 0; w < 8; ++w) bits[w] = 0u;
+    }
+    if (mask != nullptr && in) {
+        uint8_t *row = mask + static_cast<int64_t>(v) * T;
+        if ((T & 3) == 0) {  // rows are 4-byte aligned: store 4 mask bytes at a time
+            for (int j = 0; j < T; j += 4) {
+                const uint32_t nib = (bits[j >> 5] >> (j & 31)) & 0xFu;
+                *reinterpret_cast<uint32_t *>(row + j) =
+                    (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+            }
+        } else {
+            for (int j = 0; j < T; ++j) row[j] = static_cast<uint8_t>((bits[j >> 5] >> (j & 31)) & 1u);
+        }
+    }
+    if (!do_acc) return;
+    bool any_err = root < -1 || root >= T;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) any_err |= err_w[w] != 0u;
+    if (any_err) {
         if (v == 0) {
             *path_len = -1;
             *bonus = -1;
         }
         return;
     }
-    for (int round = 0; round < 8; ++round) {  // 2^8 = 256 >= any depth
-        int a2 = my_anc, d2 = my_dep;
-        uint8_t o2 = my_ok;
-        if (in && my_anc >= 0) {
-            o2 = my_ok & ok[my_anc];
-            d2 = my_dep + dep[my_anc];
-            a2 = anc[my_anc];
-        }
-        __syncthreads();
-        if (in) {
-            my_anc = a2;
-            my_dep = d2;
-            my_ok = o2;
-            anc[v] = a2;
-            dep[v] = d2;
-            ok[v] = o2;
-        }
-        __syncthreads();
+    if (root >= 0 && v == root) {
+#pragma unroll
+        for (int w = 0; w < 8; ++w) root_anc[w] = bits[w] & ~(w == (root >> 5) ? 1u << (root & 31) : 0u);
     }
-    // in root mode only root's subtree counts: every other chain ends at a top node with ok = 0
-    if (in && my_ok) atomicMax(&s_L, my_dep);
-    if (in) good[v] = 0;
     __syncthreads();
-    const int L = s_L;
-    if (L == 0) {  // forest mode with no accepted depth-1 node
+    // this node's path and whether it is accepted
+    bool accepted = in;
+    int depth = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        if (root >= 0) bits[w] &= ~root_anc[w];
+        accepted &= (bits[w] & ~match_w[w]) == 0u;
+        depth += __popc(bits[w]);
+    }
+    if (root >= 0) accepted &= ((bits[root >> 5] >> (root & 31)) & 1u) != 0u;
+    // key: depth, then the bit-reversed mask words (lexicographically smallest path = largest key)
+    uint32_t key[9];
+    key[0] = accepted ? static_cast<uint32_t>(depth) : 0u;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) key[w + 1] = accepted ? __brev(bits[w]) : 0u;
+    int node = accepted ? v : -1;
+    auto greater = [](const uint32_t (&a)[9], const uint32_t (&b)[9]) {
+#pragma unroll
+        for (int w = 0; w < 9; ++w)
+            if (a[w] != b[w]) return a[w] > b[w];
+        return false;
+    };
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        uint32_t other[9];
+#pragma unroll
+        for (int w = 0; w < 9; ++w) other[w] = __shfl_xor_sync(0xffffffffu, key[w], off);
+        const int on = __shfl_xor_sync(0xffffffffu, node, off);
+        if (greater(other, key)) {
+#pragma unroll
+            for (int w = 0; w < 9; ++w) key[w] = other[w];
+            node = on;
+        }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int w = 0; w < 9; ++w) best_key[warp][w] = key[w];
+        best_node[warp] = node;
+    }
+    __syncthreads();
+    // every thread reduces the (at most 8) warp winners the same way
+    uint32_t bk[9];
+    int bn = -1;
+#pragma unroll
+    for (int w = 0; w < 9; ++w) bk[w] = 0u;
+    for (int i = 0; i < (T + 31) / 32; ++i) {
+        uint32_t c[9];
+#pragma unroll
+        for (int w = 0; w < 9; ++w) c[w] = best_key[i][w];
+        if (greater(c, bk)) {
+#pragma unroll
+            for (int w = 0; w < 9; ++w) bk[w] = c[w];
+            bn = best_node[i];
+        }
+    }
+    const int L = static_cast<int>(bk[0]);
+    if (L == 0 || bn < 0) {  // forest mode with no accepted depth-1 node
         if (v == 0) {
             *path_len = 0;
             *bonus = ctx;
         }
         return;
     }
-    if (in && my_ok && my_dep == L) {  // mark the nodes of every maximal accepted path
-        int a = v;
-        while (a >= 0 && (root < 0 || a != root)) {
-            good[a] = 1;
-            a = par[a];
+    // the winner's path: its mask (bit-reversed back), one thread per member node
+    if (in && ((__brev(bk[1 + (v >> 5)]) >> (v & 31)) & 1u)) {
+        int pos = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const uint32_t m = __brev(bk[1 + w]);
+            if (w < (v >> 5)) pos += __popc(m);
+            else if (w == (v >> 5)) pos += __popc(m & ((1u << (v & 31)) - 1u));
         }
-        if (root >= 0) good[root] = 1;
-    }
-    __syncthreads();
-    int cur;
-    if (root >= 0) {
-        cur = root;
-    } else {
-        if (v == 0) s_next = 0x7fffffff;
-        __syncthreads();
-        if (in && par[v] < 0 && good[v]) atomicMin(&s_next, v);
-        __syncthreads();
-        cur = s_next;
-    }
-    if (v == 0) path[0] = cur;
-    for (int len = 1; len < L; ++len) {
-        __syncthreads();
-        if (v == 0) s_next = 0x7fffffff;
-        __syncthreads();
-        if (in && par[v] == cur && good[v]) atomicMin(&s_next, v);
-        __syncthreads();
-        cur = s_next;
-        if (v == 0) path[len] = cur;
+        path[pos] = v;
     }
     if (v == 0) {
         *path_len = L;
-        *bonus = tg[cur];
+        *bonus = tg[bn];
     }
+}
+
+cudaError_t launch_tree_step(const int32_t *parents, int T, uint8_t *mask, const int32_t *draft, const int32_t *tgt,
+                             int root, int ctx, int32_t *path, int32_t *path_len, int32_t *bonus, cudaStream_t s) {
+    if (T <= 0 || T > 256) return cudaErrorInvalidValue;
+    tree_step_kernel<<<1, 256, 0, s>>>(parents, T, mask, draft, tgt, root, ctx, path, path_len, bonus);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_accept(const int32_t *parents, const int32_t *draft, const int32_t *tgt, int T, int root, int ctx,
                           int32_t *path, int32_t *path_len, int32_t *bonus, cudaStream_t s) {
-    if (T < 1 || T > 256) return cudaErrorInvalidValue;
-    accept_kernel<<<1, 256, 0, s>>>(parents, draft, tgt, T, root, ctx, path, path_len, bonus);
-    return cudaGetLastError();
+    return launch_tree_step(parents, T, nullptr, draft, tgt, root, ctx, path, path_len, bonus, s);
 }
 
 // ----------------------------------------------------------------------------- commit

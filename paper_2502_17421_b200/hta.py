@@ -54,6 +54,7 @@ _SIG = {
     "hta_validate_tree_mask": (ctypes.c_int, [_P, ctypes.c_int32]),
     "hta_accept_greedy": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _P,
                                          ctypes.c_int32, _P]),
+    "hta_tree_step": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P, _P, ctypes.c_int32, ctypes.c_int32, _P, _P, _P, _P]),
     "hta_commit_kv": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, ctypes.c_int64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hta_comm_unique_id": (ctypes.c_int, [_P]),
     "hta_comm_create": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]),
@@ -325,6 +326,28 @@ def hta_accept_greedy(parents, draft_tokens, target_argmax, root: int = 0, conte
         return path, path_len, bonus
     n = int(path_len[0])
     return [int(x) for x in path[:n].tolist()], int(bonus[0])
+
+
+def hta_tree_step(parents, draft_tokens, target_argmax, root: int = 0, context_argmax: int = -1, mask=None,
+                  want_mask=True, path=None, path_len=None, bonus=None, stream=None):
+    """a0 + a6 in one device launch: (mask uint8 [T,T] or None, path int32 [T], path_len int32 [1],
+    bonus int32 [1]) from CUDA int32 tensors parents / draft_tokens / target_argmax [T]."""
+    given = (parents, draft_tokens, target_argmax)
+    parents = parents.to(torch.int32).contiguous()
+    draft_tokens = draft_tokens.to(torch.int32).contiguous()
+    target_argmax = target_argmax.to(torch.int32).contiguous()
+    T = parents.numel()
+    dev = parents.device
+    if want_mask and mask is None:
+        mask = torch.empty(T, T, dtype=torch.uint8, device=dev)
+    path = torch.empty(T, dtype=torch.int32, device=dev) if path is None else path
+    path_len = torch.empty(1, dtype=torch.int32, device=dev) if path_len is None else path_len
+    bonus = torch.empty(1, dtype=torch.int32, device=dev) if bonus is None else bonus
+    _check("hta_tree_step", lib().hta_tree_step(_ptr(parents), T, _ptr(mask if want_mask else None), _ptr(draft_tokens),
+                                                _ptr(target_argmax), root, context_argmax, _ptr(path), _ptr(path_len),
+                                                _ptr(bonus), _stream(stream)))
+    _hold(stream, *(t for t, g in zip((parents, draft_tokens, target_argmax), given) if t is not g))
+    return (mask if want_mask else None), path, path_len, bonus
 
 
 def hta_commit_kv(path, path_len, k_tree, v_tree, k_cache, v_cache, cache_seqlens, seqlens_out=None,

@@ -201,6 +201,33 @@ def test_device_accept_bit_exact(cuda_device):
             assert path[:n].cpu().tolist() == want_path and int(bonus.item()) == want_bonus, (seed, root)
 
 
+def test_tree_step_bit_exact(cuda_device):
+    """hta_tree_step (a0 + a6 in one launch): the mask equals the recursive-ancestor oracle and
+    the path / bonus equal the brute-force accept oracle, including invalid parent arrays and
+    every root choice on small trees (duplicate sibling tokens on odd seeds)."""
+    from workloads import accept_tokens
+    for seed in range(240):
+        T = [1, 2, 5, 8, 17, 33, 64, 128, 200, 256][seed % 10]
+        kind = ["random", "random_forest", "beam", "chain", "star", "heap_binary"][seed % 6]
+        par = tree_parents(kind, T, seed=seed)
+        draft, tgt, ctx = accept_tokens(par, seed, vocab=3, p_match=0.85, distinct_siblings=(seed % 2 == 0))
+        roots = (-1,) if kind == "random_forest" else ((0, -1) + ((T // 2,) if T > 2 else ()))
+        for root in roots:
+            m, path, plen, bonus = hta.hta_tree_step(par.to(cuda_device), draft.to(cuda_device), tgt.to(cuda_device),
+                                                     root=root, context_argmax=ctx)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(m.cpu().numpy(), oracle.tree_mask(par))
+            want_path, want_bonus = oracle.accept_greedy(par, draft, tgt, root=root, context_argmax=ctx)
+            n = int(plen.item())
+            assert path[:n].cpu().tolist() == want_path and int(bonus.item()) == want_bonus, (seed, root)
+    # invalid parents: path_len = -1, the offending row is all zero
+    bad = torch.tensor([-1, 0, 5, 1], dtype=torch.int32)
+    d0 = torch.zeros(4, dtype=torch.int32)
+    m, path, plen, bonus = hta.hta_tree_step(bad.to(cuda_device), d0.to(cuda_device), d0.to(cuda_device), root=0)
+    torch.cuda.synchronize()
+    assert int(plen.item()) == -1 and int(m[2].sum().item()) == 0 and int(m[3].sum().item()) == 3
+
+
 def test_deterministic(cuda_device):
     w = make_workload(1, 64, 32, 8, 128, 5000, "bf16", dist="V1", seed=15, tree="beam")
     mask = torch.from_numpy(oracle_masks(w)).to(cuda_device)

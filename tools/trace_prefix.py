@@ -35,10 +35,18 @@ def main():
     w = config_workload(name, seed=0)
     x = [t.to(dev) for t in (w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree)]
     mask = hta.hta_build_tree_mask(w.parents[0].to(dev))
+    fwd = lambda: hta.hta_forward(*x, mask)  # noqa: E731
+    if os.environ.get("PAGED"):  # the paged forward over in-order 16-key pages
+        page = 16
+        maxp = w.N // page
+        kp = x[1].reshape(w.B * maxp, page, w.H_kv, w.d).contiguous()
+        vp = x[2].reshape(w.B * maxp, page, w.H_kv, w.d).contiguous()
+        bt = torch.arange(w.B * maxp, dtype=torch.int32, device=dev).view(w.B, maxp)
+        fwd = lambda: hta.hta_forward_paged(x[0], kp, vp, bt, x[3], x[4], mask)  # noqa: E731
     L = hta.lib()
     L.hta_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
     buf = torch.zeros(32 * RECS, dtype=torch.int64, device=dev)
-    hta.hta_forward(*x, mask)
+    fwd()
     torch.cuda.synchronize()
     assert L.hta_debug_set_trace(ctypes.c_void_p(buf.data_ptr()), cta) == 0
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -46,7 +54,7 @@ def main():
         buf.zero_()
         flush.zero_()
         flush.view(torch.float32).sum()
-        hta.hta_forward(*x, mask)
+        fwd()
         torch.cuda.synchronize()
     L.hta_debug_set_trace(None, -1)
     raw = buf.cpu().view(32, RECS).tolist()
@@ -139,6 +147,15 @@ def main():
             print(f"{j:4d}: {min(r10)} | {min(r14)}..{max(r14)} (+{max(r14) - min(r10)}) | "
                   f"{rel(pv) if pv else '-'} (+{rel(pv) - max(r14) if pv else 0}) | {rel(s3) if s3 else '-'} | "
                   f"{min(r3) if r3 else '-'} (+{min(r3) - rel(s3) if r3 and s3 else 0})")
+    # producers: issue -> landed latency (V landed = event 3 of the MMA warp, K landed = event 2)
+    kw = next((w for w in range(32) if (w, 30) in ev), None)
+    vw = next((w for w in range(32) if (w, 31) in ev), None)
+    if kw is not None and vw is not None:
+        kl = [mma[2][j] - ev[(kw, 30)][j] for j in tiles if j in mma[2] and j in ev[(kw, 30)]]
+        vl = [mma[3][j] - ev[(vw, 31)][j] for j in tiles if j in mma[3] and j in ev[(vw, 31)]]
+        vlead = [mma[1][j] - ev[(vw, 31)][j] for j in tiles if j in ev[(vw, 31)]]
+        print(f"producers: K issue->landed(+S issue) median {statistics.median(kl):.0f}, V issue->landed median "
+              f"{statistics.median(vl):.0f}, V issue -> PV_j issue median {statistics.median(vlead):.0f}")
     # per warp: median lag of its publish behind the first warp of its group
     lags = defaultdict(list)
     for j in range(2, len(tiles) - 2):
