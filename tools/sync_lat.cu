@@ -6,7 +6,7 @@
 
 #include <cstdio>
 
-#include "../paper_2502_17421_b200/csrc/ptx_sm100.cuh"
+#include "ptx_extra.cuh"
 
 using namespace hta;
 
