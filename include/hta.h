@@ -78,7 +78,10 @@ typedef struct {
     int64_t tkv_strides[3]; /* [B, T, H_kv] of k_tree, v_tree; default {T*H_kv*d, H_kv*d, d} */
     int32_t num_splits;   /* KV splits of the prefix pass per (b, kv-head, row tile);
                              0 = chosen by the library from the SM count                    */
-    int32_t reserved;     /* must be 0                                                      */
+    int32_t max_seqlen;   /* optional upper bound on cache_seqlens (0 = N_max), used only to
+                             plan the split-KV schedule when the cache capacity is much larger
+                             than the filled length; a batch entry longer than the bound is
+                             still computed exactly (the last split runs to its length)     */
 } hta_shape_t;
 
 /* Human-readable name of a status (static string, never NULL). */
@@ -223,11 +226,13 @@ hta_status_t hta_tree_step(const int32_t *parents, int32_t T, uint8_t *mask,
  *   path_len     device int32 [B]: accepted nodes of batch b (<= 0: nothing to commit)
  *   k_tree, v_tree  [B, T, H_kv, d] (read);  k_cache, v_cache [B, N_max, H_kv, d] (written at
  *                rows cache_seqlens[b] ... cache_seqlens[b] + path_len[b] - 1 only)
- *   cache_seqlens   device int32 [B]: committed length n_b before the call (read)
+ *   cache_seqlens   device int32 [B]: committed length n_b before the call (read; a negative
+ *                value counts as 0)
  *   seqlens_out     device int32 [B]: n_b + the rows written (may be cache_seqlens itself: the
  *                update is made after the copies).  Rows that would land at or beyond N_max, and
  *                everything from the first node index outside [0, T) on, are not written and not
  *                counted (reading Z18).
+ * k_tree / v_tree must not overlap the cache rows being written (the copies run in parallel).
  * Enqueued on `stream`; one CTA per batch entry.  Host-checkable errors as for hta_forward. */
 hta_status_t hta_commit_kv(const hta_shape_t *shape, const int32_t *path, int64_t path_stride,
                            const int32_t *path_len, const void *k_tree, const void *v_tree,

@@ -32,7 +32,7 @@ hta_status_t check_shape(const hta_shape_t *in, Shape *out) {
     if (s.N_max < 0 || s.N_max > (int64_t(1) << 31) - 1024) return HTA_ERR_INVALID_ARGUMENT;
     if (!(s.softmax_scale > 0.f) || !std::isfinite(s.softmax_scale)) return HTA_ERR_INVALID_ARGUMENT;
     if (s.dtype != HTA_BF16 && s.dtype != HTA_FP32) return HTA_ERR_INVALID_ARGUMENT;
-    if (s.num_splits < 0 || s.reserved != 0) return HTA_ERR_INVALID_ARGUMENT;
+    if (s.num_splits < 0 || s.max_seqlen < 0) return HTA_ERR_INVALID_ARGUMENT;
     if (s.d != 64 && s.d != 128) return HTA_ERR_UNSUPPORTED;
     const int64_t d = s.d;
     auto fill = [](int64_t *st, int64_t a, int64_t b, int64_t c) {
@@ -111,7 +111,10 @@ PrefixPlan make_plan(const Shape &sh, int num_sms) {
     pl.G = sh.G;
     pl.M = s.T * sh.G;
     const int blk = s.dtype == HTA_BF16 ? kBlockN : kSimtBlock;
-    pl.n_tiles = static_cast<int>((s.N_max + blk - 1) / blk);
+    // the filled length bound (max_seqlen) plans the schedule; the last split still runs to each
+    // batch entry's own length
+    const int64_t n_plan = (s.max_seqlen > 0 && s.max_seqlen < s.N_max) ? s.max_seqlen : s.N_max;
+    pl.n_tiles = static_cast<int>((n_plan + blk - 1) / blk);
     int S = 1;
     if (s.dtype == HTA_BF16) {
         // More than 128 rows per KV head: CTA pairs (cta_group::2, 256 rows per pair), unless

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(128) prefix_simt_kernel(const PrefixParams p) 
     }
     const int64_t lo = static_cast<int64_t>(split) * p.tiles_per_split * kSimtBlock;
     int64_t hi = lo + static_cast<int64_t>(p.tiles_per_split) * kSimtBlock;
-    if (hi > n_b) hi = n_b;
+    if (hi > n_b || split == p.splits - 1) hi = n_b;  // the last split runs to the length
 
     const float *q = static_cast<const float *>(p.q) + b * p.qs0 + t * p.qs1 + h * p.qs2 + lane * E;
     const float *K = static_cast<const float *>(p.k) + b * p.ks0 + g * p.ks2 + lane * E;

@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     }
     const int64_t key_lo = static_cast<int64_t>(split) * p.tiles_per_split * kBlockN;
     int64_t key_hi = key_lo + static_cast<int64_t>(p.tiles_per_split) * kBlockN;
-    if (key_hi > n_b) key_hi = n_b;
+    if (key_hi > n_b || split == p.splits - 1) key_hi = n_b;  // the last split runs to the length
     const int n_tiles = key_hi > key_lo ? static_cast<int>((key_hi - key_lo + kBlockN - 1) / kBlockN) : 0;
     const int row0 = mg * kRowsPerTile * (PAIR ? 2 : 1) + static_cast<int>(rank) * kRowsPerTile;
     // the last tile of a split that ends at the sequence end may hold garbage rows (Z13)

@@ -303,7 +303,8 @@ __global__ void __launch_bounds__(256) commit_kv_kernel(const int32_t *__restric
     // every load at once (one round trip): the path entries, the committed length, the path length
     if (threadIdx.x < gm.T) s_node[threadIdx.x] = path[b * path_stride + threadIdx.x];
     if (threadIdx.x == 0) {
-        s_n = seqlens[b];
+        const int32_t n0 = seqlens[b];
+        s_n = n0 < 0 ? 0 : n0;  // a negative committed length counts as empty
         s_rows = path_len[b];
     }
     __syncthreads();

@@ -31,7 +31,7 @@ class hta_shape_t(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int32), ("T", ctypes.c_int32), ("H", ctypes.c_int32), ("H_kv", ctypes.c_int32),
                 ("d", ctypes.c_int32), ("N_max", ctypes.c_int64), ("softmax_scale", ctypes.c_float),
                 ("dtype", ctypes.c_int32), ("q_strides", ctypes.c_int64 * 3), ("kv_strides", ctypes.c_int64 * 3),
-                ("tkv_strides", ctypes.c_int64 * 3), ("num_splits", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("tkv_strides", ctypes.c_int64 * 3), ("num_splits", ctypes.c_int32), ("max_seqlen", ctypes.c_int32)]
 
 
 _lib = None
@@ -116,7 +116,7 @@ def _strides3(t: torch.Tensor):
 
 def make_shape(q: torch.Tensor, k_cache: Optional[torch.Tensor] = None, k_tree: Optional[torch.Tensor] = None,
                H_kv: Optional[int] = None, N_max: Optional[int] = None, scale: Optional[float] = None,
-               num_splits: int = 0) -> hta_shape_t:
+               num_splits: int = 0, max_seqlen: int = 0) -> hta_shape_t:
     """hta_shape_t from q [B,T,H,d], k_cache [B,N,H_kv,d], k_tree [B,T,H_kv,d] (strides included)."""
     B, T, H, d = q.shape
     s = hta_shape_t()
@@ -134,6 +134,7 @@ def make_shape(q: torch.Tensor, k_cache: Optional[torch.Tensor] = None, k_tree: 
     s.dtype = _dtype_code(q.dtype)
     s.q_strides = _strides3(q)
     s.num_splits = num_splits
+    s.max_seqlen = max_seqlen
     return s
 
 
@@ -181,9 +182,9 @@ def _out_like_q(q: torch.Tensor, o: Optional[torch.Tensor]) -> torch.Tensor:
 # --------------------------------------------------------------------------- attention
 
 def hta_prefix_attn(q, k_cache, v_cache, cache_seqlens=None, o_part=None, lse_part=None, ws=None,
-                    scale=None, num_splits=0, stream=None) -> Tuple[torch.Tensor, torch.Tensor]:
+                    scale=None, num_splits=0, max_seqlen=0, stream=None) -> Tuple[torch.Tensor, torch.Tensor]:
     """Unmasked prefix pass: fp32 O [B,T,H,d] and natural-log LSE [B,H,T]."""
-    shape = make_shape(q, k_cache=k_cache, scale=scale, num_splits=num_splits)
+    shape = make_shape(q, k_cache=k_cache, scale=scale, num_splits=num_splits, max_seqlen=max_seqlen)
     B, T, H, d = q.shape
     if o_part is None:
         o_part = torch.empty(B, T, H, d, dtype=torch.float32, device=q.device)
@@ -230,12 +231,12 @@ def hta_merge_lse(o_parts, lse_parts, dtype=torch.bfloat16, o=None, lse_out=None
 
 
 def hta_forward(q, k_cache, v_cache, k_tree, v_tree, mask, cache_seqlens=None, o=None, lse_out=None, ws=None,
-                want_lse=True, scale=None, num_splits=0, stream=None,
+                want_lse=True, scale=None, num_splits=0, max_seqlen=0, stream=None,
                 events=None) -> Tuple[torch.Tensor, Optional[torch.Tensor]]:
     """Full Hybrid Tree Attention of one layer: O [B,T,H,d] in q.dtype (+ LSE [B,H,T]).
     `events` = (begin, end) torch.cuda.Event pair recorded around the prefix kernel
     (hta_forward_timed)."""
-    shape = make_shape(q, k_cache=k_cache, k_tree=k_tree, scale=scale, num_splits=num_splits)
+    shape = make_shape(q, k_cache=k_cache, k_tree=k_tree, scale=scale, num_splits=num_splits, max_seqlen=max_seqlen)
     B, T, H, d = q.shape
     mbs = 0 if mask.dim() == 2 else mask.stride(0)
     o = _out_like_q(q, o)
@@ -257,13 +258,14 @@ def hta_forward(q, k_cache, v_cache, k_tree, v_tree, mask, cache_seqlens=None, o
 
 
 def hta_forward_paged(q, k_pool, v_pool, block_table, k_tree, v_tree, mask, cache_seqlens=None, o=None,
-                      lse_out=None, ws=None, want_lse=True, scale=None, num_splits=0, stream=None):
+                      lse_out=None, ws=None, want_lse=True, scale=None, num_splits=0, max_seqlen=0, stream=None):
     """hta_forward over a paged cache: k_pool/v_pool [num_pages, page_size, H_kv, d] bf16,
     block_table int32 [B, max_pages] (device)."""
     num_pages, page_size, Hkv, d = k_pool.shape
     B, T, H, _ = q.shape
     max_pages = block_table.shape[1]
-    shape = make_shape(q, k_tree=k_tree, H_kv=Hkv, N_max=max_pages * page_size, scale=scale, num_splits=num_splits)
+    shape = make_shape(q, k_tree=k_tree, H_kv=Hkv, N_max=max_pages * page_size, scale=scale, num_splits=num_splits,
+                       max_seqlen=max_seqlen)
     shape.N_max = max_pages * page_size
     mbs = 0 if mask.dim() == 2 else mask.stride(0)
     o = _out_like_q(q, o)

@@ -69,3 +69,24 @@ def test_commit_after_device_accept(cuda_device):
     assert out.cpu().tolist() == n_ref.tolist() and len(path_h) >= 2
     assert np.array_equal(kc.float().cpu().numpy(), k_ref)
     assert np.array_equal(vc.float().cpu().numpy(), v_ref)
+
+
+def test_commit_negative_seqlen_counts_as_empty(cuda_device):
+    """A negative committed length is clamped to 0 (no write before row 0): the rows land at
+    0..len-1, like the oracle's commit onto an empty cache."""
+    B, T, H, Hkv, d, N = 2, 8, 4, 2, 64, 64
+    w = make_workload(B, T, H, Hkv, d, N, "bf16", dist="V0", seed=6, tree="chain")
+    paths = np.tile(np.arange(T, dtype=np.int32), (B, 1))
+    lens = np.array([3, 5], np.int32)
+    n0 = np.array([-7, 10], np.int32)
+    k_ref, v_ref, n_ref = oracle.commit_kv(w.k_cache.float().numpy(), w.v_cache.float().numpy(),
+                                           np.maximum(n0, 0), w.k_tree.float().numpy(), w.v_tree.float().numpy(),
+                                           paths, lens)
+    dev = cuda_device
+    kc, vc = w.k_cache.to(dev), w.v_cache.to(dev)
+    out = hta.hta_commit_kv(torch.from_numpy(paths).to(dev), torch.from_numpy(lens).to(dev), w.k_tree.to(dev),
+                            w.v_tree.to(dev), kc, vc, torch.from_numpy(n0).to(dev))
+    torch.cuda.synchronize()
+    assert out.cpu().tolist() == n_ref.tolist() == [3, 15]
+    assert np.array_equal(kc.float().cpu().numpy(), k_ref)
+    assert np.array_equal(vc.float().cpu().numpy(), v_ref)

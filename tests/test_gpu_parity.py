@@ -343,3 +343,20 @@ def test_tree_logit_far_above_prefix(cuda_device, dtype):
     o, l = hta.hta_forward(*x, torch.from_numpy(mask).to(cuda_device))
     torch.cuda.synchronize()
     compare(o, l, o_ref, l_ref, dtype, "forward")
+
+
+def test_max_seqlen_hint_plans_by_filled_length(cuda_device):
+    """A preallocated cache much longer than its filled length: hta_shape_t.max_seqlen plans the
+    split-KV schedule over the filled length; the result is exact whether the bound holds (1200
+    >= every length) or is violated (600 < 1000: the last split runs to each entry's length)."""
+    sl = torch.tensor([1000, 37], dtype=torch.int32)
+    w = make_workload(2, 16, 8, 2, 128, 16384, "bf16", dist="V1", seed=21, tree="beam", seqlens=sl,
+                      garbage_tail=True)
+    mask = oracle_masks(w)
+    x = to_dev(w, cuda_device)
+    o_ref, l_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask, seqlens=w.seqlens)
+    for hint in (1200, 600, 0):
+        o, l = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], torch.from_numpy(mask).to(cuda_device),
+                               cache_seqlens=x["sl"], max_seqlen=hint)
+        torch.cuda.synchronize()
+        compare(o, l, o_ref, l_ref, "bf16", f"max_seqlen={hint}")

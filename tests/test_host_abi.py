@@ -76,7 +76,7 @@ def test_workspace_size_matches_split_plan(L):
 
 @pytest.mark.parametrize("field,value", [("T", 0), ("T", 257), ("H", 30), ("d", 96), ("N_max", -1),
                                          ("softmax_scale", 0.0), ("softmax_scale", float("nan")),
-                                         ("reserved", 1), ("num_splits", -2), ("dtype", 7)])
+                                         ("max_seqlen", -1), ("num_splits", -2), ("dtype", 7)])
 def test_invalid_shapes_rejected_on_host(L, field, value):
     s = _shape()
     setattr(s, field, value)
@@ -201,3 +201,16 @@ def test_seqpar_workspace_layout(L):
         want = r16(L.hta_workspace_size(ctypes.byref(s), 148)) + 2 * r16(P * blk) + r16(o_sl) + r16(l_sl) + \
             r16(P * o_sl) + r16(P * l_sl)
         assert L.hta_workspace_size_seqpar(ctypes.byref(s), 148, P) == want
+
+
+def test_max_seqlen_hint_shrinks_the_plan(L):
+    """With a 128k-capacity cache filled to 8k, the hint plans 8k keys: fewer tiles, so the split
+    count (and workspace) is that of an 8k cache, not of the capacity."""
+    part = lambda s: (s.B * s.T * s.H * s.d + s.B * s.H * s.T) * 4
+    full = _shape(N=131072)
+    hinted = _shape(N=131072)
+    hinted.max_seqlen = 8192
+    small = _shape(N=8192)
+    assert L.hta_workspace_size(ctypes.byref(hinted), 148) == L.hta_workspace_size(ctypes.byref(small), 148)
+    assert L.hta_workspace_size(ctypes.byref(full), 148) >= L.hta_workspace_size(ctypes.byref(hinted), 148)
+    assert L.hta_workspace_size(ctypes.byref(hinted), 148) % part(hinted) == 0
