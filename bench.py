@@ -32,6 +32,18 @@ from workloads import CONFIGS, accept_tokens  # noqa: E402
 from workloads.generators import config_workload  # noqa: E402
 
 DEFAULT_WORKLOAD = "llama8b_64k"   # BASELINE.json configs[2]: "1/2/4/8 x B200"
+DATASHEET = {"hbm_gbs": 8000.0, "bf16_tflops": 2250.0}  # roof_DS, context only
+
+
+def pct(xs, q):
+    """q-quantile (0..1) of a list by nearest rank."""
+    ys = sorted(xs)
+    return ys[min(len(ys) - 1, max(0, int(round(q * (len(ys) - 1)))))]
+
+
+def dist_us(ms_list):
+    us = [x * 1e3 for x in ms_list]
+    return {"median": statistics.median(us), "p10": pct(us, 0.1), "p90": pct(us, 0.9), "mean": statistics.mean(us)}
 METRIC = "verification_attention_tokens_per_s"
 L2_FLUSH_BYTES = 512 << 20
 
@@ -140,11 +152,11 @@ def created_events(n):
 
 # ----------------------------------------------------------------------------- oracle timing
 
-def time_oracle(w, mask_np, budget_s=12.0):
+def time_oracle(w, mask_np, budget_s=12.0, threads=None):
     """The fp64 oracle as it stands, on a bounded sample of rows of the same workload; returns
     (tokens/s extrapolated to the whole step, seconds, rows, cores)."""
     import oracle
-    cores = len(os.sched_getaffinity(0))
+    cores = threads or len(os.sched_getaffinity(0))
     rows_all = [(b, t, h) for b in range(w.B) for t in range(w.T) for h in range(w.H)]
     R = min(len(rows_all), max(cores, 8))
     t0 = time.perf_counter()
@@ -192,7 +204,8 @@ def run_reference(args, cfg, ws, rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.workload, **{k: cfg[k] for k in ("B", "T", "H", "H_kv", "d", "N")}},
             "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{n} of {tot} query rows per step, extrapolated linearly"},
+                             "sample": f"{n} of {tot} query rows per step ({dt:.1f} s measured per step), "
+                                       "extrapolated linearly"},
             "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -353,11 +366,20 @@ def main():
             pev = [(ev[2 * i], ev[2 * i + 1]) for i in range(args.steps)]
             # (a0 and the forked a6 are left out of this pass: nothing runs beside or just before
             # the timed kernel; the mask is the one the step built)
-            timed(lambda i: hta.hta_forward(d_in["q"], kc, vc, d_in["kt"], d_in["vt"], mask, cache_seqlens=sl, o=o,
-                                            lse_out=lse, ws=wsb, events=pev[i]), args.steps)
-            prefix_ms = statistics.mean(a.elapsed_time(b) for a, b in pev)
+            tev = created_events(args.steps)
+
+            def fwd_timed(i):
+                hta.hta_forward(d_in["q"], kc, vc, d_in["kt"], d_in["vt"], mask, cache_seqlens=sl, o=o, lse_out=lse,
+                                ws=wsb, events=pev[i])
+                tev[i].record()  # after the tree/merge kernel (launched without PDL in this mode)
+
+            timed(fwd_timed, args.steps)
+            prefix_all = [a.elapsed_time(b) for a, b in pev]
+            prefix_ms = statistics.mean(prefix_all)
+            tm_ms = statistics.mean(pev[i][1].elapsed_time(tev[i]) for i in range(args.steps))
         else:
-            prefix_ms = None
+            prefix_ms = tm_ms = None
+            prefix_all = []
         # (3) end to end through the public API: per-step inputs H2D from pinned host memory,
         # result (O + accepted path) D2H; the KV cache is resident model state.
         e2e_times = timed(lambda i: run_e2e(), args.steps)
@@ -397,7 +419,12 @@ def main():
                      "roofline_us": max(t_mem, t_tc) * 1e6, "frac_of_max_roof": max(t_mem, t_tc) / t_s,
                      "alg_bytes": alg_bytes, "alg_flops": alg_flops,
                      "hbm_gbs_achieved": alg_bytes / t_s / 1e9, "tflops_achieved": alg_flops / t_s / 1e12,
-                     "peaks": pk["source"] + " MEASURED_PEAKS.json (burst)"})
+                     "peaks": pk["source"] + " MEASURED_PEAKS.json (burst)",
+                     "kernel_us_dist": dist_us(prefix_all),
+                     "roof_ds_us": max(alg_bytes / (DATASHEET["hbm_gbs"] * 1e9),
+                                       alg_flops / (DATASHEET["bf16_tflops"] * 1e12)) * 1e6,
+                     "frac_ds": max(alg_bytes / (DATASHEET["hbm_gbs"] * 1e9),
+                                    alg_flops / (DATASHEET["bf16_tflops"] * 1e12)) / t_s})
         prof = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
         if os.path.exists(prof):
             try:
@@ -412,15 +439,22 @@ def main():
         "warmup": args.warmup, "ms_per_step": t_ms, "us_per_step": t_ms * 1e3, "higher_is_better": True,
         "scaling": "strong" if ws > 1 else "strong", "vs_baseline": None, "dtype": cfg["dtype"],
         "data": "synthetic (seeded; value distribution V1 sink+local; beam-search tree)",
-        "config": {"workload": args.workload, "B": w.B, "T": T, "H": w.H, "H_kv": w.H_kv, "d": w.d, "N": w.N,
-                   "parallelism": f"seq{ws}",
-                   "l2": "flushed before every timed step (512 MiB write, then two reads of it; untimed)",
-                   "step": ("a0 mask + hta_forward (a1-a4) | accept (a6) on a forked stream"
-                            + (" + NCCL exchange (a5)" if seqpar else "; CUDA graph replay"))},
+        # the same config dict as the --impl reference arm
+        "config": {"workload": args.workload, **{k: cfg[k] for k in ("B", "T", "H", "H_kv", "d", "N")}},
+        "setup": {"parallelism": f"seq{ws}",
+                  "l2": "flushed before every timed step (512 MiB write, then two reads of it; untimed)",
+                  "step": ("a0 mask + hta_forward (a1-a4) | accept (a6) on a forked stream"
+                           + (" + NCCL exchange (a5)" if seqpar else "; CUDA graph replay"))},
+        "t_us": dist_us(times),
+        "kernel_us": {"prefix": None if prefix_ms is None else prefix_ms * 1e3,
+                      "tree_merge": None if tm_ms is None else tm_ms * 1e3,
+                      "note": "prefix: CUDA events around its launch; tree_merge: from the prefix's end event to "
+                              "an event after the tree/merge kernel, launched without programmatic overlap in "
+                              "this timing pass (so it includes its launch gap)"},
         "clocks": clocks,
         "gpu_launches": launches_per_step * args.steps,
         "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "t_us": dist_us(e2e_times),
                 "note": ("per-step inputs (q, tree K/V, parents, draft/target tokens) H2D as one copy from a pinned "
                          "staging buffer, O + accepted path D2H as one copy; KV cache resident; CUDA graph")},
         "roofline": roof,
@@ -520,8 +554,11 @@ def main():
         import oracle
         mask_np = np.stack([oracle.tree_mask(w.parents[b]) for b in range(w.B)])
         tps, dt, n, tot, cores = time_oracle(w, mask_np)
+        tps1, dt1, n1, _, _ = time_oracle(w, mask_np, budget_s=4.0, threads=1)
         line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                                "sample": f"{n} of {tot} query rows ({dt:.1f} s), extrapolated linearly"}
+                                "sample": f"{n} of {tot} query rows ({dt:.1f} s), extrapolated linearly",
+                                "one_thread": {"value": tps1, "unit": "tokens/s", "t_s_per_step": w.B * w.T / tps1,
+                                               "sample": f"{n1} of {tot} query rows ({dt1:.1f} s), one thread"}}
 
     # ---- the other BASELINE configs (N = 1): µs/step, device-resident, L2 flushed
     if rank == 0 and not seqpar and not args.no_all_configs:
