@@ -171,6 +171,32 @@ hta_status_t hta_forward_paged(const hta_shape_t *shape, const void *q, const vo
                                const uint8_t *mask, int64_t mask_batch_stride, void *o,
                                float *lse_out, void *ws, size_t ws_bytes, hta_stream_t stream);
 
+/* hybrid_tree_attention over an FP8 (E4M3) KV cache (beyond the paper, which
+ * runs fp16 only): as hta_forward with
+ *   k_cache, v_cache  E4M3 bytes [B, N_max, H_kv, d] (kv_strides in ELEMENTS = bytes, multiples of
+ *                     16; 16-byte aligned rows), holding K8, V8 with
+ *                     K = k_scale[g] * K8,  V = v_scale[g] * V8  for KV head g
+ *   k_scale, v_scale  device float32 [H_kv]
+ *   q, k_tree, v_tree, o   bf16 (shape->dtype must be HTA_BF16; d 64 or 128)
+ * The E4M3 tiles are widened to f16 in shared memory (exact) and q is converted to f16 (exact in
+ * the f16 range), so the prefix contraction runs on the tensor cores in f16 with fp32
+ * accumulation and P rounded to f16; the HBM traffic of the cache is halved.  The result matches
+ * hybrid tree attention over the decoded cache within the bf16 tolerances (DESIGN.md "FP8 KV
+ * cache").  Workspace and errors as hta_forward; HTA_ERR_UNSUPPORTED for dtype fp32. */
+hta_status_t hta_forward_fp8kv(const hta_shape_t *shape, const void *q, const void *k_cache,
+                               const void *v_cache, const float *k_scale, const float *v_scale,
+                               const int32_t *cache_seqlens, const void *k_tree,
+                               const void *v_tree, const uint8_t *mask,
+                               int64_t mask_batch_stride, void *o, float *lse_out, void *ws,
+                               size_t ws_bytes, hta_stream_t stream);
+
+/* The prefix pass alone over an FP8 cache (as hta_prefix_attn; arguments as hta_forward_fp8kv). */
+hta_status_t hta_prefix_attn_fp8kv(const hta_shape_t *shape, const void *q, const void *k_cache,
+                                   const void *v_cache, const float *k_scale,
+                                   const float *v_scale, const int32_t *cache_seqlens,
+                                   float *o_part, float *lse_part, void *ws, size_t ws_bytes,
+                                   hta_stream_t stream);
+
 /* Tree mask from a parent array ("attention masks derived from prefix trees"; reading
  * Z4: mask[i][j] = 1 iff j == i or j is an ancestor of i).
  *   parents  int32 [T], parents[i] in [-1, i) (-1 = child of the committed context; reading Z6)

@@ -11,8 +11,10 @@ Contents
   tree_mask(...)     ancestor mask by recursive set walk (oracle/tree.py).
   accept_greedy(...) longest accepted root path by brute-force enumeration (oracle/tree.py).
   commit_kv(...)     append the accepted nodes' K/V rows to the cache in path order (oracle/tree.py).
+  attention_fp8kv(...) attention over an FP8 (E4M3) cache decoded from its definition (oracle/fp8.py).
 
 Parity status of each function is recorded in DESIGN.md "Oracle pins".
 """
 from .attention import attention, merge, load_library, build_library  # noqa: F401
 from .tree import tree_mask, accept_greedy, commit_kv  # noqa: F401
+from .fp8 import attention_fp8kv, decode_e4m3, e4m3_value  # noqa: F401

@@ -240,12 +240,39 @@ hta_status_t make_pool_map(CUtensorMap *map, const void *base, const hta_shape_t
     return r == CUDA_SUCCESS ? HTA_OK : HTA_ERR_INVALID_ARGUMENT;
 }
 
+// FP8 (E4M3) cache [B, N, H_kv, d] as bytes: box = box_cols x 1 x box_rows x 1, no swizzle (the
+// kernel widens the landed tile into the 128B-swizzled f16 layout itself).
+hta_status_t make_kv_map_fp8(CUtensorMap *map, const void *base, const hta_shape_t &s, int box_cols, int box_rows) {
+    EncodeTiledFn enc = encode_fn();
+    if (enc == nullptr) return HTA_ERR_CUDA;
+    cuuint64_t dims[4] = {cuuint64_t(s.d), cuuint64_t(s.H_kv), cuuint64_t(std::max<int64_t>(s.N_max, 1)),
+                          cuuint64_t(s.B)};
+    cuuint64_t strides[3] = {cuuint64_t(s.kv_strides[2]), cuuint64_t(s.kv_strides[1]), cuuint64_t(s.kv_strides[0])};
+    cuuint32_t box[4] = {cuuint32_t(box_cols), 1, cuuint32_t(box_rows), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? HTA_OK : HTA_ERR_INVALID_ARGUMENT;
+}
+
+// FP8 cache arguments of the prefix pass (nullptr: the cache has the shape's dtype).
+struct Fp8Args {
+    const float *k_scale, *v_scale;
+};
+
 // Enqueue the prefix pass writing `splits` partials at (o_out, lse_out) with the given strides.
 hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, const void *k, const void *v,
                         const int32_t *seqlens, float *o_out, float *lse_out, int64_t o_split_stride,
-                        int64_t lse_split_stride, cudaStream_t st, const PagedArgs *pg = nullptr) {
+                        int64_t lse_split_stride, cudaStream_t st, const PagedArgs *pg = nullptr,
+                        const Fp8Args *f8 = nullptr) {
     const hta_shape_t &s = sh.s;
     PrefixParams p{};
+    if (f8 != nullptr) {
+        p.kv8 = 1;
+        p.k_scale = f8->k_scale;
+        p.v_scale = f8->v_scale;
+    }
     if (pg != nullptr) {
         p.block_table = pg->block_table;
         p.bt_stride = pg->max_pages;
@@ -284,21 +311,23 @@ hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, co
     if (s.dtype == HTA_BF16) {
         CUtensorMap tk, tv;
         hta_status_t r;
-        if (pg != nullptr) {
+        if (f8 != nullptr) {
+            // a CTA of a pair loads half of each K tile (64 keys, all d) and half of each V tile
+            // (64 columns, all 128 keys) -- the same halves as the bf16 cache
+            if ((r = make_kv_map_fp8(&tk, k, s, s.d, pl.nt == 2 ? kBlockN / 2 : kBlockN)) != HTA_OK) return r;
+            if ((r = make_kv_map_fp8(&tv, v, s, pl.nt == 2 ? 64 : s.d, kBlockN)) != HTA_OK) return r;
+        } else if (pg != nullptr) {
             if ((r = make_pool_map(&tk, k, s, *pg)) != HTA_OK) return r;
             if ((r = make_pool_map(&tv, v, s, *pg)) != HTA_OK) return r;
         } else {
-            // a CTA of a pair loads half of each K tile (96 keys) and half of each V tile (64 columns)
-#ifdef HTA_Q2
-            if ((r = make_kv_map(&tk, k, s, kBlockN)) != HTA_OK) return r;
-#else
+            // a CTA of a pair loads half of each K tile (64 keys) and half of each V tile (64 columns)
             if ((r = make_kv_map(&tk, k, s, pl.nt == 2 ? kBlockN / 2 : kBlockN)) != HTA_OK) return r;
-#endif
             if ((r = make_kv_map(&tv, v, s, kBlockN)) != HTA_OK) return r;
         }
         CUtensorMap tq;
         std::memset(&tq, 0, sizeof(tq));
-        p.q_tma = make_q_map(&tq, q, s, sh.G) ? 1 : 0;
+        // the FP8 variant stages Q with plain loads (converting it to f16 on the way)
+        p.q_tma = f8 == nullptr && make_q_map(&tq, q, s, sh.G) ? 1 : 0;
         e = launch_prefix_tc(p, tq, tk, tv, prefix_tc_smem_bytes(s.d, pl.nt), st);
     } else {
         e = launch_prefix_simt(p, st);
@@ -452,7 +481,8 @@ hta_status_t hta_merge_lse(const hta_shape_t *shape, int32_t n_parts, const floa
 static hta_status_t forward_impl(const PagedArgs *pg, const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,
                                const int32_t *cache_seqlens, const void *k_tree, const void *v_tree,
                                const uint8_t *mask, int64_t mask_batch_stride, void *o, float *lse_out, void *ws,
-                               size_t ws_bytes, hta_stream_t stream, void *ev_begin, void *ev_end) {
+                               size_t ws_bytes, hta_stream_t stream, void *ev_begin, void *ev_end,
+                               const Fp8Args *f8 = nullptr) {
     Shape sh;
     hta_status_t r = check_shape(shape, &sh);
     if (r != HTA_OK) return r;
@@ -473,7 +503,7 @@ static hta_status_t forward_impl(const PagedArgs *pg, const hta_shape_t *shape, 
     const int64_t lstride = int64_t(s.B) * s.H * s.T;
     if (ev_begin != nullptr && cudaEventRecord(static_cast<cudaEvent_t>(ev_begin), st) != cudaSuccess)
         return HTA_ERR_CUDA;
-    r = run_prefix(sh, pl, q, k_cache, v_cache, cache_seqlens, o_ws, lse_ws, ostride, lstride, st, pg);
+    r = run_prefix(sh, pl, q, k_cache, v_cache, cache_seqlens, o_ws, lse_ws, ostride, lstride, st, pg, f8);
     if (r != HTA_OK) return r;
     if (ev_end != nullptr && cudaEventRecord(static_cast<cudaEvent_t>(ev_end), st) != cudaSuccess)
         return HTA_ERR_CUDA;
@@ -530,6 +560,64 @@ hta_status_t hta_forward(const hta_shape_t *shape, const void *q, const void *k_
                          hta_stream_t stream) {
     return hta_forward_timed(shape, q, k_cache, v_cache, cache_seqlens, k_tree, v_tree, mask, mask_batch_stride, o,
                              lse_out, ws, ws_bytes, stream, nullptr, nullptr);
+}
+
+// Checks of the FP8-cache entry points: bf16 q / tree / o, d = 128 or 64, E4M3 rows 16-byte aligned.
+static hta_status_t check_fp8(const hta_shape_t *shape, const void *k, const void *v, const float *ks,
+                              const float *vs) {
+    if (shape == nullptr || !k || !v || !ks || !vs) return HTA_ERR_INVALID_ARGUMENT;
+    if (shape->dtype != HTA_BF16) return HTA_ERR_UNSUPPORTED;
+    for (int i = 0; i < 3; ++i)
+        if (shape->kv_strides[i] % 16 != 0) return HTA_ERR_INVALID_ARGUMENT;  // bytes: 16-byte rows
+    if (!is_aligned(k, 16) || !is_aligned(v, 16) || !is_aligned(ks, 4) || !is_aligned(vs, 4))
+        return HTA_ERR_INVALID_ARGUMENT;
+    return HTA_OK;
+}
+
+hta_status_t hta_forward_fp8kv(const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,
+                               const float *k_scale, const float *v_scale, const int32_t *cache_seqlens,
+                               const void *k_tree, const void *v_tree, const uint8_t *mask,
+                               int64_t mask_batch_stride, void *o, float *lse_out, void *ws, size_t ws_bytes,
+                               hta_stream_t stream) {
+    hta_status_t r = check_fp8(shape, k_cache, v_cache, k_scale, v_scale);
+    if (r != HTA_OK) return r;
+    const Fp8Args f8{k_scale, v_scale};
+    return forward_impl(nullptr, shape, q, k_cache, v_cache, cache_seqlens, k_tree, v_tree, mask, mask_batch_stride, o,
+                        lse_out, ws, ws_bytes, stream, nullptr, nullptr, &f8);
+}
+
+hta_status_t hta_prefix_attn_fp8kv(const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,
+                                   const float *k_scale, const float *v_scale, const int32_t *cache_seqlens,
+                                   float *o_part, float *lse_part, void *ws, size_t ws_bytes, hta_stream_t stream) {
+    hta_status_t r = check_fp8(shape, k_cache, v_cache, k_scale, v_scale);
+    if (r != HTA_OK) return r;
+    Shape sh;
+    if ((r = check_shape(shape, &sh)) != HTA_OK) return r;
+    if (!q || !o_part || !lse_part || !is_aligned(q, 16) || !is_aligned(o_part, 16)) return HTA_ERR_INVALID_ARGUMENT;
+    if ((r = check_device()) != HTA_OK) return r;
+    const hta_shape_t &s = sh.s;
+    const PrefixPlan pl = make_plan(sh, device_sms());
+    const Fp8Args f8{k_scale, v_scale};
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (pl.splits == 1)
+        return run_prefix(sh, pl, q, k_cache, v_cache, cache_seqlens, o_part, lse_part, 0, 0, st, nullptr, &f8);
+    const size_t need = size_t(pl.splits) * part_floats(s) * sizeof(float);
+    if (ws == nullptr || ws_bytes < need || !is_aligned(ws, 16)) return HTA_ERR_WORKSPACE;
+    float *o_ws = static_cast<float *>(ws);
+    const int64_t ostride = int64_t(s.B) * s.T * s.H * s.d;
+    float *lse_ws = o_ws + size_t(pl.splits) * ostride;
+    const int64_t lstride = int64_t(s.B) * s.H * s.T;
+    r = run_prefix(sh, pl, q, k_cache, v_cache, cache_seqlens, o_ws, lse_ws, ostride, lstride, st, nullptr, &f8);
+    if (r != HTA_OK) return r;
+    TreeMergeParams p = base_tm(sh);
+    p.do_tree = 0;
+    p.n_parts = pl.splits;
+    p.o_parts = o_ws;
+    p.lse_parts = lse_ws;
+    p.o_part_stride = ostride;
+    p.lse_part_stride = lstride;
+    set_out_contig_f32(p, s, o_part, lse_part);
+    return launch_tree_merge(p, s.d, s.dtype, HTA_FP32, true, st) == cudaSuccess ? HTA_OK : HTA_ERR_CUDA;
 }
 
 hta_status_t hta_build_tree_mask(const int32_t *parents, int32_t T, uint8_t *mask, int32_t on_device,

@@ -47,6 +47,10 @@ struct PrefixParams {
     int64_t bt_stride;
     int page_size;
     int max_pages;                              // entries per block-table row (clamp)
+    // FP8 cache (kv8 = 1): k/v are E4M3 bytes, K = k_scale[g] * E4M3 and
+    // V = v_scale[g] * E4M3 per KV head g (device float [H_kv]); the maps load E4M3 tiles.
+    int kv8;
+    const float *k_scale, *v_scale;
     float *o_out;                     // [S][B][T][H][d] fp32, normalised partials
     float *lse_out;                   // [S][B][H][T] natural-log LSE
     int64_t o_split_stride, lse_split_stride;  // elements between splits

@@ -81,7 +81,8 @@ constexpr int kTraceRecs = 1024;  // per warp
 #endif
 
 // Timing diagnostics only (tools/lib_variants.sh; results are wrong): HTA_DIAG bit 1 = no P
-// stores to TMEM, bit 2 = no exponentials (P = x), bit 4 = no wait for the row-max hand-over.
+// stores to TMEM, bit 2 = no exponentials (P = x), bit 4 = no wait for the row-max hand-over,
+// bit 8 = FP8 pair widening signalled with a CTA-scope (not cluster-scope) release.
 #ifndef HTA_DIAG
 #define HTA_DIAG 0
 #endif
@@ -91,14 +92,82 @@ constexpr uint64_t kKvPolicy = kPolicyEvictFirst;  // L2 policy of the streamed 
 #define HTA_POLY 2
 #endif
 constexpr int kPolyPairs = HTA_POLY;               // pairs of every 8 whose exp2 runs on the FMA pipe
-constexpr float kSpecLimit = 0x1p60f;              // largest P the speculative pass may produce
+// Largest P the speculative pass may produce (log2: kSpecArg): 2^60 for bf16 P; 2^15 for the f16 P
+// of the FP8-cache variant (f16 overflows at 65504).
+template <bool KV8>
+struct SpecCfg {
+    static constexpr float kLimit = KV8 ? 0x1p15f : 0x1p60f;
+    static constexpr float kArg = KV8 ? 15.f : 60.f;
+};
 
 // The running max after a tile whose requirement is rho (its row max, or -inf when the tile
-// fits under m): raised only when some exponent argument would exceed 60 (P > 2^60).
-__device__ __forceinline__ float fold_max(float m, float rho) { return rho > m + 60.f ? rho : m; }
+// fits under m): raised only when some exponent argument would exceed kArg (P > 2^kArg).
+template <bool KV8>
+__device__ __forceinline__ float fold_max(float m, float rho) { return rho > m + SpecCfg<KV8>::kArg ? rho : m; }
 
-__device__ __forceinline__ void setmaxnreg_dec(void) { asm volatile("setmaxnreg.dec.sync.aligned.u32 32;"); }
-__device__ __forceinline__ void setmaxnreg_inc(void) { asm volatile("setmaxnreg.inc.sync.aligned.u32 112;"); }
+#ifndef HTA_WIDEN_UNROLL
+#define HTA_WIDEN_UNROLL 4
+#endif
+constexpr int kWidenUnroll = HTA_WIDEN_UNROLL;  // (4 with the 48-register producers)
+#ifndef HTA_L2_AHEAD
+#define HTA_L2_AHEAD 4
+#endif
+constexpr int kL2Ahead = HTA_L2_AHEAD;  // FP8 cache: tiles prefetched into L2 beyond the smem ring
+
+// FP8 KV cache: an E4M3 tile (kRows rows of kRowBytes bytes) landed by TMA in
+// the upper half of its f16 ring slot is widened IN PLACE into the slot's f16 K-major SWIZZLE_128B
+// layout ([kRowBytes/64 atoms][kRows rows][128 B]); rows >= valid are written as zeros (keys past
+// the sequence end, Z13).  Rows are converted in ascending order, each row within one warp
+// instruction, and f16 row r never overlaps an E4M3 row beyond r: nothing is overwritten before it
+// is read.  E4M3 -> f16 is exact.
+template <int kRowBytes, int kRows>
+__device__ __forceinline__ void widen_e4m3_tile(uint8_t *slot, int lane, int valid) {
+    constexpr int kChunks = kRowBytes / 16;  // 16-byte E4M3 chunks per row
+    constexpr int kSlotBytes = kRows * kRowBytes * 2;
+    const uint8_t *src = slot + kSlotBytes / 2;
+#pragma unroll kWidenUnroll
+    for (int base = 0; base < kRows * kChunks; base += 32) {
+        const int idx = base + lane;
+        const int r = idx / kChunks, c = idx % kChunks;
+        const uint4 x = *reinterpret_cast<const uint4 *>(src + r * kRowBytes + c * 16);
+        uint4 y0, y1;
+        y0.x = e4m3x2_to_f16x2(static_cast<uint16_t>(x.x));
+        y0.y = e4m3x2_to_f16x2(static_cast<uint16_t>(x.x >> 16));
+        y0.z = e4m3x2_to_f16x2(static_cast<uint16_t>(x.y));
+        y0.w = e4m3x2_to_f16x2(static_cast<uint16_t>(x.y >> 16));
+        y1.x = e4m3x2_to_f16x2(static_cast<uint16_t>(x.z));
+        y1.y = e4m3x2_to_f16x2(static_cast<uint16_t>(x.z >> 16));
+        y1.z = e4m3x2_to_f16x2(static_cast<uint16_t>(x.w));
+        y1.w = e4m3x2_to_f16x2(static_cast<uint16_t>(x.w >> 16));
+        if (r >= valid) y0 = y1 = make_uint4(0u, 0u, 0u, 0u);
+        const int e0 = c * 16;
+        const int ch = (e0 % 64) / 8;  // even: the first of the two 16-byte f16 chunks
+        uint8_t *row = slot + (e0 / 64) * (kRows * 128) + r * 128;
+        *reinterpret_cast<uint4 *>(row + ((ch ^ (r & 7)) << 4)) = y0;
+        *reinterpret_cast<uint4 *>(row + (((ch + 1) ^ (r & 7)) << 4)) = y1;
+    }
+}
+
+// Register split between the producer/MMA warpgroup and the softmax warpgroups (640 threads launch
+// at 96 registers each): 32 / 112 for the bf16 cache; the FP8 cache's producers widen tiles and
+// get more (HTA_KV8_REGS: 48 / 104).
+#ifndef HTA_KV8_REGS
+#define HTA_KV8_REGS 48
+#endif
+template <bool KV8>
+__device__ __forceinline__ void setmaxnreg_dec() {
+    if constexpr (KV8 && HTA_KV8_REGS == 48)
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
+    else
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
+}
+template <bool KV8>
+__device__ __forceinline__ void setmaxnreg_inc() {
+    if constexpr (KV8 && HTA_KV8_REGS == 48)
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
+    else
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
+}
 
 // Warp roles.  The SM sub-partition scheduler issues from the eligible warp with the highest id
 // first, so the K TMA / MMA / V TMA / spare warpgroup takes the highest ids (HTA_OTHER_WG = 4:
@@ -140,7 +209,7 @@ struct TcCfg {
     static constexpr int kThreads = 32 * (4 + 2 * kGroupWarps);
     static constexpr int kVOff = kQBytes + kSlotsK * kKBytes;   // start of the V ring
     static constexpr int kBarOff = kVOff + kSlotsV * kVBytes;
-    static constexpr int kNumBars = 2 * kSlotsK + 2 * kSlotsV + 3 * kSBufs + 4;
+    static constexpr int kNumBars = 3 * kSlotsK + 3 * kSlotsV + 3 * kSBufs + 4;
     static constexpr int kMaxOff = kBarOff + 8 * kNumBars + 8;  // row-max hand-over rho[3][128]
     static constexpr int kSmemBytes = kMaxOff + 3 * 128 * 4;    // base is 1024-aligned (__align__ below)
     static_assert(kSlotsK >= 2 && kSlotsV >= 2, "need at least 2 slots per ring");
@@ -162,11 +231,12 @@ __device__ __forceinline__ int paged_row(const PrefixParams &p, int b, int k) {
     return e * p.page_size + k % p.page_size;
 }
 
-template <int D, bool PAIR>
+template <int D, bool PAIR, bool KV8>
 __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     prefix_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
                      const __grid_constant__ CUtensorMap tmap_v, const PrefixParams p) {
     using C = TcCfg<D, PAIR>;
+    using Spec = SpecCfg<KV8>;
     extern __shared__ __align__(1024) uint8_t smem[];  // 128B-swizzled tiles need 1024B alignment
     uint8_t *sQ = smem;
     uint8_t *sK = smem + C::kQBytes;
@@ -183,7 +253,9 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     uint64_t *q_full = o_final + 1;                // [1]       Q staged (the leader's copy is the one used)
     uint64_t *v_tail_land = q_full + 1;            // [1]       this CTA's part of the last V tile landed
     uint64_t *v_tail_ready = v_tail_land + 1;      // [1]       ... and sanitised (the leader's copy is used)
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(v_tail_ready + 1);
+    uint64_t *k_land = v_tail_ready + 1;           // [kSlotsK]  FP8 cache: this CTA's E4M3 K tile landed
+    uint64_t *v_land = k_land + C::kSlotsK;        // [kSlotsV]  ... E4M3 V tile landed
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(v_land + C::kSlotsV);
     // row-max hand-over of tile j in slot j % 3: one 32-bit word per row, rho_j with the
     // generation parity (j / 3) & 1 in its lowest mantissa bit, written once by the group of tile j
     // and read by polling (no barrier) by the group of tile j+1, which is also the next writer of
@@ -219,13 +291,17 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         tma_prefetch_desc(&tmap_v);
     }
     if (warp == kWarpMma && lane == 0) {
+        // the FP8 variant fills a slot by widening in place: its full barrier counts one arrival per
+        // CTA (no TMA bytes); the E4M3 tile's TMA completes on the CTA's own land barrier
         for (int i = 0; i < C::kSlotsK; ++i) {
-            mbar_init(&k_full[i], 1);
+            mbar_init(&k_full[i], KV8 && PAIR ? 2 : 1);
             mbar_init(&k_empty[i], 1);
+            mbar_init(&k_land[i], 1);
         }
         for (int i = 0; i < C::kSlotsV; ++i) {
-            mbar_init(&v_full[i], 1);
+            mbar_init(&v_full[i], KV8 && PAIR ? 2 : 1);
             mbar_init(&v_empty[i], 1);
+            mbar_init(&v_land[i], 1);
         }
         for (int i = 0; i < C::kSBufs; ++i) {
             mbar_init(&s_full[i], 1);
@@ -287,7 +363,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             lse_base[(static_cast<int64_t>(b) * p.H + h) * p.T + t] = -INFINITY;
         }
     } else if (warp >= kOtherBase && warp < kOtherBase + 4) {
-        setmaxnreg_dec();
+        setmaxnreg_dec<KV8>();
         if (warp == kWarpK) {
             // ================= TMA producer of Q and the K ring (K_j is consumed by S_j).  K and V
             // have producers of their own, so K tiles run ahead of V tiles by as many slots as the
@@ -310,7 +386,46 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 }
             }
             const uint32_t kfull0 = PAIR ? mapa_shared(smem_u32(&k_full[0]), 0) : 0u;
-            if (p.page_size > 0) {
+            if constexpr (KV8) {
+                // FP8 cache: the whole warp loads E4M3 tiles kLead tiles ahead (lane 0 issues the
+                // TMA into the upper half of the f16 slot) and widens tile j in place, then signals
+                // the MMA warp (in a pair: the leader's barrier, both CTAs arrive)
+                constexpr int kLead = C::kSlotsK - 1;
+                auto issue = [&](int jj) {
+                    const int slot = jj % C::kSlotsK;
+                    mbar_wait(&k_empty[slot], ((jj / C::kSlotsK) & 1) ^ 1u);
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int r0 = static_cast<int>(key_lo) + (PAIR ? static_cast<int>(rank) * C::kKRows : 0);
+                        mbar_arrive_expect_tx(&k_land[slot], C::kKBytes / 2);
+                        tma_load_4d(sK + slot * C::kKBytes + C::kKBytes / 2, &tmap_k, &k_land[slot], 0, g,
+                                    r0 + jj * kBlockN, b, kKvPolicy);
+                        // the ring is shallow (each in-flight tile holds a whole f16 slot): stage the
+                        // tiles further ahead in L2
+                        if (jj + kL2Ahead < n_tiles) tma_prefetch_l2_4d(&tmap_k, 0, g, r0 + (jj + kL2Ahead) * kBlockN, b);
+                    }
+                };
+                for (int jj = 0; jj < kLead && jj < n_tiles; ++jj) issue(jj);
+                for (int j = 0; j < n_tiles; ++j) {
+                    const int slot = j % C::kSlotsK;
+                    mbar_wait(&k_land[slot], (j / C::kSlotsK) & 1);
+                    __syncwarp();
+                    HTA_TR(30, j);
+                    widen_e4m3_tile<D, C::kKRows>(sK + slot * C::kKBytes, lane, C::kKRows);
+                    fence_proxy_async_smem();  // generic-proxy writes -> read by the tensor core
+                    __syncwarp();
+                    HTA_TR(32, j);
+                    if (lane == 0) {
+                        if (PAIR && (HTA_DIAG & 8))
+                            mbar_arrive_remote(kfull0 + 8u * slot);
+                        else if (PAIR)
+                            mbar_arrive_remote_release_cluster(kfull0 + 8u * slot);
+                        else
+                            mbar_arrive(&k_full[slot]);
+                    }
+                    if (j + kLead < n_tiles) issue(j + kLead);
+                }
+            } else if (p.page_size > 0) {
                 // paged KV: the whole warp runs the loop (waits converged); lane i translates box i
                 // (16 keys) of the tile through the block table, lane 0 issues the TMA boxes
                 constexpr int kBoxes = C::kKRows / 16;
@@ -377,6 +492,45 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             // barrier of this CTA (v_tail_land); the MMA warp then waits on v_tail_ready (both CTAs
             // of a pair arrive) instead of v_full.
             const uint32_t vfull0 = PAIR ? mapa_shared(smem_u32(&v_full[0]), 0) : 0u;
+            if constexpr (KV8) {
+                // FP8 cache: as the K producer; rows past the sequence end of the last tile are
+                // written as zeros while widening (so no separate sanitising pass)
+                constexpr int kLead = C::kSlotsV - 1;
+                auto issue = [&](int jj) {
+                    const int slot = jj % C::kSlotsV;
+                    mbar_wait(&v_empty[slot], ((jj / C::kSlotsV) & 1) ^ 1u);
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int c0 = PAIR ? static_cast<int>(rank) * 64 : 0;
+                        mbar_arrive_expect_tx(&v_land[slot], C::kVBytes / 2);
+                        tma_load_4d(sV + slot * C::kVBytes + C::kVBytes / 2, &tmap_v, &v_land[slot], c0, g,
+                                    static_cast<int>(key_lo) + jj * kBlockN, b, kKvPolicy);
+                        if (jj + kL2Ahead < n_tiles)
+                            tma_prefetch_l2_4d(&tmap_v, c0, g, static_cast<int>(key_lo) + (jj + kL2Ahead) * kBlockN, b);
+                    }
+                };
+                for (int jj = 0; jj < kLead && jj < n_tiles; ++jj) issue(jj);
+                for (int j = 0; j < n_tiles; ++j) {
+                    const int slot = j % C::kSlotsV;
+                    mbar_wait(&v_land[slot], (j / C::kSlotsV) & 1);
+                    __syncwarp();
+                    HTA_TR(31, j);
+                    widen_e4m3_tile<C::kVCols, kBlockN>(sV + slot * C::kVBytes, lane,
+                                                        (tail_zero && j == n_tiles - 1) ? tail_valid : kBlockN);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    HTA_TR(33, j);
+                    if (lane == 0) {
+                        if (PAIR && (HTA_DIAG & 8))
+                            mbar_arrive_remote(vfull0 + 8u * slot);
+                        else if (PAIR)
+                            mbar_arrive_remote_release_cluster(vfull0 + 8u * slot);
+                        else
+                            mbar_arrive(&v_full[slot]);
+                    }
+                    if (j + kLead < n_tiles) issue(j + kLead);
+                }
+            } else {
             auto v_bar = [&](int j, int slot, bool tail) -> uint32_t {  // barrier the tile's TMA signals
                 if (tail) return smem_u32(v_tail_land);
                 return PAIR ? vfull0 + 8u * slot : smem_u32(&v_full[slot]);
@@ -451,6 +605,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                         mbar_arrive(v_tail_ready);
                 }
             }
+            }  // !KV8
         } else if (warp == kWarpMma && leader) {
             // ================= MMA issuer: the whole warp of the leader CTA runs this loop with
             // warp-uniform values and elect.sync issues each tcgen05 op (one lane, no waterfall);
@@ -458,8 +613,9 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             // barrier waits: S_0, S_1, S_2, then per tile j: PV_j (needs V_j and P_j), S_{j+3}
             // (needs K_{j+3}; its buffer was last read by PV_j, issued just before).
             constexpr int kM = PAIR ? 256 : 128;
-            const uint32_t idesc_qk = idesc_bf16_f32(kM, kBlockN, 0);
-            const uint32_t idesc_pv = idesc_bf16_f32(kM, D, 1);
+            // FP8 cache: Q, the widened K/V and P are f16 (E4M3 and bf16 Q convert exactly)
+            const uint32_t idesc_qk = KV8 ? idesc_f16_f32(kM, kBlockN, 0) : idesc_bf16_f32(kM, kBlockN, 0);
+            const uint32_t idesc_pv = KV8 ? idesc_f16_f32(kM, D, 1) : idesc_bf16_f32(kM, D, 1);
             const uint64_t qd0 = sdesc_sw128(smem_u32(sQ), 16, 1024);
             const uint64_t kd0 = sdesc_sw128(smem_u32(sK), 16, 1024);
             const uint64_t vd0 = sdesc_sw128(smem_u32(sV), kBlockN * 128, 1024);
@@ -500,7 +656,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             __syncwarp();
             for (int jj = 0; jj < C::kSBufs && jj < n_tiles; ++jj) start_S(jj);
             for (int j = 0; j < n_tiles; ++j) {
-                if (tail_zero && j == n_tiles - 1) {  // the V producers sanitised this tile
+                if (!KV8 && tail_zero && j == n_tiles - 1) {  // the V producers sanitised this tile
                     if (PAIR)
                         mbar_wait_cluster(v_tail_ready, 0);
                     else
@@ -537,7 +693,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             __syncwarp();
         }
     } else {
-        setmaxnreg_inc();
+        setmaxnreg_inc<KV8>();
         // ================= softmax: group grp takes tiles j = grp, grp + 2, ...; warp gw of a
         // group owns rows 32*(gw%4) + 16*(gw/4) .. +15 of the tile (TMEM lane quarter gw % 4 =
         // warp % 4); lane t holds row (t & 15) of them, keys [64*(t>>4), +64) of each tile.
@@ -568,6 +724,12 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             for (int i = 0; i < kPer; ++i) {
                 const int idx = qt + i * kQThreads;
                 const int r = idx / kChunks, ch = idx % kChunks;
+                if constexpr (KV8) {  // bf16 -> f16 (exact for |q| in the f16 range)
+                    uint32_t *w = reinterpret_cast<uint32_t *>(&val[i]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        w[e] = pack_f16x2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xFFFF0000u));
+                }
                 if (idx < kRowsPerTile * kChunks)
                     *reinterpret_cast<uint4 *>(sQ + (ch / 8) * C::kRegionBytes + r * 128 + (((ch & 7) ^ (r & 7)) << 4)) =
                         val[i];
@@ -588,7 +750,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         const int grow = row0 + r;
         const bool pad_warp = row0 + quarter * 32 + rh * 16 >= p.M;  // warp-uniform
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32 + rh * 16) << 16;
-        const float c = p.scale_log2;
+        const float c = KV8 ? p.scale_log2 * p.k_scale[g] : p.scale_log2;  // K = k_scale[g] * E4M3
         const uint32_t pfull0 = PAIR ? mapa_shared(smem_u32(&p_full[0]), 0) : 0u;
         constexpr int kHalf = kBlockN / 2;  // S columns per thread
         // m_run: the row's running max (log2 units) as last known to this group; the group's row
@@ -675,7 +837,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                             acc1 = __fadd2_rn(acc1, pp);
                         else
                             acc0 = __fadd2_rn(acc0, pp);
-                        pk[ch * (kChunk / 2) + i] = pack_bf16x2(pp.x, pp.y);
+                        pk[ch * (kChunk / 2) + i] = KV8 ? pack_f16x2(pp.x, pp.y) : pack_bf16x2(pp.x, pp.y);
                     }
                 }
                 return (acc0.x + acc1.x) + (acc0.y + acc1.y);
@@ -694,7 +856,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             // group's last fold; tile j-1 is folded in below).
             const float m_spec = m_run;
             float lsum = exp_pack(m_spec, std::true_type{});
-            const bool ovf = __any_sync(0xffffffffu, !(lsum <= kSpecLimit) || xmax_poly > 60.f);
+            const bool ovf = __any_sync(0xffffffffu, !(lsum <= Spec::kLimit) || xmax_poly > Spec::kArg);
             // rho_j: this tile's row max if the speculative pass overflowed, else -inf (the tile
             // needs no larger running max than the row already has).  Handed to the group of tile
             // j+1 at once: no group waits on the other before its own hand-over.
@@ -718,10 +880,10 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     while (((wv = ld_volatile_shared(src)) & 1u) != want)
                         if (global_ns() - t0 > kWatchdogNs) __trap();
                 }
-                m_prev = fold_max(m_prev, __uint_as_float(wv));
+                m_prev = fold_max<KV8>(m_prev, __uint_as_float(wv));
             }
             HTA_TRS(3);
-            const float m_fin = fold_max(m_prev, rho);
+            const float m_fin = fold_max<KV8>(m_prev, rho);
             if (__any_sync(0xffffffffu, ovf || m_fin != m_spec)) lsum = exp_pack(m_fin, std::false_type{});
             // P_j over S_j in TMEM (columns [Ch/2, Ch/2 + 32)), without waiting
             if (!(HTA_DIAG & 1)) {
@@ -769,7 +931,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             const float li = x_l[((i >> 1) * 128 + r) * 2 + (i & 1)];
             if (li > 0.f) l_tot += li * fast_exp2(mi - m_tot);
         }
-        const float inv = 1.0f / l_tot;
+        const float inv = (KV8 ? p.v_scale[g] : 1.0f) / l_tot;  // V = v_scale[g] * E4M3
         const bool row_ok = grow < p.M && !pad_warp;
         int t = 0, h = 0;
         if (row_ok) {
@@ -822,11 +984,11 @@ extern "C" __attribute__((visibility("default"))) int hta_debug_set_trace(void *
 }
 #endif
 
-template <int D, bool PAIR>
+template <int D, bool PAIR, bool KV8>
 static cudaError_t launch_tc(const PrefixParams &p, const CUtensorMap &tq, const CUtensorMap &tk, const CUtensorMap &tv,
                              cudaStream_t s) {
     using C = TcCfg<D, PAIR>;
-    auto kern = prefix_tc_kernel<D, PAIR>;
+    auto kern = prefix_tc_kernel<D, PAIR, KV8>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
@@ -857,9 +1019,15 @@ int prefix_tc_smem_bytes(int d, int nt) {
 
 cudaError_t launch_prefix_tc(const PrefixParams &p, const CUtensorMap &tq, const CUtensorMap &tk, const CUtensorMap &tv,
                              int, cudaStream_t s) {
+    if (p.kv8) {
+        if (p.d == 128)
+            return p.nt == 2 ? launch_tc<128, true, true>(p, tq, tk, tv, s) : launch_tc<128, false, true>(p, tq, tk, tv, s);
+        if (p.d == 64 && p.nt == 1) return launch_tc<64, false, true>(p, tq, tk, tv, s);
+        return cudaErrorInvalidValue;
+    }
     if (p.d == 128)
-        return p.nt == 2 ? launch_tc<128, true>(p, tq, tk, tv, s) : launch_tc<128, false>(p, tq, tk, tv, s);
-    if (p.d == 64 && p.nt == 1) return launch_tc<64, false>(p, tq, tk, tv, s);
+        return p.nt == 2 ? launch_tc<128, true, false>(p, tq, tk, tv, s) : launch_tc<128, false, false>(p, tq, tk, tv, s);
+    if (p.d == 64 && p.nt == 1) return launch_tc<64, false, false>(p, tq, tk, tv, s);
     return cudaErrorInvalidValue;
 }
 

@@ -144,6 +144,12 @@ __device__ __forceinline__ void tma_load_4d(void *smem_dst, const void *map, uin
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
         : "memory");
 }
+// L2 prefetch of a tensor box (no shared-memory destination, no completion).
+__device__ __forceinline__ void tma_prefetch_l2_4d(const void *map, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];" ::"l"(map), "r"(c0), "r"(c1),
+                 "r"(c2), "r"(c3)
+                 : "memory");
+}
 // The same with the completion barrier given as a shared::cta address.
 __device__ __forceinline__ void tma_load_4d_bar(void *smem_dst, const void *map, uint32_t bar, int c0, int c1, int c2,
                                                 int c3, uint64_t policy) {
@@ -250,6 +256,11 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_byt
     return d;
 }
 
+// Instruction descriptor for kind::f16 with f16 A/B and fp32 accumulate (a/b_format = 0).
+__host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N, int b_mn_major) {
+    return (1u << 4) | (static_cast<uint32_t>(b_mn_major) << 16) | ((static_cast<uint32_t>(N) >> 3) << 17) |
+           ((static_cast<uint32_t>(M) >> 4) << 24);
+}
 // Instruction descriptor for kind::f16 with bf16 A/B and fp32 accumulate.
 // bits: [4,6) c_format=1 (F32), [7,10) a_format=1 (BF16), [10,13) b_format=1 (BF16),
 // [15] a_major (0 = K), [16] b_major (1 = MN), [17,23) N>>3, [24,29) M>>4.
@@ -354,6 +365,17 @@ __device__ __forceinline__ void tmem_st_16x16_split_nowait(uint32_t taddr, const
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+// Two FP8 E4M3 values (low byte = first element) -> f16x2, exact (E4M3 is a subset of f16).
+__device__ __forceinline__ uint32_t e4m3x2_to_f16x2(uint16_t x) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(r) : "h"(x));
+    return r;
+}
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

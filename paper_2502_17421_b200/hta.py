@@ -50,6 +50,10 @@ _SIG = {
     "hta_forward_paged": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, _P, _P, ctypes.c_int32, ctypes.c_int32, _P,
                                          ctypes.c_int32, _P, _P, _P, _P, ctypes.c_int64, _P, _P, _P, ctypes.c_size_t,
                                          _P]),
+    "hta_forward_fp8kv": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                         ctypes.c_int64, _P, _P, _P, ctypes.c_size_t, _P]),
+    "hta_prefix_attn_fp8kv": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                             ctypes.c_size_t, _P]),
     "hta_build_tree_mask": (ctypes.c_int, [_P, ctypes.c_int32, _P, ctypes.c_int32, _P]),
     "hta_validate_tree_mask": (ctypes.c_int, [_P, ctypes.c_int32]),
     "hta_accept_greedy": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _P,
@@ -280,6 +284,57 @@ def hta_forward_paged(q, k_pool, v_pool, block_table, k_tree, v_tree, mask, cach
         ws.numel() * ws.element_size(), _stream(stream)))
     _hold(stream, None if ws is ws_given else ws, None if bt is block_table else bt)
     return o, lse_out
+
+
+def _fp8_shape(q, k8, k_tree=None, scale=None, num_splits=0, max_seqlen=0):
+    """Shape of an FP8-cache call: k8 is a uint8 (E4M3 bytes) [B, N, H_kv, d] tensor."""
+    if k8.dtype not in (torch.uint8, getattr(torch, "float8_e4m3fn", torch.uint8)):
+        raise TypeError("the FP8 cache must hold E4M3 bytes (uint8 or float8_e4m3fn)")
+    shape = make_shape(q, k_tree=k_tree, H_kv=k8.shape[2], N_max=k8.shape[1], scale=scale, num_splits=num_splits,
+                       max_seqlen=max_seqlen)
+    shape.N_max, shape.H_kv = k8.shape[1], k8.shape[2]
+    shape.kv_strides = _strides3(k8)
+    return shape
+
+
+def hta_forward_fp8kv(q, k8, v8, k_scale, v_scale, k_tree, v_tree, mask, cache_seqlens=None, o=None, lse_out=None,
+                      ws=None, want_lse=True, scale=None, num_splits=0, max_seqlen=0, stream=None):
+    """hta_forward over an E4M3 cache k8 / v8 [B, N, H_kv, d] (uint8 bytes) with per-KV-head
+    float32 scales (K = k_scale[g] * K8, V = v_scale[g] * V8); q / tree K,V / O bf16."""
+    shape = _fp8_shape(q, k8, k_tree=k_tree, scale=scale, num_splits=num_splits, max_seqlen=max_seqlen)
+    B, T, H, d = q.shape
+    mbs = 0 if mask.dim() == 2 else mask.stride(0)
+    o = _out_like_q(q, o)
+    if want_lse and lse_out is None:
+        lse_out = torch.empty(B, H, T, dtype=torch.float32, device=q.device)
+    ws_given = ws
+    ws = _workspace(shape, q.device, ws)
+    ks, vs = k_scale.to(torch.float32).contiguous(), v_scale.to(torch.float32).contiguous()
+    _check("hta_forward_fp8kv", lib().hta_forward_fp8kv(
+        ctypes.byref(shape), _ptr(q), _ptr(k8), _ptr(v8), _ptr(ks), _ptr(vs), _ptr(cache_seqlens), _ptr(k_tree),
+        _ptr(v_tree), _ptr(mask), mbs, _ptr(o), _ptr(lse_out), _ptr(ws), ws.numel() * ws.element_size(),
+        _stream(stream)))
+    _hold(stream, None if ws is ws_given else ws, None if ks is k_scale else ks, None if vs is v_scale else vs)
+    return o, lse_out
+
+
+def hta_prefix_attn_fp8kv(q, k8, v8, k_scale, v_scale, cache_seqlens=None, o_part=None, lse_part=None, ws=None,
+                          scale=None, num_splits=0, max_seqlen=0, stream=None):
+    """Prefix pass over an E4M3 cache: fp32 O [B,T,H,d] and natural-log LSE [B,H,T]."""
+    shape = _fp8_shape(q, k8, scale=scale, num_splits=num_splits, max_seqlen=max_seqlen)
+    B, T, H, d = q.shape
+    if o_part is None:
+        o_part = torch.empty(B, T, H, d, dtype=torch.float32, device=q.device)
+    if lse_part is None:
+        lse_part = torch.empty(B, H, T, dtype=torch.float32, device=q.device)
+    ws_given = ws
+    ws = _workspace(shape, q.device, ws)
+    ks, vs = k_scale.to(torch.float32).contiguous(), v_scale.to(torch.float32).contiguous()
+    _check("hta_prefix_attn_fp8kv", lib().hta_prefix_attn_fp8kv(
+        ctypes.byref(shape), _ptr(q), _ptr(k8), _ptr(v8), _ptr(ks), _ptr(vs), _ptr(cache_seqlens), _ptr(o_part),
+        _ptr(lse_part), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
+    _hold(stream, None if ws is ws_given else ws, None if ks is k_scale else ks, None if vs is v_scale else vs)
+    return o_part, lse_part
 
 
 # --------------------------------------------------------------------------- tree utilities

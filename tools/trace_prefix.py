@@ -36,6 +36,12 @@ def main():
     x = [t.to(dev) for t in (w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree)]
     mask = hta.hta_build_tree_mask(w.parents[0].to(dev))
     fwd = lambda: hta.hta_forward(*x, mask)  # noqa: E731
+    if os.environ.get("FP8"):  # the forward over an E4M3 copy of the cache
+        from workloads import fp8_cache
+        k8, ks = fp8_cache(w.k_cache)
+        v8, vs = fp8_cache(w.v_cache)
+        k8, v8, ks, vs = k8.to(dev), v8.to(dev), ks.to(dev), vs.to(dev)
+        fwd = lambda: hta.hta_forward_fp8kv(x[0], k8, v8, ks, vs, x[3], x[4], mask)  # noqa: E731
     if os.environ.get("PAGED"):  # the paged forward over in-order 16-key pages
         page = 16
         maxp = w.N // page
@@ -156,6 +162,17 @@ def main():
         vlead = [mma[1][j] - ev[(vw, 31)][j] for j in tiles if j in ev[(vw, 31)]]
         print(f"producers: K issue->landed(+S issue) median {statistics.median(kl):.0f}, V issue->landed median "
               f"{statistics.median(vl):.0f}, V issue -> PV_j issue median {statistics.median(vlead):.0f}")
+    # FP8 cache: per producer, landed (30/31) -> widened (32/33) and the gap between tiles
+    for e0, e1, nm in ((30, 32, "K"), (31, 33, "V")):
+        w0 = next((w for w in range(32) if (w, e1) in ev), None)
+        if w0 is None:
+            continue
+        a, bb = ev[(w0, e0)], ev[(w0, e1)]
+        js = sorted(j for j in bb if j in a)
+        wid = [bb[j] - a[j] for j in js]
+        gap = [a[j2] - bb[j1] for j1, j2 in zip(js, js[1:])]
+        print(f"FP8 {nm} producer (warp {w0}): widen median {statistics.median(wid):.0f} cycles, "
+              f"wait for the next tile to land median {statistics.median(gap):.0f}")
     # per warp: median lag of its publish behind the first warp of its group
     lags = defaultdict(list)
     for j in range(2, len(tiles) - 2):

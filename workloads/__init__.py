@@ -15,4 +15,5 @@ from .generators import (  # noqa: F401
     beam_tree,
     random_mask,
     accept_tokens,
+    fp8_cache,
 )

@@ -244,3 +244,17 @@ def config_workload(name: str, dist: str = "V1", seed: int = 0, **over) -> Workl
     c.update(over)
     return make_workload(c["B"], c["T"], c["H"], c["H_kv"], c["d"], c["N"], c["dtype"],
                          dist=dist, seed=seed, tree=c["tree"])
+
+
+def fp8_cache(x: torch.Tensor):
+    """An E4M3 copy of a cache tensor [B, N, H_kv, d] for the FP8-cache row:
+    per KV head a power-of-two scale (2^ceil(log2(amax / 448)), so that scale * E4M3 is exact in
+    float32) and the E4M3 bytes of x / scale (torch's round-to-nearest conversion).  Returns
+    (bytes uint8 [B, N, H_kv, d], scale float32 [H_kv]).  Input generation only: the E4M3 values
+    are the inputs both the oracle and the GPU path decode."""
+    xf = x.float()
+    finite = torch.where(torch.isfinite(xf), xf.abs(), torch.zeros_like(xf))
+    amax = finite.amax(dim=(0, 1, 3)).clamp_min(1e-30)
+    scale = torch.exp2(torch.ceil(torch.log2(amax / 448.0)))
+    q8 = (xf / scale[None, None, :, None]).to(torch.float8_e4m3fn)
+    return q8.view(torch.uint8), scale.to(torch.float32)
