@@ -32,6 +32,7 @@ from workloads import CONFIGS, accept_tokens  # noqa: E402
 from workloads.generators import config_workload  # noqa: E402
 
 DEFAULT_WORKLOAD = "llama8b_64k"   # BASELINE.json configs[2]: "1/2/4/8 x B200"
+SCALE_WORKLOAD = "llama8b_128k_t128"  # BASELINE.json configs[4]: the >= 6x scaling target
 DATASHEET = {"hbm_gbs": 8000.0, "bf16_tflops": 2250.0}  # roof_DS, context only
 
 
@@ -219,6 +220,7 @@ def main():
     ap.add_argument("--impl", default="hta", choices=["hta", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-all-configs", action="store_true")
+    ap.add_argument("--no-scale-config", action="store_true", help="skip the 128k/T=128 step line")
     ap.add_argument("--ref-budget", type=float, default=60.0, help="seconds of oracle work for --impl reference")
     ap.add_argument("--force-seqpar", action="store_true",
                     help="run the sequence-parallel step (NCCL) even on one rank: checks the N > 1 code path "
@@ -239,6 +241,7 @@ def main():
     seqpar = ws > 1 or args.force_seqpar
     if seqpar:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "WARN")  # no banner on stdout: rank 0 prints ONE JSON line
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=ws)
@@ -253,7 +256,9 @@ def main():
     parents_h = w.parents[0].contiguous()
     draft_h, tgt_h, ctx = accept_tokens(parents_h, seed=0, vocab=32000, p_match=0.8)
     src = {"q": w.q, "kt": w.k_tree, "vt": w.v_tree, "parents": parents_h, "draft": draft_h, "tgt": tgt_h}
-    # per-step inputs packed in one pinned staging buffer (one H2D copy per end-to-end step)
+    # per-step inputs packed in one pinned staging buffer (one H2D copy per end-to-end step; split
+    # copies with the tree K/V overlapping the prefix pass (hta_forward_ex) measured slower: the
+    # event wait costs the tree/merge kernel its programmatic early launch)
     host_buf, host = packed({k: (v.shape, v.dtype) for k, v in src.items()}, "cpu")
     for k, v in src.items():
         host[k].copy_(v)
@@ -276,7 +281,7 @@ def main():
 
     side = torch.cuda.Stream(device=dev)
 
-    def step(x, events=None):
+    def step(x, events=None, tree_ready=None):
         """One verification step: a0 -> a1..a4 (a5) on the current stream; a6 (independent of
         the attention: it needs only the tree and the target's argmax) on a forked stream."""
         cur = torch.cuda.current_stream()
@@ -286,10 +291,12 @@ def main():
                                   path=path, path_len=plen, bonus=bonus)                    # a6
         hta.hta_build_tree_mask(x["parents"], mask)                                         # a0
         if seqpar:                                                                          # a1-a5
+            if tree_ready is not None:
+                cur.wait_event(tree_ready)
             comm.forward(x["q"], kc, vc, x["kt"], x["vt"], mask, cache_seqlens_local=sl, o=o, lse_out=lse, ws=wsb)
         else:                                                                               # a1-a4
             hta.hta_forward(x["q"], kc, vc, x["kt"], x["vt"], mask, cache_seqlens=sl, o=o, lse_out=lse, ws=wsb,
-                            events=events)
+                            events=events, tree_ready=tree_ready)
         cur.wait_stream(side)
 
     launches_per_step = 5 if seqpar else 4
@@ -312,7 +319,8 @@ def main():
 
     e2e_buf, e2e_in = packed({k: (v.shape, v.dtype) for k, v in src.items()}, dev)
     graphs = {}
-    if not seqpar:  # (NCCL calls of the sequence-parallel step are issued eagerly)
+    graph_note = "CUDA graph replay"
+    try:  # (NCCL supports stream capture; the sequence-parallel step is captured too)
         for name, fn in (("step", lambda: step(d_in)), ("e2e", e2e_body)):
             cs = torch.cuda.Stream(device=dev)
             cs.wait_stream(torch.cuda.current_stream())
@@ -327,6 +335,10 @@ def main():
         for _ in range(args.warmup):
             graphs["step"].replay()
             graphs["e2e"].replay()
+        torch.cuda.synchronize()
+    except RuntimeError as exc:  # capture refused: time the eager step instead (and say so)
+        graphs = {}
+        graph_note = f"eager (graph capture failed: {str(exc)[:80]})"
         torch.cuda.synchronize()
     run_step = graphs["step"].replay if "step" in graphs else (lambda: step(d_in))
     run_e2e = graphs["e2e"].replay if "e2e" in graphs else e2e_body
@@ -444,7 +456,7 @@ def main():
         "setup": {"parallelism": f"seq{ws}",
                   "l2": "flushed before every timed step (512 MiB write, then two reads of it; untimed)",
                   "step": ("a0 mask + hta_forward (a1-a4) | accept (a6) on a forked stream"
-                           + (" + NCCL exchange (a5)" if seqpar else "; CUDA graph replay"))},
+                           + (" + NCCL exchange (a5)" if seqpar else "") + "; " + graph_note)},
         "t_us": dist_us(times),
         "kernel_us": {"prefix": None if prefix_ms is None else prefix_ms * 1e3,
                       "tree_merge": None if tm_ms is None else tm_ms * 1e3,
@@ -456,9 +468,15 @@ def main():
         "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "t_us": dist_us(e2e_times),
                 "note": ("per-step inputs (q, tree K/V, parents, draft/target tokens) H2D as one copy from a pinned "
-                         "staging buffer, O + accepted path D2H as one copy; KV cache resident; CUDA graph")},
+                         "staging buffer, O + accepted path D2H as one copy; KV cache resident; " + graph_note)},
         "roofline": roof,
     }
+
+    # ---- the scaling config (BASELINE.json configs[4], 128k prefix / 128-token tree): the same
+    # step (sharded over the ranks for N > 1), so the driver's per-N runs also give its curve
+    if args.workload != SCALE_WORKLOAD and not args.no_scale_config:
+        line["scale_config"] = time_step_for(SCALE_WORKLOAD, dev, ws, rank, comm, flush, args, max_over_ranks,
+                                             barrier)
 
     # ---- commit of the accepted path's K/V rows into the cache (device, after
     # a6), timed on its own (L2 flushed); measured after the step timings since it writes rows
@@ -549,6 +567,10 @@ def main():
                     "cache; 16-row TMA boxes through the block table"}
         del kp, vp
 
+    # ---- the forward over an FP8 (E4M3) copy of the HBM-bound MHA config
+    if not seqpar and not args.no_all_configs:
+        line["next_rows"]["f4_fp8_kv"] = bench_fp8(dev, flush, k=max(5, args.steps // 5))
+
     # ---- cpu baseline (rank 0, N = 1 only): the oracle as it stands, bounded sample
     if rank == 0 and not seqpar and not args.no_cpu_baseline:
         import oracle
@@ -574,6 +596,115 @@ def main():
     if comm is not None:
         comm.close()
         torch.distributed.destroy_process_group()
+
+
+def time_step_for(name, dev, ws, rank, comm, flush, args, max_over_ranks, barrier):
+    """The verification step (a0 mask + hta_forward, or hta_forward_seqpar over this rank's
+    contiguous KV shard for N > 1) of another workload, graph-captured, L2 flushed before each
+    replay, CUDA events; max over ranks."""
+    from paper_2502_17421_b200 import hta
+    w = config_workload(name, seed=0)
+    lo, hi = hta.shard_bounds(w.N, ws, rank)
+    kc = w.k_cache[:, lo:hi].contiguous().to(dev)
+    vc = w.v_cache[:, lo:hi].contiguous().to(dev)
+    sl = torch.clamp(w.seqlens - lo, 0, hi - lo).to(torch.int32).to(dev)
+    x = {k: getattr(w, k).to(dev) for k in ("q", "k_tree", "v_tree")}
+    parents = w.parents[0].to(dev)
+    mask = torch.empty(w.T, w.T, dtype=torch.uint8, device=dev)
+    Hx = w.H // ws
+    o = torch.empty(w.B, w.T, Hx, w.d, dtype=w.torch_dtype, device=dev)
+    lse = torch.empty(w.B, Hx, w.T, dtype=torch.float32, device=dev)
+    shape = hta.make_shape(x["q"], k_cache=kc, k_tree=x["k_tree"])
+    wsb = (torch.empty(comm.workspace_size(shape), dtype=torch.uint8, device=dev) if comm is not None
+           else hta.new_workspace(shape, dev))
+
+    def fn():
+        hta.hta_build_tree_mask(parents, mask)
+        if comm is not None:
+            comm.forward(x["q"], kc, vc, x["k_tree"], x["v_tree"], mask, cache_seqlens_local=sl, o=o, lse_out=lse,
+                         ws=wsb)
+        else:
+            hta.hta_forward(x["q"], kc, vc, x["k_tree"], x["v_tree"], mask, cache_seqlens=sl, o=o, lse_out=lse, ws=wsb)
+
+    for _ in range(args.warmup):
+        fn()
+    torch.cuda.synchronize()
+    run = fn
+    try:
+        cs = torch.cuda.Stream(device=dev)
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            fn()
+        torch.cuda.current_stream().wait_stream(cs)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        run = g.replay
+    except RuntimeError:
+        torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        flush.view(torch.float32).sum()
+        flush.view(torch.float32).sum()
+        evs[i][0].record()
+        run()
+        evs[i][1].record()
+    torch.cuda.synchronize()
+    barrier()
+    t_ms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in evs))
+    del kc, vc, wsb
+    torch.cuda.empty_cache()
+    return {"workload": name, "us_per_step": t_ms * 1e3, "value": w.B * w.T / (t_ms * 1e-3), "unit": "tokens/s",
+            "n_gpus": ws, "keys_per_rank": hi - lo, "scaling": "strong",
+            "step": "a0 mask + " + ("hta_forward_seqpar (NCCL exchange)" if comm is not None else "hta_forward") +
+                    ("; CUDA graph" if run is not fn else "; eager")}
+
+
+def bench_fp8(dev, flush, k=10, name="longchat7b_16k"):
+    """hta_forward_fp8kv vs hta_forward on the same workload (E4M3 copy of its cache, per-head
+    scales), L2 flushed, CUDA events around each call; roofline on the FP8 bytes."""
+    from paper_2502_17421_b200 import hta
+    from workloads import fp8_cache
+    w = config_workload(name, seed=0)
+    k8, ks = fp8_cache(w.k_cache)
+    v8, vs = fp8_cache(w.v_cache)
+    x = {"q": w.q.to(dev), "kc": w.k_cache.to(dev), "vc": w.v_cache.to(dev), "kt": w.k_tree.to(dev),
+         "vt": w.v_tree.to(dev), "k8": k8.to(dev), "v8": v8.to(dev), "ks": ks.to(dev), "vs": vs.to(dev)}
+    mask = hta.hta_build_tree_mask(w.parents[0].to(dev))
+    shape = hta.make_shape(x["q"], k_cache=x["kc"], k_tree=x["kt"])
+    wsb = hta.new_workspace(shape, dev)
+    o, lse = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask, ws=wsb)
+    f8 = lambda: hta.hta_forward_fp8kv(x["q"], x["k8"], x["v8"], x["ks"], x["vs"], x["kt"], x["vt"], mask,  # noqa
+                                       o=o, lse_out=lse, ws=wsb)
+    b16 = lambda: hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask, o=o, lse_out=lse, ws=wsb)  # noqa
+    res = {}
+    for nm, fn in (("fp8", f8), ("bf16", b16)):
+        ts = []
+        for i in range(k + 3):
+            e = created_events(2)
+            flush.fill_(i & 0xFF)
+            flush.view(torch.float32).sum()
+            e[0].record()
+            fn()
+            e[1].record()
+            torch.cuda.synchronize()
+            if i >= 3:
+                ts.append(e[0].elapsed_time(e[1]) * 1e3)
+        res[nm] = statistics.mean(ts)
+    cfg = dict(CONFIGS[name])
+    kv8_bytes = 2 * cfg["B"] * cfg["N"] * cfg["H_kv"] * cfg["d"] * 1 + 2 * cfg["B"] * cfg["T"] * cfg["H"] * cfg["d"] * 2
+    pk = peaks()
+    t_roof = kv8_bytes / (pk["hbm_gbs"] * 1e9)
+    del x, o, lse, wsb
+    torch.cuda.empty_cache()
+    return {"workload": name, "us": res["fp8"], "bf16_us": res["bf16"], "roofline_us": t_roof * 1e6,
+            "frac_of_roofline": t_roof * 1e6 / res["fp8"], "bound": "hbm",
+            "note": "hta_forward_fp8kv (E4M3 cache, per-KV-head scales; tiles widened to f16 in shared memory by the "
+                    "producer warps) vs hta_forward on the bf16 cache; roofline on the E4M3 bytes + Q/O"}
 
 
 def bench_config(name, dev, flush, k=10):

@@ -154,6 +154,17 @@ hta_status_t hta_forward_timed(const hta_shape_t *shape, const void *q, const vo
                                size_t ws_bytes, hta_stream_t stream, void *ev_prefix_begin,
                                void *ev_prefix_end);
 
+/* hta_forward whose tree inputs arrive late: `tree_inputs_ready` (a cudaEvent_t, or NULL) is
+ * waited for on `stream` after the prefix kernel is enqueued and before the tree/merge kernel, so
+ * k_tree, v_tree and mask may still be in flight (e.g. copied from the host on another stream)
+ * while the prefix pass streams the cache -- only q and the cache gate the prefix.  Otherwise
+ * identical to hta_forward. */
+hta_status_t hta_forward_ex(const hta_shape_t *shape, const void *q, const void *k_cache,
+                            const void *v_cache, const int32_t *cache_seqlens, const void *k_tree,
+                            const void *v_tree, const uint8_t *mask, int64_t mask_batch_stride,
+                            void *o, float *lse_out, void *ws, size_t ws_bytes,
+                            hta_stream_t stream, void *tree_inputs_ready);
+
 /* hybrid_tree_attention over a PAGED KV cache (the block-table layout of
  * flash_attn_with_kvcache, for batched serving): as hta_forward (bf16 only), with
  *   k_pool, v_pool  bf16 [num_pages, page_size, H_kv, d] contiguous (the pages of all batches)

@@ -482,7 +482,7 @@ static hta_status_t forward_impl(const PagedArgs *pg, const hta_shape_t *shape, 
                                const int32_t *cache_seqlens, const void *k_tree, const void *v_tree,
                                const uint8_t *mask, int64_t mask_batch_stride, void *o, float *lse_out, void *ws,
                                size_t ws_bytes, hta_stream_t stream, void *ev_begin, void *ev_end,
-                               const Fp8Args *f8 = nullptr) {
+                               const Fp8Args *f8 = nullptr, void *tree_ready = nullptr) {
     Shape sh;
     hta_status_t r = check_shape(shape, &sh);
     if (r != HTA_OK) return r;
@@ -506,6 +506,10 @@ static hta_status_t forward_impl(const PagedArgs *pg, const hta_shape_t *shape, 
     r = run_prefix(sh, pl, q, k_cache, v_cache, cache_seqlens, o_ws, lse_ws, ostride, lstride, st, pg, f8);
     if (r != HTA_OK) return r;
     if (ev_end != nullptr && cudaEventRecord(static_cast<cudaEvent_t>(ev_end), st) != cudaSuccess)
+        return HTA_ERR_CUDA;
+    // the tree inputs (k_tree, v_tree, mask) may still be in flight on another stream: only the
+    // tree/merge kernel waits for them, the prefix kernel above does not
+    if (tree_ready != nullptr && cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(tree_ready), 0) != cudaSuccess)
         return HTA_ERR_CUDA;
     TreeMergeParams p = base_tm(sh);
     p.q = q;
@@ -534,6 +538,14 @@ hta_status_t hta_forward_timed(const hta_shape_t *shape, const void *q, const vo
                                size_t ws_bytes, hta_stream_t stream, void *ev_begin, void *ev_end) {
     return forward_impl(nullptr, shape, q, k_cache, v_cache, cache_seqlens, k_tree, v_tree, mask, mask_batch_stride, o,
                         lse_out, ws, ws_bytes, stream, ev_begin, ev_end);
+}
+
+hta_status_t hta_forward_ex(const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,
+                            const int32_t *cache_seqlens, const void *k_tree, const void *v_tree, const uint8_t *mask,
+                            int64_t mask_batch_stride, void *o, float *lse_out, void *ws, size_t ws_bytes,
+                            hta_stream_t stream, void *tree_inputs_ready) {
+    return forward_impl(nullptr, shape, q, k_cache, v_cache, cache_seqlens, k_tree, v_tree, mask, mask_batch_stride, o,
+                        lse_out, ws, ws_bytes, stream, nullptr, nullptr, nullptr, tree_inputs_ready);
 }
 
 hta_status_t hta_forward_paged(const hta_shape_t *shape, const void *q, const void *k_pool, const void *v_pool,

@@ -47,6 +47,8 @@ _SIG = {
                                    _P, ctypes.c_size_t, _P]),
     "hta_forward_timed": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, _P, _P, _P, ctypes.c_int64,
                                          _P, _P, _P, ctypes.c_size_t, _P, _P, _P]),
+    "hta_forward_ex": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, _P, _P, _P, ctypes.c_int64, _P, _P,
+                                      _P, ctypes.c_size_t, _P, _P]),
     "hta_forward_paged": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, _P, _P, ctypes.c_int32, ctypes.c_int32, _P,
                                          ctypes.c_int32, _P, _P, _P, _P, ctypes.c_int64, _P, _P, _P, ctypes.c_size_t,
                                          _P]),
@@ -236,10 +238,11 @@ def hta_merge_lse(o_parts, lse_parts, dtype=torch.bfloat16, o=None, lse_out=None
 
 def hta_forward(q, k_cache, v_cache, k_tree, v_tree, mask, cache_seqlens=None, o=None, lse_out=None, ws=None,
                 want_lse=True, scale=None, num_splits=0, max_seqlen=0, stream=None,
-                events=None) -> Tuple[torch.Tensor, Optional[torch.Tensor]]:
+                events=None, tree_ready=None) -> Tuple[torch.Tensor, Optional[torch.Tensor]]:
     """Full Hybrid Tree Attention of one layer: O [B,T,H,d] in q.dtype (+ LSE [B,H,T]).
     `events` = (begin, end) torch.cuda.Event pair recorded around the prefix kernel
-    (hta_forward_timed)."""
+    (hta_forward_timed); `tree_ready` = a torch.cuda.Event the tree/merge kernel waits for
+    (hta_forward_ex: k_tree / v_tree / mask may still be in flight during the prefix pass)."""
     shape = make_shape(q, k_cache=k_cache, k_tree=k_tree, scale=scale, num_splits=num_splits, max_seqlen=max_seqlen)
     B, T, H, d = q.shape
     mbs = 0 if mask.dim() == 2 else mask.stride(0)
@@ -248,7 +251,12 @@ def hta_forward(q, k_cache, v_cache, k_tree, v_tree, mask, cache_seqlens=None, o
         lse_out = torch.empty(B, H, T, dtype=torch.float32, device=q.device)
     ws_given = ws
     ws = _workspace(shape, q.device, ws)
-    if events is None:
+    if tree_ready is not None:
+        _check("hta_forward_ex", lib().hta_forward_ex(
+            ctypes.byref(shape), _ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(cache_seqlens), _ptr(k_tree),
+            _ptr(v_tree), _ptr(mask), mbs, _ptr(o), _ptr(lse_out), _ptr(ws), ws.numel() * ws.element_size(),
+            _stream(stream), ctypes.c_void_p(tree_ready.cuda_event)))
+    elif events is None:
         _check("hta_forward", lib().hta_forward(ctypes.byref(shape), _ptr(q), _ptr(k_cache), _ptr(v_cache),
                                                 _ptr(cache_seqlens), _ptr(k_tree), _ptr(v_tree), _ptr(mask), mbs,
                                                 _ptr(o), _ptr(lse_out), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))

@@ -1,6 +1,8 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times
-(default split plan), on rows sampled across every KV head, tree depth and batch; the oracle
-computes exactly those rows (fp64, explicit mask)."""
+(default split plan): every row of the headline config (Llama-8B-64k, 2048 rows), >= 1024 rows of
+QwQ-32k x 4 and of Llama-8B-128k/T=128, and rows sampled across every KV head, tree depth and batch
+for the other configs / distributions; the oracle computes exactly those rows (fp64, explicit
+mask, all host cores)."""
 import numpy as np
 import pytest
 import torch
@@ -16,6 +18,8 @@ pytestmark = pytest.mark.gpu
 
 
 def sample_rows(B, T, H, n, seed):
+    if n >= B * T * H:  # every row
+        return [(b, t, h) for b in range(B) for t in range(T) for h in range(H)]
     g = named_generator(seed, "rows")
     rows = {(0, 0, 0), (B - 1, T - 1, H - 1)}
     while len(rows) < n:
@@ -34,7 +38,9 @@ def test_config_full_size_sampled(cuda_device, name, dist):
     o, l = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], torch.from_numpy(mask).to(cuda_device),
                            cache_seqlens=x["sl"])
     torch.cuda.synchronize()
-    rows = sample_rows(w.B, w.T, w.H, 64 if w.N > 1000 else w.B * w.T * w.H, seed=1)
+    n_all = w.B * w.T * w.H
+    want = {"llama8b_64k": n_all, "qwq32b_32k_b4": 1024, "llama8b_128k_t128": 1024}.get(name, 64) if dist == "V1" else 64
+    rows = sample_rows(w.B, w.T, w.H, min(n_all, want) if w.N > 1000 else n_all, seed=1)
     ro, rl = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask, seqlens=w.seqlens, rows=rows)
     idx = torch.tensor(rows)
     og = o[idx[:, 0], idx[:, 1], idx[:, 2]]

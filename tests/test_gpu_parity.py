@@ -360,3 +360,29 @@ def test_max_seqlen_hint_plans_by_filled_length(cuda_device):
                                cache_seqlens=x["sl"], max_seqlen=hint)
         torch.cuda.synchronize()
         compare(o, l, o_ref, l_ref, "bf16", f"max_seqlen={hint}")
+
+
+def test_forward_ex_tree_inputs_late(cuda_device):
+    """hta_forward_ex: k_tree / v_tree / mask produced on another stream after the call is
+    enqueued; only the tree/merge kernel waits for them (the event), and the result equals
+    hta_forward's."""
+    w = make_workload(1, 64, 32, 8, 128, 3000, "bf16", dist="V1", seed=19, tree="beam")
+    mask_h = torch.from_numpy(oracle_masks(w)[0])
+    x = to_dev(w, cuda_device)
+    o_ref, l_ref = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask_h.to(cuda_device))
+    kt = torch.zeros_like(x["kt"])
+    vt = torch.zeros_like(x["vt"])
+    m = torch.zeros(64, 64, dtype=torch.uint8, device=cuda_device)
+    side = torch.cuda.Stream()
+    ready = torch.cuda.Event()
+    torch.cuda.synchronize()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(2_000_000)  # the tree inputs land well after the prefix pass started
+        kt.copy_(x["kt"])
+        vt.copy_(x["vt"])
+        m.copy_(mask_h.to(cuda_device))
+        ready.record()
+    o, l = hta.hta_forward(x["q"], x["kc"], x["vc"], kt, vt, m, tree_ready=ready)
+    torch.cuda.synchronize()
+    assert torch.equal(o, o_ref) and torch.equal(l, l_ref)

@@ -38,3 +38,35 @@ def test_seqpar_one_rank_vs_oracle(cuda_device, comm, case, gather):
                         cache_seqlens_local=x["sl"], gather_output=gather)
     torch.cuda.synchronize()
     compare(o, l, o_ref, l_ref, "bf16", f"seqpar P=1 gather={gather}")
+
+
+def test_seqpar_step_in_cuda_graph(cuda_device, comm):
+    """The sequence-parallel step (prefix -> split combine -> NCCL exchange -> merge) captured as a
+    CUDA graph (NCCL supports stream capture) replays to the eager result, bit for bit."""
+    w = make_workload(1, 64, 32, 8, 128, 4000, "bf16", dist="V1", seed=8, tree="beam")
+    mask = torch.from_numpy(oracle_masks(w)).to(cuda_device)
+    x = to_dev(w, cuda_device)
+    o_e, l_e = comm.forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask, cache_seqlens_local=x["sl"],
+                            gather_output=True)
+    torch.cuda.synchronize()
+    o = torch.zeros_like(o_e)
+    lse = torch.zeros_like(l_e)
+    shape = hta.make_shape(x["q"], k_cache=x["kc"], k_tree=x["kt"])
+    ws = torch.empty(comm.workspace_size(shape), dtype=torch.uint8, device=cuda_device)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        comm.forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask, cache_seqlens_local=x["sl"], gather_output=True,
+                     o=o, lse_out=lse, ws=ws)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        comm.forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask, cache_seqlens_local=x["sl"], gather_output=True,
+                     o=o, lse_out=lse, ws=ws)
+    o.zero_()
+    lse.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(o, o_e) and torch.equal(lse, l_e)
+    assert not comm.async_error()
