@@ -120,50 +120,61 @@ constexpr int kL2Ahead = HTA_L2_AHEAD;  // FP8 cache: tiles prefetched into L2 b
 // the sequence end, Z13).  Rows are converted in ascending order, each row within one warp
 // instruction, and f16 row r never overlaps an E4M3 row beyond r: nothing is overwritten before it
 // is read.  E4M3 -> f16 is exact.
+// The loads of a batch of kWidenUnroll chunk rows are issued before any of its stores (one shared
+// memory round trip per batch; written out explicitly because the compiler cannot reorder the loads
+// above stores that may alias them).  That is safe: the f16 rows a batch writes overlap only E4M3
+// rows of the same batch or earlier ones (f16 row r covers E4M3 rows <= r in both slot shapes).
 template <int kRowBytes, int kRows>
 __device__ __forceinline__ void widen_e4m3_tile(uint8_t *slot, int lane, int valid) {
     constexpr int kChunks = kRowBytes / 16;  // 16-byte E4M3 chunks per row
     constexpr int kSlotBytes = kRows * kRowBytes * 2;
+    constexpr int kIters = kRows * kChunks / 32;
+    static_assert(kIters % kWidenUnroll == 0, "widen batches");
     const uint8_t *src = slot + kSlotBytes / 2;
-#pragma unroll kWidenUnroll
-    for (int base = 0; base < kRows * kChunks; base += 32) {
-        const int idx = base + lane;
-        const int r = idx / kChunks, c = idx % kChunks;
-        const uint4 x = *reinterpret_cast<const uint4 *>(src + r * kRowBytes + c * 16);
-        uint4 y0, y1;
-        y0.x = e4m3x2_to_f16x2(static_cast<uint16_t>(x.x));
-        y0.y = e4m3x2_to_f16x2(static_cast<uint16_t>(x.x >> 16));
-        y0.z = e4m3x2_to_f16x2(static_cast<uint16_t>(x.y));
-        y0.w = e4m3x2_to_f16x2(static_cast<uint16_t>(x.y >> 16));
-        y1.x = e4m3x2_to_f16x2(static_cast<uint16_t>(x.z));
-        y1.y = e4m3x2_to_f16x2(static_cast<uint16_t>(x.z >> 16));
-        y1.z = e4m3x2_to_f16x2(static_cast<uint16_t>(x.w));
-        y1.w = e4m3x2_to_f16x2(static_cast<uint16_t>(x.w >> 16));
-        if (r >= valid) y0 = y1 = make_uint4(0u, 0u, 0u, 0u);
-        const int e0 = c * 16;
-        const int ch = (e0 % 64) / 8;  // even: the first of the two 16-byte f16 chunks
-        uint8_t *row = slot + (e0 / 64) * (kRows * 128) + r * 128;
-        *reinterpret_cast<uint4 *>(row + ((ch ^ (r & 7)) << 4)) = y0;
-        *reinterpret_cast<uint4 *>(row + (((ch + 1) ^ (r & 7)) << 4)) = y1;
+#pragma unroll 1
+    for (int it0 = 0; it0 < kIters; it0 += kWidenUnroll) {
+        uint4 x[kWidenUnroll];
+#pragma unroll
+        for (int u = 0; u < kWidenUnroll; ++u) {
+            const int idx = (it0 + u) * 32 + lane;
+            x[u] = *reinterpret_cast<const uint4 *>(src + (idx / kChunks) * kRowBytes + (idx % kChunks) * 16);
+        }
+#pragma unroll
+        for (int u = 0; u < kWidenUnroll; ++u) {
+            const int idx = (it0 + u) * 32 + lane;
+            const int r = idx / kChunks, c = idx % kChunks;
+            uint4 y0, y1;
+            y0.x = e4m3x2_to_f16x2(static_cast<uint16_t>(x[u].x));
+            y0.y = e4m3x2_to_f16x2(static_cast<uint16_t>(x[u].x >> 16));
+            y0.z = e4m3x2_to_f16x2(static_cast<uint16_t>(x[u].y));
+            y0.w = e4m3x2_to_f16x2(static_cast<uint16_t>(x[u].y >> 16));
+            y1.x = e4m3x2_to_f16x2(static_cast<uint16_t>(x[u].z));
+            y1.y = e4m3x2_to_f16x2(static_cast<uint16_t>(x[u].z >> 16));
+            y1.z = e4m3x2_to_f16x2(static_cast<uint16_t>(x[u].w));
+            y1.w = e4m3x2_to_f16x2(static_cast<uint16_t>(x[u].w >> 16));
+            if (r >= valid) y0 = y1 = make_uint4(0u, 0u, 0u, 0u);
+            const int e0 = c * 16;
+            const int ch = (e0 % 64) / 8;  // even: the first of the two 16-byte f16 chunks
+            uint8_t *row = slot + (e0 / 64) * (kRows * 128) + r * 128;
+            *reinterpret_cast<uint4 *>(row + ((ch ^ (r & 7)) << 4)) = y0;
+            *reinterpret_cast<uint4 *>(row + (((ch + 1) ^ (r & 7)) << 4)) = y1;
+        }
     }
 }
 
 // Register split between the producer/MMA warpgroup and the softmax warpgroups (640 threads launch
-// at 96 registers each): 32 / 112 for the bf16 cache; the FP8 cache's producers widen tiles and
-// get more (HTA_KV8_REGS: 48 / 104).
-#ifndef HTA_KV8_REGS
-#define HTA_KV8_REGS 48
-#endif
+// at 96 registers each): 32 / 112 for the bf16 cache; the FP8 cache's producers widen tiles in
+// batches and get more: 64 / 104 (4 x 32 x 64 + 16 x 32 x 104 <= 64 K registers).
 template <bool KV8>
 __device__ __forceinline__ void setmaxnreg_dec() {
-    if constexpr (KV8 && HTA_KV8_REGS == 48)
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
+    if constexpr (KV8)
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
     else
         asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
 }
 template <bool KV8>
 __device__ __forceinline__ void setmaxnreg_inc() {
-    if constexpr (KV8 && HTA_KV8_REGS == 48)
+    if constexpr (KV8)
         asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
     else
         asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");

@@ -109,6 +109,19 @@ def main():
         if mma[2]:
             s_is = [rel(mma[2][j]) for j in sorted(mma[2])]
             print(f"     S issues: first {s_is[0]}, K_0..2 landed at {s_is[:3]}")
+    # FP8 cache producers: 30 -> 32 = K tile landed -> widened (warp of the K ring), 31 -> 33 (V)
+    for a, b_, nm in ((30, 32, "K"), (31, 33, "V")):
+        for wi in range(32):
+            if (wi, b_) not in ev:
+                continue
+            st, en = ev[(wi, a)], ev[(wi, b_)]
+            js = sorted(j for j in en if j in st)
+            if not js:
+                continue
+            dur = [en[j] - st[j] for j in js]
+            per = [en[y] - en[x] for x, y in zip(js, js[1:])]
+            print(f"producer warp {wi} ({nm}): {len(js)} tiles widened; landed->widened median "
+                  f"{statistics.median(dur):.0f}, widened period median {statistics.median(per) if per else 0:.0f}")
     for wi in sm:
         ten = ev.get((wi, 10), {})
         if not ten:
