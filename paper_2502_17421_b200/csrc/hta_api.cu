@@ -104,8 +104,10 @@ int best_splits(int ctas, int n_tiles, int num_sms, double *cost_out) {
     return S;
 }
 
-// Split-KV work plan.
-PrefixPlan make_plan(const Shape &sh, int num_sms) {
+// Split-KV work plan.  tree_tiles: masked tree tiles the
+// last split of every unit appends (fused tree pass of hta_forward); they are planned as tiles of
+// the key range like the cache tiles, so the last split carries correspondingly fewer cache tiles.
+PrefixPlan make_plan(const Shape &sh, int num_sms, int tree_tiles = 0) {
     const hta_shape_t &s = sh.s;
     PrefixPlan pl{};
     pl.G = sh.G;
@@ -114,7 +116,7 @@ PrefixPlan make_plan(const Shape &sh, int num_sms) {
     // the filled length bound (max_seqlen) plans the schedule; the last split still runs to each
     // batch entry's own length
     const int64_t n_plan = (s.max_seqlen > 0 && s.max_seqlen < s.N_max) ? s.max_seqlen : s.N_max;
-    pl.n_tiles = static_cast<int>((n_plan + blk - 1) / blk);
+    pl.n_tiles = static_cast<int>((n_plan + blk - 1) / blk) + (s.dtype == HTA_BF16 ? tree_tiles : 0);
     int S = 1;
     if (s.dtype == HTA_BF16) {
         // More than 128 rows per KV head: CTA pairs (cta_group::2, 256 rows per pair), unless
@@ -215,6 +217,29 @@ bool make_q_map(CUtensorMap *map, const void *q, const hta_shape_t &s, int G) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Tree tiles of the fused tree pass (hta_forward, bf16, T <= 256): ceil(T / 128).
+int fused_tree_tiles(const hta_shape_t &s) {
+    return s.dtype == HTA_BF16 && s.T >= 1 && s.T <= 256 ? (s.T + kBlockN - 1) / kBlockN : 0;
+}
+
+// 4-D map over k_tree / v_tree [B, T, H_kv, d] (tkv_strides): box = 64 x 1 x box_rows x 1, 128B
+// swizzle, rows past T zero-filled.  false when the strides are not 16-byte multiples (the tree
+// pass then runs in the tree/merge kernel).
+bool make_tree_map(CUtensorMap *map, const void *base, const hta_shape_t &s, int box_rows) {
+    for (int i = 0; i < 3; ++i)
+        if ((s.tkv_strides[i] * 2) % 16 != 0) return false;
+    EncodeTiledFn enc = encode_fn();
+    if (enc == nullptr) return false;
+    cuuint64_t dims[4] = {cuuint64_t(s.d), cuuint64_t(s.H_kv), cuuint64_t(s.T), cuuint64_t(s.B)};
+    cuuint64_t strides[3] = {cuuint64_t(s.tkv_strides[2] * 2), cuuint64_t(s.tkv_strides[1] * 2),
+                             cuuint64_t(s.tkv_strides[0] * 2)};
+    cuuint32_t box[4] = {64, 1, cuuint32_t(box_rows), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Paged KV cache: a contiguous pool [num_pages, page_size, H_kv, d] and a
 // block table [B][max_pages] of page indices.
 struct PagedArgs {
@@ -261,11 +286,19 @@ struct Fp8Args {
     const float *k_scale, *v_scale;
 };
 
+// Fused tree pass arguments of the prefix pass (tree_tiles = 0: none).
+struct TreeArgs {
+    int tree_tiles;
+    const uint8_t *mask;
+    int64_t mask_bs;
+    CUtensorMap tkt, tvt;
+};
+
 // Enqueue the prefix pass writing `splits` partials at (o_out, lse_out) with the given strides.
 hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, const void *k, const void *v,
                         const int32_t *seqlens, float *o_out, float *lse_out, int64_t o_split_stride,
                         int64_t lse_split_stride, cudaStream_t st, const PagedArgs *pg = nullptr,
-                        const Fp8Args *f8 = nullptr) {
+                        const Fp8Args *f8 = nullptr, const TreeArgs *tr = nullptr) {
     const hta_shape_t &s = sh.s;
     PrefixParams p{};
     if (f8 != nullptr) {
@@ -328,7 +361,16 @@ hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, co
         std::memset(&tq, 0, sizeof(tq));
         // the FP8 variant stages Q with plain loads (converting it to f16 on the way)
         p.q_tma = f8 == nullptr && make_q_map(&tq, q, s, sh.G) ? 1 : 0;
-        e = launch_prefix_tc(p, tq, tk, tv, prefix_tc_smem_bytes(s.d, pl.nt), st);
+        CUtensorMap none;
+        std::memset(&none, 0, sizeof(none));
+        if (tr != nullptr && tr->tree_tiles > 0) {
+            p.tree_tiles = tr->tree_tiles;
+            p.mask = tr->mask;
+            p.mask_bs = tr->mask_bs;
+        }
+        const bool fused = p.tree_tiles > 0;
+        e = launch_prefix_tc(p, tq, tk, tv, fused ? tr->tkt : none, fused ? tr->tvt : none,
+                             prefix_tc_smem_bytes(s.d, pl.nt), st);
     } else {
         e = launch_prefix_simt(p, st);
     }
@@ -388,8 +430,10 @@ int32_t hta_version(void) { return 100; }
 size_t hta_workspace_size(const hta_shape_t *shape, int32_t num_sms) {
     Shape sh;
     if (check_shape(shape, &sh) != HTA_OK) return size_t(-1);
-    const PrefixPlan pl = make_plan(sh, num_sms > 0 ? num_sms : kDefaultSms);
-    return size_t(pl.splits) * part_floats(sh.s) * sizeof(float);
+    const int sms = num_sms > 0 ? num_sms : kDefaultSms;
+    // the larger of the plans with and without the fused tree tiles (hta_forward uses the latter)
+    const int splits = std::max(make_plan(sh, sms).splits, make_plan(sh, sms, fused_tree_tiles(sh.s)).splits);
+    return size_t(splits) * part_floats(sh.s) * sizeof(float);
 }
 
 hta_status_t hta_prefix_attn(const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,
@@ -493,7 +537,24 @@ static hta_status_t forward_impl(const PagedArgs *pg, const hta_shape_t *shape, 
         !is_aligned(v_tree, 16) || !is_aligned(o, 16))
         return HTA_ERR_INVALID_ARGUMENT;
     if ((r = check_device()) != HTA_OK) return r;
-    const PrefixPlan pl = make_plan(sh, device_sms());
+    // The tree pass runs inside the prefix kernel (masked tree tiles appended to the last split of
+    // every unit) for single-CTA row groups; it stays in the tree/merge kernel
+    // beside the merge for CTA pairs (there the tree tile costs the pair kernel about what the
+    // separate tree pass costs the tail: Llama-8B-64k 69.2 vs 69.6 us, 128k 217.7 vs 217.6 us),
+    // for an FP8 cache, when the tree inputs arrive late on another stream (tree_ready), and when
+    // k_tree / v_tree cannot be described by a tensor map.
+    TreeArgs tr{};
+    PrefixPlan pl = make_plan(sh, device_sms());
+    if (f8 == nullptr && tree_ready == nullptr && fused_tree_tiles(s) > 0) {
+        const PrefixPlan plt = make_plan(sh, device_sms(), fused_tree_tiles(s));
+        if (plt.nt == 1 && make_tree_map(&tr.tkt, k_tree, s, kBlockN) &&
+            make_tree_map(&tr.tvt, v_tree, s, kBlockN)) {
+            tr.tree_tiles = fused_tree_tiles(s);
+            tr.mask = mask;
+            tr.mask_bs = mask_batch_stride;
+            pl = plt;
+        }
+    }
     const size_t need = size_t(pl.splits) * part_floats(s) * sizeof(float);
     if (ws == nullptr || ws_bytes < need || !is_aligned(ws, 16)) return HTA_ERR_WORKSPACE;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -503,7 +564,7 @@ static hta_status_t forward_impl(const PagedArgs *pg, const hta_shape_t *shape, 
     const int64_t lstride = int64_t(s.B) * s.H * s.T;
     if (ev_begin != nullptr && cudaEventRecord(static_cast<cudaEvent_t>(ev_begin), st) != cudaSuccess)
         return HTA_ERR_CUDA;
-    r = run_prefix(sh, pl, q, k_cache, v_cache, cache_seqlens, o_ws, lse_ws, ostride, lstride, st, pg, f8);
+    r = run_prefix(sh, pl, q, k_cache, v_cache, cache_seqlens, o_ws, lse_ws, ostride, lstride, st, pg, f8, &tr);
     if (r != HTA_OK) return r;
     if (ev_end != nullptr && cudaEventRecord(static_cast<cudaEvent_t>(ev_end), st) != cudaSuccess)
         return HTA_ERR_CUDA;
@@ -517,7 +578,7 @@ static hta_status_t forward_impl(const PagedArgs *pg, const hta_shape_t *shape, 
     p.vt = v_tree;
     p.mask = mask;
     p.mask_bs = mask_batch_stride;
-    p.do_tree = 1;
+    p.do_tree = tr.tree_tiles > 0 ? 0 : 1;  // (fused: the partials already hold the tree part)
     p.n_parts = pl.splits;
     p.o_parts = o_ws;
     p.lse_parts = lse_ws;

@@ -51,6 +51,13 @@ struct PrefixParams {
     // V = v_scale[g] * E4M3 per KV head g (device float [H_kv]); the maps load E4M3 tiles.
     int kv8;
     const float *k_scale, *v_scale;
+    // Fused tree pass (hta_forward, bf16 cache): the last split of every unit appends tree_tiles
+    // (= ceil(T / 128)) masked tiles of the tree keys (tmap_kt / tmap_vt over k_tree / v_tree) to
+    // its cache tiles, so its partial already holds the tree part (the Appendix C merge applied
+    // inside the online softmax).  Row r of token t sees tree key s iff mask[b*mask_bs + t*T + s].
+    int tree_tiles;
+    const uint8_t *mask;
+    int64_t mask_bs;
     float *o_out;                     // [S][B][T][H][d] fp32, normalised partials
     float *lse_out;                   // [S][B][H][T] natural-log LSE
     int64_t o_split_stride, lse_split_stride;  // elements between splits
@@ -83,7 +90,8 @@ struct TreeMergeParams {
 
 // Launchers (return cudaGetLastError() of the launch).
 cudaError_t launch_prefix_tc(const PrefixParams &p, const CUtensorMap &tmap_q, const CUtensorMap &tmap_k,
-                             const CUtensorMap &tmap_v, int smem_bytes, cudaStream_t s);
+                             const CUtensorMap &tmap_v, const CUtensorMap &tmap_kt, const CUtensorMap &tmap_vt,
+                             int smem_bytes, cudaStream_t s);
 int prefix_tc_smem_bytes(int d, int nt);
 cudaError_t launch_prefix_simt(const PrefixParams &p, cudaStream_t s);
 cudaError_t launch_tree_merge(const TreeMergeParams &p, int d, hta_dtype_t in_dtype, hta_dtype_t out_dtype,

@@ -162,6 +162,50 @@ __device__ __forceinline__ void widen_e4m3_tile(uint8_t *slot, int lane, int val
     }
 }
 
+// Mask bits of the fused tree pass for one 32-key chunk: bit i = mask byte base + i of the row is
+// nonzero (bytes >= T read as 0).  16-byte loads when the row is 16-byte aligned (T % 16 == 0),
+// else byte loads; never past byte T - 1.
+__device__ __forceinline__ uint32_t tree_chunk_bits(const uint8_t *mrow, int T, int base) {
+    uint32_t bits = 0u;
+    if (((reinterpret_cast<uintptr_t>(mrow) | static_cast<uintptr_t>(T)) & 15u) == 0) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            if (base + 16 * q >= T) break;
+            const uint4 v = *reinterpret_cast<const uint4 *>(mrow + base + 16 * q);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t nz = __vcmpne4(w[e], 0u);  // 0xFF per nonzero byte
+                const uint32_t b4 = (nz & 1u) | ((nz >> 7) & 2u) | ((nz >> 14) & 4u) | ((nz >> 21) & 8u);
+                bits |= b4 << (16 * q + 4 * e);
+            }
+        }
+    } else {
+        for (int i = 0; i < 32 && base + i < T; ++i)
+            if (mrow[base + i] != 0) bits |= 1u << i;
+    }
+    return bits;
+}
+
+// Fused tree pass: set S to -inf in TMEM for the keys of a tree tile the row's mask hides.  The
+// calling thread's 64 S values of the tile (two 32-column chunks, 16x32bx2 shape, half offset 64)
+// start at TMEM address `at`; mrow = the row's mask bytes (nullptr: a padding row, all hidden),
+// k0 = the tree key of the first of the 64 columns.  Not inlined: keeps the softmax loop's
+// schedule independent of this rarely taken path.
+__device__ __noinline__ void mask_tree_tile(uint32_t at, const uint8_t *mrow, int T, int k0) {
+#pragma unroll 1
+    for (int ch = 0; ch < 2; ++ch) {
+        float sm[32];
+        tmem_ld_x32_nowait<64>(at + ch * 32, sm);
+        tmem_ld_wait_fence<32>(sm);
+        const uint32_t bits = mrow != nullptr ? tree_chunk_bits(mrow, T, k0 + ch * 32) : 0u;
+#pragma unroll
+        for (int cc = 0; cc < 32; ++cc)
+            if (!((bits >> cc) & 1u)) sm[cc] = -INFINITY;
+        tmem_st_16x32_split<64>(at + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(sm));
+    }
+}
+
 // Register split between the producer/MMA warpgroup and the softmax warpgroups (640 threads launch
 // at 96 registers each): 32 / 112 for the bf16 cache; the FP8 cache's producers widen tiles in
 // batches and get more: 64 / 104 (4 x 32 x 64 + 16 x 32 x 104 <= 64 K registers).
@@ -242,10 +286,13 @@ __device__ __forceinline__ int paged_row(const PrefixParams &p, int b, int k) {
     return e * p.page_size + k % p.page_size;
 }
 
-template <int D, bool PAIR, bool KV8>
+// TREE: the fused tree pass (tree tiles appended to the last split); the kernels without it carry
+// none of its code, so their schedule is exactly that of the plain prefix pass.
+template <int D, bool PAIR, bool KV8, bool TREE>
 __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     prefix_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
-                     const __grid_constant__ CUtensorMap tmap_v, const PrefixParams p) {
+                     const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ CUtensorMap tmap_kt,
+                     const __grid_constant__ CUtensorMap tmap_vt, const PrefixParams p) {
     using C = TcCfg<D, PAIR>;
     using Spec = SpecCfg<KV8>;
     extern __shared__ __align__(1024) uint8_t smem[];  // 128B-swizzled tiles need 1024B alignment
@@ -300,6 +347,10 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         if (p.q_tma) tma_prefetch_desc(&tmap_q);
         tma_prefetch_desc(&tmap_k);
         tma_prefetch_desc(&tmap_v);
+        if (TREE) {
+            tma_prefetch_desc(&tmap_kt);
+            tma_prefetch_desc(&tmap_vt);
+        }
     }
     if (warp == kWarpMma && lane == 0) {
         // the FP8 variant fills a slot by widening in place: its full barrier counts one arrival per
@@ -354,11 +405,13 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     const int64_t key_lo = static_cast<int64_t>(split) * p.tiles_per_split * kBlockN;
     int64_t key_hi = key_lo + static_cast<int64_t>(p.tiles_per_split) * kBlockN;
     if (key_hi > n_b || split == p.splits - 1) key_hi = n_b;  // the last split runs to the length
-    const int n_tiles = key_hi > key_lo ? static_cast<int>((key_hi - key_lo + kBlockN - 1) / kBlockN) : 0;
+    // nc cache tiles, then (last split, fused tree pass) the tree tiles: tiles j >= nc
+    const int nc = key_hi > key_lo ? static_cast<int>((key_hi - key_lo + kBlockN - 1) / kBlockN) : 0;
+    const int n_tiles = nc + (TREE && split == p.splits - 1 ? p.tree_tiles : 0);
     const int row0 = mg * kRowsPerTile * (PAIR ? 2 : 1) + static_cast<int>(rank) * kRowsPerTile;
-    // the last tile of a split that ends at the sequence end may hold garbage rows (Z13)
-    const int tail_valid = static_cast<int>(key_hi - (key_lo + static_cast<int64_t>(n_tiles - 1) * kBlockN));
-    const bool tail_zero = n_tiles > 0 && tail_valid < kBlockN && key_hi == n_b && n_b < p.N_max;
+    // the last cache tile of a split that ends at the sequence end may hold garbage rows (Z13)
+    const int tail_valid = static_cast<int>(key_hi - (key_lo + static_cast<int64_t>(nc - 1) * kBlockN));
+    const bool tail_zero = nc > 0 && tail_valid < kBlockN && key_hi == n_b && n_b < p.N_max;
 
     float *o_base = p.o_out + static_cast<int64_t>(split) * p.o_split_stride;
     float *lse_base = p.lse_out + static_cast<int64_t>(split) * p.lse_split_stride;
@@ -397,6 +450,20 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 }
             }
             const uint32_t kfull0 = PAIR ? mapa_shared(smem_u32(&k_full[0]), 0) : 0u;
+            // tree tile jt of the fused tree pass: keys [jt*128, +128) of k_tree (rows past T are
+            // zero-filled by TMA and masked); a CTA of a pair loads its 64-key half
+            auto load_tree_k = [&](uint8_t *dst, uint32_t bar_pair, uint64_t *bar, int jt) {
+                const int r0 = jt * kBlockN + (PAIR ? static_cast<int>(rank) * C::kKRows : 0);
+#pragma unroll
+                for (int kb = 0; kb < C::kKB; ++kb) {
+                    if (PAIR)
+                        tma_load_4d_pair(dst + kb * (C::kKRows * 128), &tmap_kt, bar_pair, kb * 64, g, r0, b,
+                                         kPolicyEvictNormal);
+                    else
+                        tma_load_4d(dst + kb * (C::kKRows * 128), &tmap_kt, bar, kb * 64, g, r0, b,
+                                    kPolicyEvictNormal);
+                }
+            };
             if constexpr (KV8) {
                 // FP8 cache: the whole warp loads E4M3 tiles kLead tiles ahead (lane 0 issues the
                 // TMA into the upper half of the f16 slot) and widens tile j in place, then signals
@@ -456,6 +523,10 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                             mbar_arrive_expect_tx(&k_full[slot], C::kKBytes);
                         }
                     }
+                    if (TREE && j >= nc) {  // a tree tile: the tree K map (not paged)
+                        if (lane == 0) load_tree_k(dst, kfull0 + 8u * slot, &k_full[slot], j - nc);
+                        continue;
+                    }
 #pragma unroll
                     for (int i = 0; i < kBoxes; ++i) {
                         const int r = __shfl_sync(0xffffffffu, prow, i);
@@ -479,6 +550,15 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);
                     HTA_TR(30, j);
                     uint8_t *dst = sK + slot * C::kKBytes;
+                    if (TREE && j >= nc) {  // a tree tile
+                        if (PAIR) {
+                            if (leader) mbar_arrive_expect_tx(&k_full[slot], 2u * C::kKBytes);
+                        } else {
+                            mbar_arrive_expect_tx(&k_full[slot], C::kKBytes);
+                        }
+                        load_tree_k(dst, kfull0 + 8u * slot, &k_full[slot], j - nc);
+                        continue;
+                    }
                     if (PAIR) {
                         if (leader) mbar_arrive_expect_tx(&k_full[slot], 2u * C::kKBytes);
 #pragma unroll
@@ -527,7 +607,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     __syncwarp();
                     HTA_TR(31, j);
                     widen_e4m3_tile<C::kVCols, kBlockN>(sV + slot * C::kVBytes, lane,
-                                                        (tail_zero && j == n_tiles - 1) ? tail_valid : kBlockN);
+                                                        (tail_zero && j == nc - 1) ? tail_valid : kBlockN);
                     fence_proxy_async_smem();
                     __syncwarp();
                     HTA_TR(33, j);
@@ -565,18 +645,36 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     for (int kb = 0; kb < C::kKB; ++kb)
                         tma_load_4d_bar(dst + kb * (kBlockN * 128), &tmap_v, bar, kb * 64, g, r, bb, kKvPolicy);
             };
+            // tree tile jt of the fused tree pass: all 128 keys (rows past T zero-filled by TMA)
+            auto load_tree_v = [&](uint8_t *dst, uint32_t bar, int jt) {
+                if (PAIR)
+                    tma_load_4d_pair(dst, &tmap_vt, bar, static_cast<int>(rank) * 64, g, jt * kBlockN, b,
+                                     kPolicyEvictNormal);
+                else
+#pragma unroll
+                    for (int kb = 0; kb < C::kKB; ++kb)
+                        tma_load_4d_bar(dst + kb * (kBlockN * 128), &tmap_vt, bar, kb * 64, g, jt * kBlockN, b,
+                                        kPolicyEvictNormal);
+            };
+            // (the tail tile is sanitised after the loop; the tree tiles after it are issued first,
+            // which needs no slot the tail tile's PV must free: kSlotsV > 2 >= tree tiles)
+            static_assert(C::kSlotsV >= 3, "tree tiles are issued before the tail tile is sanitised");
             if (p.page_size > 0) {
                 constexpr int kBoxes = kBlockN / 16;
                 for (int j = 0; j < n_tiles; ++j) {
                     const int n0 = static_cast<int>(key_lo) + j * kBlockN;
                     const int prow = paged_row(p, b, n0 + 16 * (lane < kBoxes ? lane : 0));
                     const int slot = j % C::kSlotsV;
-                    const bool tail = tail_zero && j == n_tiles - 1;
+                    const bool tail = tail_zero && j == nc - 1;
                     mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
                     __syncwarp();
                     HTA_TR(31, j);
                     uint8_t *dst = sV + slot * C::kVBytes;
                     if (lane == 0) v_expect(slot, tail);
+                    if (TREE && j >= nc) {
+                        if (lane == 0) load_tree_v(dst, v_bar(j, slot, false), j - nc);
+                        continue;
+                    }
 #pragma unroll
                     for (int i = 0; i < kBoxes; ++i) {
                         const int r = __shfl_sync(0xffffffffu, prow, i);
@@ -587,18 +685,21 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 for (int j = 0; j < n_tiles; ++j) {
                     const int n0 = static_cast<int>(key_lo) + j * kBlockN;
                     const int slot = j % C::kSlotsV;
-                    const bool tail = tail_zero && j == n_tiles - 1;
+                    const bool tail = tail_zero && j == nc - 1;
                     mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
                     HTA_TR(31, j);
                     v_expect(slot, tail);
-                    v_load(sV + slot * C::kVBytes, v_bar(j, slot, tail), tail, n0, b);
+                    if (TREE && j >= nc)
+                        load_tree_v(sV + slot * C::kVBytes, v_bar(j, slot, false), j - nc);
+                    else
+                        v_load(sV + slot * C::kVBytes, v_bar(j, slot, tail), tail, n0, b);
                 }
             }
             __syncwarp();
             if (tail_zero) {
                 mbar_wait(v_tail_land, 0);
                 __syncwarp();
-                uint8_t *vt = sV + ((n_tiles - 1) % C::kSlotsV) * C::kVBytes;
+                uint8_t *vt = sV + ((nc - 1) % C::kSlotsV) * C::kVBytes;
                 constexpr int kAtoms = C::kVCols / 64;  // 128-byte column atoms per key row
                 const int n_chunks = (kBlockN - tail_valid) * kAtoms * 8;  // 16-byte chunks to zero
                 for (int i = lane; i < n_chunks; i += 32) {
@@ -667,7 +768,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             __syncwarp();
             for (int jj = 0; jj < C::kSBufs && jj < n_tiles; ++jj) start_S(jj);
             for (int j = 0; j < n_tiles; ++j) {
-                if (!KV8 && tail_zero && j == n_tiles - 1) {  // the V producers sanitised this tile
+                if (!KV8 && tail_zero && j == nc - 1) {  // the V producers sanitised this tile
                     if (PAIR)
                         mbar_wait_cluster(v_tail_ready, 0);
                     else
@@ -767,6 +868,12 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         // m_run: the row's running max (log2 units) as last known to this group; the group's row
         // sum l_run (this thread's columns of the group's tiles) is expressed in the scale m_run.
         float m_run = -INFINITY, l_run = 0.f;
+        // Fused tree pass: the row's mask bytes are prefetched into L1 now and read as bits when
+        // the tree tile comes up (no registers held across the cache tiles).
+        // (the row's mask bytes, recomputed where used: nothing held across the cache tiles)
+        auto mask_row = [&]() { return p.mask + b * p.mask_bs + static_cast<int64_t>(grow / p.G) * p.T; };
+        if (TREE && n_tiles > nc && grow < p.M && !pad_warp)
+            for (int k = chalf * kHalf; k < p.T; k += kBlockN) prefetch_l1(mask_row() + k);
 #ifdef HTA_TRACE
         uint32_t tr_c[6] = {0, 0, 0, 0, 0, 0};
 #endif
@@ -785,6 +892,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             }
         };
         for (int j = grp; j < n_tiles; j += 2) {
+            const bool tree_tile = TREE && j >= nc;  // a tree tile of the fused tree pass
             const int buf = j % C::kSBufs;
             mbar_wait(&s_full[buf], static_cast<uint32_t>((j / C::kSBufs) & 1));
             tc_fence_after();
@@ -795,7 +903,13 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 publish(j);
                 continue;
             }
-            const bool last = j == n_tiles - 1;
+            // a tree tile: the keys the mask hides are set to -inf in TMEM before the softmax reads
+            // S, in a function of its own so that the exponential loop
+            // is scheduled exactly as for the cache tiles
+            if (tree_tile)
+                mask_tree_tile(tmem + lane_off + s_col(buf), grow < p.M ? mask_row() : nullptr, p.T,
+                               (j - nc) * kBlockN + chalf * kHalf);
+            const bool last = !tree_tile && j == nc - 1;  // the split's last cache tile
             // S_j of this thread in two chunks of 32 columns (keys [kHalf*chalf + 32*ch, +32)): the
             // chunk's values are loaded, turned into packed P and dead before the next chunk
             // loads, so the softmax fits its register budget without spills.  Keys past the split
@@ -875,10 +989,12 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             if (ovf) rho = row_max();  // (rare: a group's first tile, or a jump of the logits)
             HTA_TRS(2);
             // hand rho_j over ("no requirement" is -FLT_MAX rather than -inf, so the tagged word
-            // stays a finite float); both groups fold the same tagged values
+            // stays a finite float); both groups fold the same tagged values.  A row whose keys
+            // are all hidden in this tile (tree tile) has rho = -inf: no requirement either.
             const uint32_t gen = static_cast<uint32_t>((j / 3) & 1);
-            if (ovf) rho = __uint_as_float((__float_as_uint(rho) & ~1u) | gen);
-            if (chalf == 0) st_volatile_shared(&m_sh[(j % 3) * 128 + r], ovf ? __float_as_uint(rho) : (0xFF7FFFFEu | gen));
+            const bool req = TREE ? ovf && rho != -INFINITY : ovf;
+            if (req) rho = __uint_as_float((__float_as_uint(rho) & ~1u) | gen);
+            if (chalf == 0) st_volatile_shared(&m_sh[(j % 3) * 128 + r], req ? __float_as_uint(rho) : (0xFF7FFFFEu | gen));
             // the running max after tile j-1 (fold of rho_{j-1}), then after tile j; both groups
             // fold the same sequence rho_0, rho_1, ... and agree on every tile's max
             float m_prev = m_run;
@@ -891,11 +1007,22 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     while (((wv = ld_volatile_shared(src)) & 1u) != want)
                         if (global_ns() - t0 > kWatchdogNs) __trap();
                 }
-                m_prev = fold_max<KV8>(m_prev, __uint_as_float(wv));
+                // (TREE: a row may have seen no key at all yet, m = -inf, which the "no
+                // requirement" word -FLT_MAX would otherwise raise)
+                if (!TREE || (wv | 1u) != 0xFF7FFFFFu) m_prev = fold_max<KV8>(m_prev, __uint_as_float(wv));
             }
             HTA_TRS(3);
             const float m_fin = fold_max<KV8>(m_prev, rho);
-            if (__any_sync(0xffffffffu, ovf || m_fin != m_spec)) lsum = exp_pack(m_fin, std::false_type{});
+            if (!TREE) {
+                if (__any_sync(0xffffffffu, ovf || m_fin != m_spec)) lsum = exp_pack(m_fin, std::false_type{});
+            } else if (__any_sync(0xffffffffu, ovf || m_fin != m_spec)) {
+                lsum = exp_pack(m_fin == -INFINITY ? 0.f : m_fin, std::false_type{});
+                if (m_fin == -INFINITY) {  // a row with no visible key yet (tree tile): P = 0 exactly
+                    lsum = 0.f;            // (the polynomial slots give 2^-126 for -inf, not 0)
+#pragma unroll
+                    for (int i = 0; i < kHalf / 2; ++i) pk[i] = 0u;
+                }
+            }
             // P_j over S_j in TMEM (columns [Ch/2, Ch/2 + 32)), without waiting
             if (!(HTA_DIAG & 1)) {
                 tmem_st_16x16_split_nowait<kHalf / 2>(tmem + lane_off + s_col(buf), pk);
@@ -942,7 +1069,8 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             const float li = x_l[((i >> 1) * 128 + r) * 2 + (i & 1)];
             if (li > 0.f) l_tot += li * fast_exp2(mi - m_tot);
         }
-        const float inv = (KV8 ? p.v_scale[g] : 1.0f) / l_tot;  // V = v_scale[g] * E4M3
+        // V = v_scale[g] * E4M3; l_tot = 0: no visible key in the split (O = 0, LSE = -inf)
+        const float inv = TREE && !(l_tot > 0.f) ? 0.f : (KV8 ? p.v_scale[g] : 1.0f) / l_tot;
         const bool row_ok = grow < p.M && !pad_warp;
         int t = 0, h = 0;
         if (row_ok) {
@@ -995,11 +1123,11 @@ extern "C" __attribute__((visibility("default"))) int hta_debug_set_trace(void *
 }
 #endif
 
-template <int D, bool PAIR, bool KV8>
+template <int D, bool PAIR, bool KV8, bool TREE = false>
 static cudaError_t launch_tc(const PrefixParams &p, const CUtensorMap &tq, const CUtensorMap &tk, const CUtensorMap &tv,
-                             cudaStream_t s) {
+                             const CUtensorMap &tkt, const CUtensorMap &tvt, cudaStream_t s) {
     using C = TcCfg<D, PAIR>;
-    auto kern = prefix_tc_kernel<D, PAIR, KV8>;
+    auto kern = prefix_tc_kernel<D, PAIR, KV8, TREE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
@@ -1018,7 +1146,7 @@ static cudaError_t launch_tc(const PrefixParams &p, const CUtensorMap &tq, const
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, p);
+    e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tkt, tvt, p);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -1029,16 +1157,26 @@ int prefix_tc_smem_bytes(int d, int nt) {
 }
 
 cudaError_t launch_prefix_tc(const PrefixParams &p, const CUtensorMap &tq, const CUtensorMap &tk, const CUtensorMap &tv,
-                             int, cudaStream_t s) {
+                             const CUtensorMap &tkt, const CUtensorMap &tvt, int, cudaStream_t s) {
     if (p.kv8) {
+        if (p.tree_tiles != 0) return cudaErrorInvalidValue;  // (the FP8 variant has no fused tree pass)
         if (p.d == 128)
-            return p.nt == 2 ? launch_tc<128, true, true>(p, tq, tk, tv, s) : launch_tc<128, false, true>(p, tq, tk, tv, s);
-        if (p.d == 64 && p.nt == 1) return launch_tc<64, false, true>(p, tq, tk, tv, s);
+            return p.nt == 2 ? launch_tc<128, true, true>(p, tq, tk, tv, tkt, tvt, s)
+                             : launch_tc<128, false, true>(p, tq, tk, tv, tkt, tvt, s);
+        if (p.d == 64 && p.nt == 1) return launch_tc<64, false, true>(p, tq, tk, tv, tkt, tvt, s);
+        return cudaErrorInvalidValue;
+    }
+    if (p.tree_tiles < 0 || p.tree_tiles > 2) return cudaErrorInvalidValue;
+    if (p.tree_tiles > 0) {  // the fused tree pass (single-CTA row groups, hta_api.cu forward_impl)
+        if (p.nt != 1) return cudaErrorInvalidValue;
+        if (p.d == 128) return launch_tc<128, false, false, true>(p, tq, tk, tv, tkt, tvt, s);
+        if (p.d == 64) return launch_tc<64, false, false, true>(p, tq, tk, tv, tkt, tvt, s);
         return cudaErrorInvalidValue;
     }
     if (p.d == 128)
-        return p.nt == 2 ? launch_tc<128, true, false>(p, tq, tk, tv, s) : launch_tc<128, false, false>(p, tq, tk, tv, s);
-    if (p.d == 64 && p.nt == 1) return launch_tc<64, false, false>(p, tq, tk, tv, s);
+        return p.nt == 2 ? launch_tc<128, true, false>(p, tq, tk, tv, tkt, tvt, s)
+                         : launch_tc<128, false, false>(p, tq, tk, tv, tkt, tvt, s);
+    if (p.d == 64 && p.nt == 1) return launch_tc<64, false, false>(p, tq, tk, tv, tkt, tvt, s);
     return cudaErrorInvalidValue;
 }
 

@@ -144,6 +144,11 @@ __device__ __forceinline__ void tma_load_4d(void *smem_dst, const void *map, uin
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
         : "memory");
 }
+// L1 prefetch of the 128-byte line holding addr (generic global address).
+__device__ __forceinline__ void prefetch_l1(const void *addr) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(addr));
+}
+
 // L2 prefetch of a tensor box (no shared-memory destination, no completion).
 __device__ __forceinline__ void tma_prefetch_l2_4d(const void *map, int c0, int c1, int c2, int c3) {
     asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];" ::"l"(map), "r"(c0), "r"(c1),

@@ -364,8 +364,9 @@ def test_max_seqlen_hint_plans_by_filled_length(cuda_device):
 
 def test_forward_ex_tree_inputs_late(cuda_device):
     """hta_forward_ex: k_tree / v_tree / mask produced on another stream after the call is
-    enqueued; only the tree/merge kernel waits for them (the event), and the result equals
-    hta_forward's."""
+    enqueued; only the tree/merge kernel waits for them (the event; the tree pass then runs in
+    that kernel instead of the prefix kernel), and the result matches the oracle as
+    hta_forward's does."""
     w = make_workload(1, 64, 32, 8, 128, 3000, "bf16", dist="V1", seed=19, tree="beam")
     mask_h = torch.from_numpy(oracle_masks(w)[0])
     x = to_dev(w, cuda_device)
@@ -385,4 +386,34 @@ def test_forward_ex_tree_inputs_late(cuda_device):
         ready.record()
     o, l = hta.hta_forward(x["q"], x["kc"], x["vc"], kt, vt, m, tree_ready=ready)
     torch.cuda.synchronize()
-    assert torch.equal(o, o_ref) and torch.equal(l, l_ref)
+    oo, lo = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, oracle_masks(w))
+    compare(o_ref, l_ref, oo, lo, "bf16", "forward (fused tree pass)")
+    compare(o, l, oo, lo, "bf16", "forward_ex (tree inputs late)")
+
+
+@pytest.mark.parametrize("case", [
+    # B, T, H, Hkv, d, N, seqlens, num_splits: single-CTA row groups (the fused tree pass)
+    (2, 200, 2, 2, 64, 700, (700, 0), 0),       # two tree tiles; an empty cache
+    (3, 64, 8, 8, 128, 1000, (1000, 1, 129), 0),  # MHA (LongChat rows); 1-key and 129-key caches
+    (2, 64, 10, 2, 128, 900, (900, 300), 7),    # G = 5, forced splits: the last split holds only tree
+    (1, 17, 3, 1, 128, 16, (0,), 0),            # an empty cache: the tree tile alone
+])
+def test_fused_tree_pass_edge_cases(cuda_device, case):
+    """hta_forward runs the tree pass inside the prefix kernel for single-CTA row groups (tree
+    tiles appended to each unit's last split, masked in TMEM).  Arbitrary masks with empty rows,
+    caches shorter than a tile or empty, two tree tiles (T > 128) and a last split holding only
+    the tree tile all match the oracle; an all-zero mask row over an empty cache is the sentinel
+    (O = 0, LSE = -inf)."""
+    B, T, H, Hkv, d, N, sl, ns = case
+    seqlens = torch.tensor(sl, dtype=torch.int32)
+    w = make_workload(B, T, H, Hkv, d, N, "bf16", dist="V1", seed=41, tree="random", seqlens=seqlens,
+                      garbage_tail=True)
+    mask = random_mask(B, T, 0.35, seed=7).numpy()
+    mask[0, 3] = 0
+    mask[-1, T - 1] = 0
+    x = to_dev(w, cuda_device)
+    o_ref, l_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, mask, seqlens=w.seqlens)
+    o, l = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], torch.from_numpy(mask).to(cuda_device),
+                           cache_seqlens=x["sl"], num_splits=ns)
+    torch.cuda.synchronize()
+    compare(o, l, o_ref, l_ref, "bf16", f"fused tree pass {case}")
