@@ -281,25 +281,28 @@ def main():
 
     side = torch.cuda.Stream(device=dev)
 
-    def step(x, events=None, tree_ready=None):
-        """One verification step: a0 -> a1..a4 (a5) on the current stream; a6 (independent of
-        the attention: it needs only the tree and the target's argmax) on a forked stream."""
+    def step(x, events=None):
+        """One verification step.  One GPU: a0 (the tree mask, kept for the other layers of the
+        step) and a6 (the accepted path: it needs only the tree and the target's argmax) in one
+        launch on a forked stream, beside a1-a4 on the current stream, which derives each row's
+        visible tree keys from the parent array itself (hta_forward_tree), so the mask build is
+        off the attention's critical path.  N > 1: a0 + a6, then a1-a5 (the sequence-parallel
+        exchange takes the mask)."""
         cur = torch.cuda.current_stream()
+        if seqpar:
+            hta.hta_tree_step(x["parents"], x["draft"], x["tgt"], root=0, context_argmax=ctx, mask=mask,
+                              path=path, path_len=plen, bonus=bonus)                         # a0 + a6
+            comm.forward(x["q"], kc, vc, x["kt"], x["vt"], mask, cache_seqlens_local=sl, o=o, lse_out=lse, ws=wsb)
+            return
         side.wait_stream(cur)
         with torch.cuda.stream(side):
-            hta.hta_accept_greedy(x["parents"], x["draft"], x["tgt"], root=0, context_argmax=ctx,
-                                  path=path, path_len=plen, bonus=bonus)                    # a6
-        hta.hta_build_tree_mask(x["parents"], mask)                                         # a0
-        if seqpar:                                                                          # a1-a5
-            if tree_ready is not None:
-                cur.wait_event(tree_ready)
-            comm.forward(x["q"], kc, vc, x["kt"], x["vt"], mask, cache_seqlens_local=sl, o=o, lse_out=lse, ws=wsb)
-        else:                                                                               # a1-a4
-            hta.hta_forward(x["q"], kc, vc, x["kt"], x["vt"], mask, cache_seqlens=sl, o=o, lse_out=lse, ws=wsb,
-                            events=events, tree_ready=tree_ready)
+            hta.hta_tree_step(x["parents"], x["draft"], x["tgt"], root=0, context_argmax=ctx, mask=mask,
+                              path=path, path_len=plen, bonus=bonus)                         # a0 + a6
+        hta.hta_forward_tree(x["q"], kc, vc, x["kt"], x["vt"], x["parents"], cache_seqlens=sl, o=o,
+                             lse_out=lse, ws=wsb, events=events)                              # a1-a4
         cur.wait_stream(side)
 
-    launches_per_step = 5 if seqpar else 4
+    launches_per_step = 4 if seqpar else 3  # tree step; prefix, (local merge, final merge | tree/merge)
 
     def barrier():
         if seqpar:
@@ -381,8 +384,8 @@ def main():
             tev = created_events(args.steps)
 
             def fwd_timed(i):
-                hta.hta_forward(d_in["q"], kc, vc, d_in["kt"], d_in["vt"], mask, cache_seqlens=sl, o=o, lse_out=lse,
-                                ws=wsb, events=pev[i])
+                hta.hta_forward_tree(d_in["q"], kc, vc, d_in["kt"], d_in["vt"], d_in["parents"], cache_seqlens=sl,
+                                     o=o, lse_out=lse, ws=wsb, events=pev[i])
                 tev[i].record()  # after the tree/merge kernel (launched without PDL in this mode)
 
             timed(fwd_timed, args.steps)
@@ -455,14 +458,17 @@ def main():
         "config": {"workload": args.workload, **{k: cfg[k] for k in ("B", "T", "H", "H_kv", "d", "N")}},
         "setup": {"parallelism": f"seq{ws}",
                   "l2": "flushed before every timed step (512 MiB write, then two reads of it; untimed)",
-                  "step": ("a0 mask + hta_forward (a1-a4) | accept (a6) on a forked stream"
-                           + (" + NCCL exchange (a5)" if seqpar else "") + "; " + graph_note)},
+                  "step": (("a0 mask + a6 accept (hta_tree_step), then hta_forward_seqpar (a1-a5, NCCL exchange)"
+                            if seqpar else
+                            "a0 mask + a6 accept (hta_tree_step) on a forked stream | hta_forward_tree (a1-a4; "
+                            "visibility from the parent array)") + "; " + graph_note)},
         "t_us": dist_us(times),
         "kernel_us": {"prefix": None if prefix_ms is None else prefix_ms * 1e3,
                       "tree_merge": None if tm_ms is None else tm_ms * 1e3,
-                      "note": "prefix: CUDA events around its launch; tree_merge: from the prefix's end event to "
-                              "an event after the tree/merge kernel, launched without programmatic overlap in "
-                              "this timing pass (so it includes its launch gap)"},
+                      "note": "prefix: CUDA events around its launch (the tree pass runs in it for single-CTA row "
+                              "groups); tree_merge: from the prefix's end event to an event after the tree/merge "
+                              "kernel, launched without programmatic overlap in this timing pass (so it includes "
+                              "its launch gap)"},
         "clocks": clocks,
         "gpu_launches": launches_per_step * args.steps,
         "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
@@ -618,13 +624,21 @@ def time_step_for(name, dev, ws, rank, comm, flush, args, max_over_ranks, barrie
     wsb = (torch.empty(comm.workspace_size(shape), dtype=torch.uint8, device=dev) if comm is not None
            else hta.new_workspace(shape, dev))
 
+    side = torch.cuda.Stream(device=dev)
+
     def fn():
-        hta.hta_build_tree_mask(parents, mask)
         if comm is not None:
+            hta.hta_build_tree_mask(parents, mask)
             comm.forward(x["q"], kc, vc, x["k_tree"], x["v_tree"], mask, cache_seqlens_local=sl, o=o, lse_out=lse,
                          ws=wsb)
-        else:
-            hta.hta_forward(x["q"], kc, vc, x["k_tree"], x["v_tree"], mask, cache_seqlens=sl, o=o, lse_out=lse, ws=wsb)
+        else:  # (as the main step: the mask built beside the forward, which walks the parents)
+            cur = torch.cuda.current_stream()
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):
+                hta.hta_build_tree_mask(parents, mask)
+            hta.hta_forward_tree(x["q"], kc, vc, x["k_tree"], x["v_tree"], parents, cache_seqlens=sl, o=o,
+                                 lse_out=lse, ws=wsb)
+            cur.wait_stream(side)
 
     for _ in range(args.warmup):
         fn()
@@ -660,8 +674,8 @@ def time_step_for(name, dev, ws, rank, comm, flush, args, max_over_ranks, barrie
     torch.cuda.empty_cache()
     return {"workload": name, "us_per_step": t_ms * 1e3, "value": w.B * w.T / (t_ms * 1e-3), "unit": "tokens/s",
             "n_gpus": ws, "keys_per_rank": hi - lo, "scaling": "strong",
-            "step": "a0 mask + " + ("hta_forward_seqpar (NCCL exchange)" if comm is not None else "hta_forward") +
-                    ("; CUDA graph" if run is not fn else "; eager")}
+            "step": ("a0 mask + hta_forward_seqpar (NCCL exchange)" if comm is not None
+                     else "a0 mask on a forked stream | hta_forward_tree") + ("; CUDA graph" if run is not fn else "; eager")}
 
 
 def bench_fp8(dev, flush, k=10, name="longchat7b_16k"):
@@ -712,8 +726,8 @@ def bench_config(name, dev, flush, k=10):
     w = config_workload(name, seed=0)
     x = {"q": w.q.to(dev), "kc": w.k_cache.to(dev), "vc": w.v_cache.to(dev), "kt": w.k_tree.to(dev),
          "vt": w.v_tree.to(dev), "parents": w.parents[0].to(dev)}
-    mask = hta.hta_build_tree_mask(x["parents"])
-    o, lse = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask)
+    par = x["parents"]
+    o, lse = hta.hta_forward_tree(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], par)
     shape = hta.make_shape(x["q"], k_cache=x["kc"], k_tree=x["kt"])
     wsb = hta.new_workspace(shape, dev)
     ts, tp = [], []
@@ -721,11 +735,11 @@ def bench_config(name, dev, flush, k=10):
         e = created_events(4)
         flush.fill_(i & 0xFF)
         e[0].record()
-        hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask, o=o, lse_out=lse, ws=wsb)
+        hta.hta_forward_tree(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], par, o=o, lse_out=lse, ws=wsb)
         e[1].record()
         flush.fill_(i & 0xFF)
-        hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask, o=o, lse_out=lse, ws=wsb,
-                        events=(e[2], e[3]))
+        hta.hta_forward_tree(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], par, o=o, lse_out=lse, ws=wsb,
+                             events=(e[2], e[3]))
         torch.cuda.synchronize()
         if i >= 3:
             ts.append(e[0].elapsed_time(e[1]))

@@ -134,8 +134,11 @@ hta_status_t hta_merge_lse(const hta_shape_t *shape, int32_t n_parts, const floa
 
 /* hybrid_tree_attention: prefix pass + tree pass + merge, i.e. the full
  * verification-step attention of one layer.  Two kernels: the split-KV prefix kernel, then
- * one kernel that runs the tree pass and merges the split partials with it.  Arguments as
- * above; o in shape->dtype with q_strides; lse_out optional (NULL). */
+ * one kernel that merges the split partials.  The tree pass runs in the prefix kernel (masked
+ * tree tiles appended to each unit's last split) for bf16 caches whose row groups are single
+ * CTAs (T*H/H_kv rows packing into 128-row tiles; MHA, G = 5, d = 64), else in the second kernel
+ * beside the merge; the result is the same up to rounding.  Arguments as above; o in
+ * shape->dtype with q_strides; lse_out optional (NULL). */
 hta_status_t hta_forward(const hta_shape_t *shape, const void *q, const void *k_cache,
                          const void *v_cache, const int32_t *cache_seqlens, const void *k_tree,
                          const void *v_tree, const uint8_t *mask, int64_t mask_batch_stride,
@@ -164,6 +167,24 @@ hta_status_t hta_forward_ex(const hta_shape_t *shape, const void *q, const void 
                             const void *v_tree, const uint8_t *mask, int64_t mask_batch_stride,
                             void *o, float *lse_out, void *ws, size_t ws_bytes,
                             hta_stream_t stream, void *tree_inputs_ready);
+
+/* hta_forward with the tree given by its parent array instead of a mask (
+ * reading Z4): row t sees tree key s iff s == t or s is an ancestor of t, derived inside the
+ * kernels by walking the parent links -- the same rows hta_build_tree_mask writes (a chain
+ * through an invalid entry, parents[a] < -1 or >= a, hides the whole row).  The mask build (a0)
+ * is then off the attention's critical path: a verification step can build the mask it keeps
+ * (hta_tree_step) on another stream while this runs.
+ *   parents    device int32 [B][T] (parents_batch_stride elements apart; 0 = one tree shared
+ *              by the batch), parents[t] in [-1, t)
+ *   ev_prefix_begin / ev_prefix_end  optional cudaEvent_t recorded around the prefix kernel,
+ *              as in hta_forward_timed (NULL: none)
+ * Other arguments, layout, ownership and errors as hta_forward. */
+hta_status_t hta_forward_tree(const hta_shape_t *shape, const void *q, const void *k_cache,
+                              const void *v_cache, const int32_t *cache_seqlens,
+                              const void *k_tree, const void *v_tree, const int32_t *parents,
+                              int64_t parents_batch_stride, void *o, float *lse_out, void *ws,
+                              size_t ws_bytes, hta_stream_t stream, void *ev_prefix_begin,
+                              void *ev_prefix_end);
 
 /* hybrid_tree_attention over a PAGED KV cache (the block-table layout of
  * flash_attn_with_kvcache, for batched serving): as hta_forward (bf16 only), with

@@ -291,6 +291,8 @@ struct TreeArgs {
     int tree_tiles;
     const uint8_t *mask;
     int64_t mask_bs;
+    const int32_t *parents;  // (mask == nullptr) visibility from the parent array
+    int64_t par_bs;
     CUtensorMap tkt, tvt;
 };
 
@@ -367,6 +369,8 @@ hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, co
             p.tree_tiles = tr->tree_tiles;
             p.mask = tr->mask;
             p.mask_bs = tr->mask_bs;
+            p.parents = tr->parents;
+            p.par_bs = tr->par_bs;
         }
         const bool fused = p.tree_tiles > 0;
         e = launch_prefix_tc(p, tq, tk, tv, fused ? tr->tkt : none, fused ? tr->tvt : none,
@@ -526,13 +530,17 @@ static hta_status_t forward_impl(const PagedArgs *pg, const hta_shape_t *shape, 
                                const int32_t *cache_seqlens, const void *k_tree, const void *v_tree,
                                const uint8_t *mask, int64_t mask_batch_stride, void *o, float *lse_out, void *ws,
                                size_t ws_bytes, hta_stream_t stream, void *ev_begin, void *ev_end,
-                               const Fp8Args *f8 = nullptr, void *tree_ready = nullptr) {
+                               const Fp8Args *f8 = nullptr, void *tree_ready = nullptr,
+                               const int32_t *parents = nullptr, int64_t parents_bs = 0) {
     Shape sh;
     hta_status_t r = check_shape(shape, &sh);
     if (r != HTA_OK) return r;
     const hta_shape_t &s = sh.s;
-    if (!q || !k_cache || !v_cache || !k_tree || !v_tree || !mask || !o) return HTA_ERR_INVALID_ARGUMENT;
-    if (mask_batch_stride != 0 && mask_batch_stride < int64_t(s.T) * s.T) return HTA_ERR_INVALID_ARGUMENT;
+    // the tree's visibility: the mask, or (hta_forward_tree) the parent array
+    if (!q || !k_cache || !v_cache || !k_tree || !v_tree || (!mask && !parents) || !o) return HTA_ERR_INVALID_ARGUMENT;
+    if (mask != nullptr && mask_batch_stride != 0 && mask_batch_stride < int64_t(s.T) * s.T)
+        return HTA_ERR_INVALID_ARGUMENT;
+    if (mask == nullptr && parents_bs != 0 && parents_bs < s.T) return HTA_ERR_INVALID_ARGUMENT;
     if (!is_aligned(q, 16) || !is_aligned(k_cache, 16) || !is_aligned(v_cache, 16) || !is_aligned(k_tree, 16) ||
         !is_aligned(v_tree, 16) || !is_aligned(o, 16))
         return HTA_ERR_INVALID_ARGUMENT;
@@ -552,6 +560,8 @@ static hta_status_t forward_impl(const PagedArgs *pg, const hta_shape_t *shape, 
             tr.tree_tiles = fused_tree_tiles(s);
             tr.mask = mask;
             tr.mask_bs = mask_batch_stride;
+            tr.parents = mask == nullptr ? parents : nullptr;
+            tr.par_bs = parents_bs;
             pl = plt;
         }
     }
@@ -578,6 +588,8 @@ static hta_status_t forward_impl(const PagedArgs *pg, const hta_shape_t *shape, 
     p.vt = v_tree;
     p.mask = mask;
     p.mask_bs = mask_batch_stride;
+    p.parents = mask == nullptr ? parents : nullptr;
+    p.par_bs = parents_bs;
     p.do_tree = tr.tree_tiles > 0 ? 0 : 1;  // (fused: the partials already hold the tree part)
     p.n_parts = pl.splits;
     p.o_parts = o_ws;
@@ -625,6 +637,16 @@ hta_status_t hta_forward_paged(const hta_shape_t *shape, const void *q, const vo
     const PagedArgs pg{block_table, max_pages, page_size, num_pages};
     return forward_impl(&pg, &s, q, k_pool, v_pool, cache_seqlens, k_tree, v_tree, mask, mask_batch_stride, o, lse_out,
                         ws, ws_bytes, stream, nullptr, nullptr);
+}
+
+hta_status_t hta_forward_tree(const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,
+                              const int32_t *cache_seqlens, const void *k_tree, const void *v_tree,
+                              const int32_t *parents, int64_t parents_batch_stride, void *o, float *lse_out, void *ws,
+                              size_t ws_bytes, hta_stream_t stream, void *ev_prefix_begin, void *ev_prefix_end) {
+    if (parents == nullptr) return HTA_ERR_INVALID_ARGUMENT;
+    return forward_impl(nullptr, shape, q, k_cache, v_cache, cache_seqlens, k_tree, v_tree, nullptr, 0, o, lse_out, ws,
+                        ws_bytes, stream, ev_prefix_begin, ev_prefix_end, nullptr, nullptr, parents,
+                        parents_batch_stride);
 }
 
 hta_status_t hta_forward(const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,

@@ -58,6 +58,8 @@ struct PrefixParams {
     int tree_tiles;
     const uint8_t *mask;
     int64_t mask_bs;
+    const int32_t *parents;           // hta_forward_tree: visibility from parents [b*par_bs + t] instead of mask
+    int64_t par_bs;
     float *o_out;                     // [S][B][T][H][d] fp32, normalised partials
     float *lse_out;                   // [S][B][H][T] natural-log LSE
     int64_t o_split_stride, lse_split_stride;  // elements between splits
@@ -72,6 +74,8 @@ struct TreeMergeParams {
     int64_t ts0, ts1, ts2;
     const uint8_t *mask;              // [B,T,T]
     int64_t mask_bs;                  // batch stride (0 = shared)
+    const int32_t *parents;           // or (mask == nullptr) the parent array [B,T] (visibility = ancestors)
+    int64_t par_bs;                   // batch stride of parents (0 = shared)
     float scale;
     int do_tree;                      // run the masked tree pass
     int n_parts;                      // prefix partials to merge (0 = none)

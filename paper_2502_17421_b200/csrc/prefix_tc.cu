@@ -192,13 +192,35 @@ __device__ __forceinline__ uint32_t tree_chunk_bits(const uint8_t *mrow, int T, 
 // start at TMEM address `at`; mrow = the row's mask bytes (nullptr: a padding row, all hidden),
 // k0 = the tree key of the first of the 64 columns.  Not inlined: keeps the softmax loop's
 // schedule independent of this rarely taken path.
-__device__ __noinline__ void mask_tree_tile(uint32_t at, const uint8_t *mrow, int T, int k0) {
+// Visibility bits of tree keys [k0, k0 + 64) for token t derived from the parent array (hta_forward
+// _tree): t and its ancestors, walking parent links (Z4); a chain that meets an invalid link
+// (parents[a] < -1 or >= a) makes the row all-hidden, exactly as hta_build_tree_mask's row.
+__device__ __forceinline__ void ancestor_bits64(const int32_t *par, int t, int k0, uint32_t (&w)[2]) {
+    w[0] = w[1] = 0u;
+    int a = t;
+    while (a >= 0) {
+        if (a >= k0 && a < k0 + 64) w[(a - k0) >> 5] |= 1u << ((a - k0) & 31);
+        const int pa = par[a];
+        if (pa < -1 || pa >= a) {
+            w[0] = w[1] = 0u;
+            return;
+        }
+        a = pa;
+    }
+}
+
+// mrow: the row's mask bytes; or (mrow == nullptr, par != nullptr) the parent array and the row's
+// token t; neither: a padding row (all hidden).
+__device__ __noinline__ void mask_tree_tile(uint32_t at, const uint8_t *mrow, const int32_t *par, int t, int T,
+                                            int k0) {
+    uint32_t pw[2] = {0u, 0u};
+    if (mrow == nullptr && par != nullptr) ancestor_bits64(par, t, k0, pw);
 #pragma unroll 1
     for (int ch = 0; ch < 2; ++ch) {
         float sm[32];
         tmem_ld_x32_nowait<64>(at + ch * 32, sm);
         tmem_ld_wait_fence<32>(sm);
-        const uint32_t bits = mrow != nullptr ? tree_chunk_bits(mrow, T, k0 + ch * 32) : 0u;
+        const uint32_t bits = mrow != nullptr ? tree_chunk_bits(mrow, T, k0 + ch * 32) : pw[ch];
 #pragma unroll
         for (int cc = 0; cc < 32; ++cc)
             if (!((bits >> cc) & 1u)) sm[cc] = -INFINITY;
@@ -873,7 +895,12 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         // (the row's mask bytes, recomputed where used: nothing held across the cache tiles)
         auto mask_row = [&]() { return p.mask + b * p.mask_bs + static_cast<int64_t>(grow / p.G) * p.T; };
         if (TREE && n_tiles > nc && grow < p.M && !pad_warp)
-            for (int k = chalf * kHalf; k < p.T; k += kBlockN) prefetch_l1(mask_row() + k);
+            for (int k = chalf * kHalf; k < p.T; k += kBlockN) {
+                if (p.parents != nullptr)  // (the line of the row's own parent entry; its walk starts there)
+                    prefetch_l1(p.parents + b * p.par_bs + grow / p.G);
+                else
+                    prefetch_l1(mask_row() + k);
+            }
 #ifdef HTA_TRACE
         uint32_t tr_c[6] = {0, 0, 0, 0, 0, 0};
 #endif
@@ -907,7 +934,8 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             // S, in a function of its own so that the exponential loop
             // is scheduled exactly as for the cache tiles
             if (tree_tile)
-                mask_tree_tile(tmem + lane_off + s_col(buf), grow < p.M ? mask_row() : nullptr, p.T,
+                mask_tree_tile(tmem + lane_off + s_col(buf), grow < p.M && p.parents == nullptr ? mask_row() : nullptr,
+                               grow < p.M ? p.parents + b * p.par_bs : nullptr, grow / p.G, p.T,
                                (j - nc) * kBlockN + chalf * kHalf);
             const bool last = !tree_tile && j == nc - 1;  // the split's last cache tile
             // S_j of this thread in two chunks of 32 columns (keys [kHalf*chalf + 32*ch, +32)): the

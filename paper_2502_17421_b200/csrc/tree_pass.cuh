@@ -88,13 +88,44 @@ __device__ __forceinline__ float tree_row(const TreeMergeParams &p, int b, int t
     // one round trip for q and the whole mask row (T <= 256: up to 8 bytes per lane)
     float qv[E];
     VecIO<Tin, E>::load(static_cast<const Tin *>(p.q) + b * p.qs0 + t * p.qs1 + h * p.qs2 + lane * E, qv);
-    const uint8_t *mrow = p.mask + b * p.mask_bs + static_cast<int64_t>(t) * p.T;
-    uint8_t mb[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) mb[c] = (c * 32 < p.T && c * 32 + lane < p.T) ? mrow[c * 32 + lane] : 0;
     uint32_t vis[8];
+    if (p.mask != nullptr) {
+        const uint8_t *mrow = p.mask + b * p.mask_bs + static_cast<int64_t>(t) * p.T;
+        uint8_t mb[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) vis[c] = __ballot_sync(0xffffffffu, mb[c] != 0);
+        for (int c = 0; c < 8; ++c) mb[c] = (c * 32 < p.T && c * 32 + lane < p.T) ? mrow[c * 32 + lane] : 0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) vis[c] = __ballot_sync(0xffffffffu, mb[c] != 0);
+    } else {
+        // hta_forward_tree: the row's visible keys are t and its ancestors (Z4), found by walking
+        // the parent links held in registers (lane l: parents[32c + l]); a chain through an
+        // invalid link (parents[a] < -1 or >= a) hides the whole row, as hta_build_tree_mask does
+        const int32_t *prow = p.parents + b * p.par_bs;
+        int par[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) par[c] = c * 32 + lane < p.T ? prow[c * 32 + lane] : -1;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) vis[c] = 0u;
+        int a = t;
+        while (a >= 0) {
+            int pa = -1;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                if (c * 32 >= p.T) break;
+                const int x = __shfl_sync(0xffffffffu, par[c], a & 31);
+                if (c == (a >> 5)) {
+                    pa = x;
+                    vis[c] |= 1u << (a & 31);
+                }
+            }
+            if (pa < -1 || pa >= a) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) vis[c] = 0u;
+                break;
+            }
+            a = pa;
+        }
+    }
     const Tin *Kt = static_cast<const Tin *>(p.kt) + b * p.ts0 + g * p.ts2 + lane * E;
     const Tin *Vt = static_cast<const Tin *>(p.vt) + b * p.ts0 + g * p.ts2 + lane * E;
     using Acc = typename std::conditional<std::is_same<Tin, float>::value, double, float>::type;

@@ -417,3 +417,50 @@ def test_fused_tree_pass_edge_cases(cuda_device, case):
                            cache_seqlens=x["sl"], num_splits=ns)
     torch.cuda.synchronize()
     compare(o, l, o_ref, l_ref, "bf16", f"fused tree pass {case}")
+
+
+@pytest.mark.parametrize("case", [
+    # B, T, H, Hkv, d, N, tree kinds per batch entry (one shared tree when a single kind)
+    (1, 64, 32, 8, 128, 3000, ("beam",)),                 # CTA pairs: the tree pass walks in the tree/merge kernel
+    (2, 64, 8, 8, 128, 2000, ("random", "chain")),        # MHA single CTAs: the walk in the prefix kernel
+    (2, 200, 4, 2, 64, 900, ("random_forest", "star")),   # two tree tiles, forests (several roots)
+    (1, 256, 16, 4, 128, 700, ("chain",)),                # T = 256, depth 255
+    (3, 30, 10, 2, 128, 500, ("heap_binary", "roots", "random")),  # G = 5
+])
+def test_forward_tree_from_parents(cuda_device, case):
+    """hta_forward_tree derives each row's visible tree keys from the parent array inside the
+    kernels (Z4).  Its result is bit-identical to hta_forward over the mask hta_build_tree_mask
+    writes, and matches the oracle over the oracle's tree mask."""
+    B, T, H, Hkv, d, N, kinds = case
+    w = make_workload(B, T, H, Hkv, d, N, "bf16", dist="V1", seed=29, tree="beam")
+    par = torch.stack([tree_parents(kinds[b % len(kinds)], T, seed=b) for b in range(B)])
+    shared = len(kinds) == 1
+    x = to_dev(w, cuda_device)
+    p_dev = par[0].to(cuda_device) if shared else par.to(cuda_device)
+    masks = np.stack([oracle.tree_mask(par[0 if shared else b]) for b in range(B)])
+    o_ref, l_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, masks)
+    o, l = hta.hta_forward_tree(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], p_dev)
+    m_dev = torch.stack([hta.hta_build_tree_mask(par[0 if shared else b].to(cuda_device)) for b in range(B)])
+    om, lm = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], m_dev)
+    torch.cuda.synchronize()
+    compare(o, l, o_ref, l_ref, "bf16", f"forward_tree {case}")
+    assert torch.equal(o, om) and torch.equal(l, lm), "hta_forward_tree differs from hta_forward over the built mask"
+
+
+def test_forward_tree_invalid_parents_hide_rows(cuda_device):
+    """An invalid parent entry hides every row whose chain meets it, exactly as the all-zero rows
+    hta_build_tree_mask writes for it (pairs and single CTAs)."""
+    for (H, Hkv) in ((32, 8), (8, 8)):
+        w = make_workload(1, 64, H, Hkv, 128, 1500, "bf16", dist="V1", seed=31, tree="beam")
+        par = tree_parents("random", 64, seed=4).clone()
+        par[10] = 10        # self-parent
+        par[40] = 57        # a later node
+        par[50] = -3        # below -1
+        x = to_dev(w, cuda_device)
+        p_dev = par.to(cuda_device)
+        o, l = hta.hta_forward_tree(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], p_dev)
+        m_dev = hta.hta_build_tree_mask(p_dev)
+        om, lm = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], m_dev)
+        torch.cuda.synchronize()
+        assert m_dev.sum(1).eq(0).any(), "the invalid entries must hide some rows"
+        assert torch.equal(o, om) and torch.equal(l, lm)

@@ -30,12 +30,17 @@ def main():
         lse = torch.empty(w.B, w.H, w.T, dtype=torch.float32, device=dev)
         op = torch.empty(w.B, w.T, w.H, w.d, dtype=torch.float32, device=dev)
         ready = torch.cuda.Event()
+        evs = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        parents = w.parents[0].to(dev)
         args = (x["q"], x["k_cache"], x["v_cache"], x["k_tree"], x["v_tree"], mask)
         fns = {
             "fused": lambda: hta.hta_forward(*args, o=o, lse_out=lse, ws=ws),
             "unfused": lambda: (ready.record(), hta.hta_forward(*args, o=o, lse_out=lse, ws=ws, tree_ready=ready)),
             "prefix_attn": lambda: hta.hta_prefix_attn(x["q"], x["k_cache"], x["v_cache"], o_part=op, lse_part=lse,
                                                        ws=ws),
+            "forward_tree": lambda: hta.hta_forward_tree(x["q"], x["k_cache"], x["v_cache"], x["k_tree"], x["v_tree"],
+                                                         parents, o=o, lse_out=lse, ws=ws),
+            "timed(events)": lambda: hta.hta_forward(*args, o=o, lse_out=lse, ws=ws, events=evs),
         }
         res = {}
         for nm, fn in fns.items():

@@ -20,11 +20,7 @@ __device__ __forceinline__ uint32_t ex2_f16x2(uint32_t x) {
     asm("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
     return y;
 }
-__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
-    uint32_t r;
-    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-    return r;
-}
+// (pack_f16x2: from ptx_sm100.cuh)
 template <int EMU8, bool SPREAD = false>
 __global__ void __launch_bounds__(256, 1) softmax_loop(int iters, float c, float *out) {
     float s[64];

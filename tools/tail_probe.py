@@ -77,6 +77,26 @@ def main():
         fwd()
         cur.wait_stream(side)
 
+    def fwd_tree():
+        hta.hta_forward_tree(x["q"], x["k_cache"], x["v_cache"], x["k_tree"], x["v_tree"], parents, o=o, lse_out=lse,
+                             ws=wsb)
+
+    def tstep():
+        hta.hta_tree_step(parents, dr, tg, root=0, context_argmax=ctx, mask=mask, path=path, path_len=plen,
+                          bonus=bonus)
+
+    def bench_step():  # bench.py's step: a0 + a6 forked beside hta_forward_tree
+        cur = torch.cuda.current_stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            tstep()
+        fwd_tree()
+        cur.wait_stream(side)
+
+    def tstep_then_fwd_tree():
+        tstep()
+        fwd_tree()
+
     def fused_step():
         hta.hta_tree_step(parents, dr, tg, root=0, context_argmax=ctx, mask=mask, path=path, path_len=plen,
                           bonus=bonus)
@@ -124,7 +144,9 @@ def main():
     res = {"prefix": statistics.mean(pre)}
     for nm, fn in (("forward", fwd), ("mask+fwd", mask_fwd), ("step", step), ("accept", acc),
                    ("acc;mask;fwd", step_acc_first), ("mask;fwd;acc", step_acc_last),
-                   ("mask;(acc|fwd)", step_side_after_mask), ("tree_step;fwd", fused_step)):
+                   ("mask;(acc|fwd)", step_side_after_mask), ("tree_step;fwd", fused_step),
+                   ("fwd_tree", fwd_tree), ("tree_step", tstep), ("tree_step|fwd_tree", bench_step),
+                   ("tree_step;fwd_tree", tstep_then_fwd_tree)):
         res[nm] = t(graph(fn).replay)
     print(name + ": " + ", ".join(f"{k} {v:.1f} us" for k, v in res.items()), flush=True)
 
