@@ -139,6 +139,7 @@ __device__ __forceinline__ void widen_e4m3_tile(uint8_t *slot, int lane, int val
             const int idx = (it0 + u) * 32 + lane;
             x[u] = *reinterpret_cast<const uint4 *>(src + (idx / kChunks) * kRowBytes + (idx % kChunks) * 16);
         }
+        __syncwarp();  // every lane's loads of the batch before any lane's stores over them
 #pragma unroll
         for (int u = 0; u < kWidenUnroll; ++u) {
             const int idx = (it0 + u) * 32 + lane;
