@@ -282,24 +282,22 @@ def main():
     side = torch.cuda.Stream(device=dev)
 
     def step(x, events=None):
-        """One verification step.  One GPU: a0 (the tree mask, kept for the other layers of the
-        step) and a6 (the accepted path: it needs only the tree and the target's argmax) in one
-        launch on a forked stream, beside a1-a4 on the current stream, which derives each row's
-        visible tree keys from the parent array itself (hta_forward_tree), so the mask build is
-        off the attention's critical path.  N > 1: a0 + a6, then a1-a5 (the sequence-parallel
-        exchange takes the mask)."""
+        """One verification step: a0 (the tree mask, kept for the other layers of the step) and
+        a6 (the accepted path: it needs only the tree and the target's argmax) in one launch on a
+        forked stream, beside a1-a4 (a5 for N > 1) on the current stream, which derives each
+        row's visible tree keys from the parent array itself (hta_forward_tree /
+        hta_forward_seqpar_tree), so the mask build is off the attention's critical path."""
         cur = torch.cuda.current_stream()
-        if seqpar:
-            hta.hta_tree_step(x["parents"], x["draft"], x["tgt"], root=0, context_argmax=ctx, mask=mask,
-                              path=path, path_len=plen, bonus=bonus)                         # a0 + a6
-            comm.forward(x["q"], kc, vc, x["kt"], x["vt"], mask, cache_seqlens_local=sl, o=o, lse_out=lse, ws=wsb)
-            return
         side.wait_stream(cur)
         with torch.cuda.stream(side):
             hta.hta_tree_step(x["parents"], x["draft"], x["tgt"], root=0, context_argmax=ctx, mask=mask,
                               path=path, path_len=plen, bonus=bonus)                         # a0 + a6
-        hta.hta_forward_tree(x["q"], kc, vc, x["kt"], x["vt"], x["parents"], cache_seqlens=sl, o=o,
-                             lse_out=lse, ws=wsb, events=events)                              # a1-a4
+        if seqpar:                                                                          # a1-a5
+            comm.forward(x["q"], kc, vc, x["kt"], x["vt"], cache_seqlens_local=sl, o=o, lse_out=lse, ws=wsb,
+                         parents=x["parents"])
+        else:                                                                               # a1-a4
+            hta.hta_forward_tree(x["q"], kc, vc, x["kt"], x["vt"], x["parents"], cache_seqlens=sl, o=o,
+                                 lse_out=lse, ws=wsb, events=events)
         cur.wait_stream(side)
 
     launches_per_step = 4 if seqpar else 3  # tree step; prefix, (local merge, final merge | tree/merge)
@@ -458,10 +456,9 @@ def main():
         "config": {"workload": args.workload, **{k: cfg[k] for k in ("B", "T", "H", "H_kv", "d", "N")}},
         "setup": {"parallelism": f"seq{ws}",
                   "l2": "flushed before every timed step (512 MiB write, then two reads of it; untimed)",
-                  "step": (("a0 mask + a6 accept (hta_tree_step), then hta_forward_seqpar (a1-a5, NCCL exchange)"
-                            if seqpar else
-                            "a0 mask + a6 accept (hta_tree_step) on a forked stream | hta_forward_tree (a1-a4; "
-                            "visibility from the parent array)") + "; " + graph_note)},
+                  "step": ("a0 mask + a6 accept (hta_tree_step) on a forked stream | " +
+                           ("hta_forward_seqpar_tree (a1-a5, NCCL exchange" if seqpar else "hta_forward_tree (a1-a4") +
+                           "; visibility from the parent array); " + graph_note)},
         "t_us": dist_us(times),
         "kernel_us": {"prefix": None if prefix_ms is None else prefix_ms * 1e3,
                       "tree_merge": None if tm_ms is None else tm_ms * 1e3,
@@ -626,19 +623,18 @@ def time_step_for(name, dev, ws, rank, comm, flush, args, max_over_ranks, barrie
 
     side = torch.cuda.Stream(device=dev)
 
-    def fn():
-        if comm is not None:
+    def fn():  # (as the main step: the mask built beside the forward, which walks the parents)
+        cur = torch.cuda.current_stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
             hta.hta_build_tree_mask(parents, mask)
-            comm.forward(x["q"], kc, vc, x["k_tree"], x["v_tree"], mask, cache_seqlens_local=sl, o=o, lse_out=lse,
-                         ws=wsb)
-        else:  # (as the main step: the mask built beside the forward, which walks the parents)
-            cur = torch.cuda.current_stream()
-            side.wait_stream(cur)
-            with torch.cuda.stream(side):
-                hta.hta_build_tree_mask(parents, mask)
+        if comm is not None:
+            comm.forward(x["q"], kc, vc, x["k_tree"], x["v_tree"], cache_seqlens_local=sl, o=o, lse_out=lse, ws=wsb,
+                         parents=parents)
+        else:
             hta.hta_forward_tree(x["q"], kc, vc, x["k_tree"], x["v_tree"], parents, cache_seqlens=sl, o=o,
                                  lse_out=lse, ws=wsb)
-            cur.wait_stream(side)
+        cur.wait_stream(side)
 
     for _ in range(args.warmup):
         fn()
@@ -674,8 +670,9 @@ def time_step_for(name, dev, ws, rank, comm, flush, args, max_over_ranks, barrie
     torch.cuda.empty_cache()
     return {"workload": name, "us_per_step": t_ms * 1e3, "value": w.B * w.T / (t_ms * 1e-3), "unit": "tokens/s",
             "n_gpus": ws, "keys_per_rank": hi - lo, "scaling": "strong",
-            "step": ("a0 mask + hta_forward_seqpar (NCCL exchange)" if comm is not None
-                     else "a0 mask on a forked stream | hta_forward_tree") + ("; CUDA graph" if run is not fn else "; eager")}
+            "step": "a0 mask on a forked stream | " + ("hta_forward_seqpar_tree (NCCL exchange)" if comm is not None
+                                                       else "hta_forward_tree") +
+                    ("; CUDA graph" if run is not fn else "; eager")}
 
 
 def bench_fp8(dev, flush, k=10, name="longchat7b_16k"):

@@ -346,6 +346,19 @@ hta_status_t hta_forward_seqpar(hta_comm_t comm, const hta_shape_t *shape_local,
                                 int32_t gather_output, void *ws, size_t ws_bytes,
                                 hta_stream_t stream);
 
+/* hta_forward_seqpar with the tree given by its parent array instead of a mask (as
+ * hta_forward_tree: each row's visible tree keys derived in the final merge by walking the
+ * parent links, bit-identical to the mask hta_build_tree_mask writes), so the mask build can
+ * run beside the step.  parents: device int32 [B][T] (parents_batch_stride apart; 0 = shared).
+ * Other arguments, layout, ownership and errors as hta_forward_seqpar. */
+hta_status_t hta_forward_seqpar_tree(hta_comm_t comm, const hta_shape_t *shape_local, const void *q,
+                                     const void *k_cache_local, const void *v_cache_local,
+                                     const int32_t *cache_seqlens_local, const void *k_tree,
+                                     const void *v_tree, const int32_t *parents,
+                                     int64_t parents_batch_stride, void *o, float *lse_out,
+                                     int32_t gather_output, void *ws, size_t ws_bytes,
+                                     hta_stream_t stream);
+
 /* hta_forward_seqpar for all ranks of a loopback communicator at once, on `stream` of the
  * current device.  Per-rank arguments are HOST arrays of `nranks` DEVICE pointers:
  *   k_cache_local[r], v_cache_local[r], cache_seqlens_local[r] (the array itself may be NULL:

@@ -848,13 +848,16 @@ hta_status_t seqpar_local_parts(const hta_shape_t *shape, const void *q, const v
 }
 
 hta_status_t seqpar_final_merge(const hta_shape_t *shape, int P, int rank, const void *q, const void *kt,
-                                const void *vt, const uint8_t *mask, int64_t mask_bs, const float *recvb,
-                                size_t blk_floats, void *o, float *lse, cudaStream_t st) {
+                                const void *vt, const uint8_t *mask, int64_t mask_bs, const int32_t *parents,
+                                int64_t par_bs, const float *recvb, size_t blk_floats, void *o, float *lse,
+                                cudaStream_t st) {
     Shape sh;
     hta_status_t r = check_shape(shape, &sh);
     if (r != HTA_OK) return r;
     const hta_shape_t &s = sh.s;
-    if (mask_bs != 0 && mask_bs < int64_t(s.T) * s.T) return HTA_ERR_INVALID_ARGUMENT;
+    if (mask == nullptr && parents == nullptr) return HTA_ERR_INVALID_ARGUMENT;
+    if (mask != nullptr && mask_bs != 0 && mask_bs < int64_t(s.T) * s.T) return HTA_ERR_INVALID_ARGUMENT;
+    if (mask == nullptr && par_bs != 0 && par_bs < s.T) return HTA_ERR_INVALID_ARGUMENT;
     const int Hp = s.H / P;
     TreeMergeParams p = base_tm(sh);
     p.Hr = Hp;
@@ -864,6 +867,8 @@ hta_status_t seqpar_final_merge(const hta_shape_t *shape, int P, int rank, const
     p.vt = vt;
     p.mask = mask;
     p.mask_bs = mask_bs;
+    p.parents = mask == nullptr ? parents : nullptr;
+    p.par_bs = par_bs;
     p.do_tree = 1;
     p.n_parts = P;
     p.o_parts = recvb;

@@ -138,8 +138,9 @@ hta_status_t seqpar_local_parts(const hta_shape_t *s, const void *q, const void 
                                 cudaStream_t st);
 // Merge the P received partials (blocks of `blk_floats`) with the tree pass of heads
 // [r*H/P, (r+1)*H/P) into o [B,T,H/P,d] (dtype) and lse [B,H/P,T] (optional).
+// The tree's visibility is the mask, or (mask == nullptr) the parent array (ancestor walk).
 hta_status_t seqpar_final_merge(const hta_shape_t *s, int P, int r, const void *q, const void *kt, const void *vt,
-                                const uint8_t *mask, int64_t mask_bs, const float *recvb, size_t blk_floats, void *o,
-                                float *lse, cudaStream_t st);
+                                const uint8_t *mask, int64_t mask_bs, const int32_t *parents, int64_t par_bs,
+                                const float *recvb, size_t blk_floats, void *o, float *lse, cudaStream_t st);
 
 }  // namespace hta

@@ -150,11 +150,13 @@ hta_status_t phase_local(const Geometry &g, const RankWs &w, const void *q, cons
 }
 
 // Phase 3 of rank r: the P received prefix partials + the tree pass of heads [r*Hp, (r+1)*Hp).
+// recvb: the P received blocks (rank r's own block included).
 hta_status_t phase_merge(const Geometry &g, const RankWs &w, int r, const void *q, const void *kt, const void *vt,
-                         const uint8_t *mask, int64_t mbs, void *o, float *lse, int gather, cudaStream_t st) {
+                         const uint8_t *mask, int64_t mbs, const int32_t *parents, int64_t pbs, const float *recvb,
+                         void *o, float *lse, int gather, cudaStream_t st) {
     void *o_local = gather ? static_cast<void *>(w.own_o) : o;
     float *l_local = gather ? w.own_l : lse;
-    return seqpar_final_merge(&g.s, g.P, r, q, kt, vt, mask, mbs, w.recvb, g.blk, o_local, l_local, st);
+    return seqpar_final_merge(&g.s, g.P, r, q, kt, vt, mask, mbs, parents, pbs, recvb, g.blk, o_local, l_local, st);
 }
 
 // Phase 4 (gather_output): the P gathered head slices [P][B,T,Hp,d] -> o [B,T,H,d] (and LSE).
@@ -249,14 +251,20 @@ size_t hta_workspace_size_seqpar(const hta_shape_t *shape_local, int32_t num_sms
     return g.ws_bytes;
 }
 
-hta_status_t hta_forward_seqpar(hta_comm_t comm, const hta_shape_t *shape_local, const void *q,
-                                const void *k_cache_local, const void *v_cache_local,
-                                const int32_t *cache_seqlens_local, const void *k_tree, const void *v_tree,
-                                const uint8_t *mask, int64_t mask_batch_stride, void *o, float *lse_out,
-                                int32_t gather_output, void *ws, size_t ws_bytes, hta_stream_t stream) {
+}  // extern "C"
+
+// hta_forward_seqpar / hta_forward_seqpar_tree: the tree's visibility from the mask or (mask ==
+// nullptr) the parent array.
+static hta_status_t seqpar_forward(hta_comm_t comm, const hta_shape_t *shape_local, const void *q,
+                                   const void *k_cache_local, const void *v_cache_local,
+                                   const int32_t *cache_seqlens_local, const void *k_tree, const void *v_tree,
+                                   const uint8_t *mask, int64_t mask_batch_stride, const int32_t *parents,
+                                   int64_t parents_bs, void *o, float *lse_out, int32_t gather_output, void *ws,
+                                   size_t ws_bytes, hta_stream_t stream) {
     if (comm == nullptr || shape_local == nullptr) return HTA_ERR_INVALID_ARGUMENT;
     if (comm->comm == nullptr) return HTA_ERR_INVALID_ARGUMENT;  // loopback: hta_forward_seqpar_loopback
-    if (!q || !k_cache_local || !v_cache_local || !k_tree || !v_tree || !mask || !o) return HTA_ERR_INVALID_ARGUMENT;
+    if (!q || !k_cache_local || !v_cache_local || !k_tree || !v_tree || (!mask && !parents) || !o)
+        return HTA_ERR_INVALID_ARGUMENT;
     if (!aligned16(q) || !aligned16(k_cache_local) || !aligned16(v_cache_local) || !aligned16(k_tree) ||
         !aligned16(v_tree) || !aligned16(o) || !aligned16(ws))
         return HTA_ERR_INVALID_ARGUMENT;
@@ -277,8 +285,9 @@ hta_status_t hta_forward_seqpar(hta_comm_t comm, const hta_shape_t *shape_local,
     // 1) local prefix pass -> one destination-major partial per row
     if ((rc = phase_local(g, w, q, k_cache_local, v_cache_local, cache_seqlens_local, st)) != HTA_OK) return rc;
     // 2) all-to-all of head slices: block p of sendb goes to rank p, block p of recvb comes from p
-    if (cudaMemcpyAsync(w.recvb + size_t(r) * g.blk, w.sendb + size_t(r) * g.blk, g.blk * sizeof(float),
-                        cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    // (one rank: its single block is merged straight from the send buffer)
+    if (P > 1 && cudaMemcpyAsync(w.recvb + size_t(r) * g.blk, w.sendb + size_t(r) * g.blk, g.blk * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, st) != cudaSuccess)
         return HTA_ERR_CUDA;
     if (P > 1) {
         if (api.GroupStart() != 0) return HTA_ERR_NCCL;
@@ -293,8 +302,8 @@ hta_status_t hta_forward_seqpar(hta_comm_t comm, const hta_shape_t *shape_local,
         if (api.GroupEnd() != 0) return HTA_ERR_NCCL;
     }
     // 3) merge the P prefix partials with the tree partial of heads [r*Hp, (r+1)*Hp)
-    if ((rc = phase_merge(g, w, r, q, k_tree, v_tree, mask, mask_batch_stride, o, lse_out, gather_output, st)) !=
-        HTA_OK)
+    if ((rc = phase_merge(g, w, r, q, k_tree, v_tree, mask, mask_batch_stride, parents, parents_bs,
+                          P > 1 ? w.recvb : w.sendb, o, lse_out, gather_output, st)) != HTA_OK)
         return rc;
     if (!gather_output) return HTA_OK;
     // 4) all-gather of the head slices, then [P][B,T,Hp,d] -> [B,T,H,d]
@@ -306,6 +315,28 @@ hta_status_t hta_forward_seqpar(hta_comm_t comm, const hta_shape_t *shape_local,
     }
     if (api.GroupEnd() != 0) return HTA_ERR_NCCL;
     return phase_reassemble(g, w, o, lse_out, st);
+}
+
+extern "C" {
+
+hta_status_t hta_forward_seqpar(hta_comm_t comm, const hta_shape_t *shape_local, const void *q,
+                                const void *k_cache_local, const void *v_cache_local,
+                                const int32_t *cache_seqlens_local, const void *k_tree, const void *v_tree,
+                                const uint8_t *mask, int64_t mask_batch_stride, void *o, float *lse_out,
+                                int32_t gather_output, void *ws, size_t ws_bytes, hta_stream_t stream) {
+    if (mask == nullptr) return HTA_ERR_INVALID_ARGUMENT;
+    return seqpar_forward(comm, shape_local, q, k_cache_local, v_cache_local, cache_seqlens_local, k_tree, v_tree,
+                          mask, mask_batch_stride, nullptr, 0, o, lse_out, gather_output, ws, ws_bytes, stream);
+}
+
+hta_status_t hta_forward_seqpar_tree(hta_comm_t comm, const hta_shape_t *shape_local, const void *q,
+                                     const void *k_cache_local, const void *v_cache_local,
+                                     const int32_t *cache_seqlens_local, const void *k_tree, const void *v_tree,
+                                     const int32_t *parents, int64_t parents_batch_stride, void *o, float *lse_out,
+                                     int32_t gather_output, void *ws, size_t ws_bytes, hta_stream_t stream) {
+    if (parents == nullptr) return HTA_ERR_INVALID_ARGUMENT;
+    return seqpar_forward(comm, shape_local, q, k_cache_local, v_cache_local, cache_seqlens_local, k_tree, v_tree,
+                          nullptr, 0, parents, parents_batch_stride, o, lse_out, gather_output, ws, ws_bytes, stream);
 }
 
 hta_status_t hta_forward_seqpar_loopback(hta_comm_t comm, const hta_shape_t *shape_local, const void *q,
@@ -345,8 +376,8 @@ hta_status_t hta_forward_seqpar_loopback(hta_comm_t comm, const hta_shape_t *sha
                                 g.blk * sizeof(float), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
                 return HTA_ERR_CUDA;
     for (int r = 0; r < P; ++r)
-        if ((rc = phase_merge(g, w[r], r, q, k_tree, v_tree, mask, mask_batch_stride, o[r], lse(r), gather_output,
-                              st)) != HTA_OK)
+        if ((rc = phase_merge(g, w[r], r, q, k_tree, v_tree, mask, mask_batch_stride, nullptr, 0, w[r].recvb, o[r],
+                              lse(r), gather_output, st)) != HTA_OK)
             return rc;
     if (!gather_output) return HTA_OK;
     // the all-gather: rank src's own slice -> slot src of every rank's gather buffer

@@ -72,6 +72,8 @@ _SIG = {
     "hta_workspace_size_seqpar": (ctypes.c_size_t, [ctypes.POINTER(hta_shape_t), ctypes.c_int32, ctypes.c_int32]),
     "hta_forward_seqpar": (ctypes.c_int, [_P, ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, _P, _P, _P,
                                           ctypes.c_int64, _P, _P, ctypes.c_int32, _P, ctypes.c_size_t, _P]),
+    "hta_forward_seqpar_tree": (ctypes.c_int, [_P, ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, _P, _P, _P,
+                                               ctypes.c_int64, _P, _P, ctypes.c_int32, _P, ctypes.c_size_t, _P]),
     "hta_forward_seqpar_loopback": (ctypes.c_int, [_P, ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, _P, _P, _P,
                                                    ctypes.c_int64, _P, _P, ctypes.c_int32, _P, ctypes.c_size_t,
                                                    _P]),
@@ -501,9 +503,13 @@ class HtaComm:
             raise HtaError("hta_workspace_size_seqpar", 1)
         return n
 
-    def forward(self, q, k_cache_local, v_cache_local, k_tree, v_tree, mask, cache_seqlens_local=None,
+    def forward(self, q, k_cache_local, v_cache_local, k_tree, v_tree, mask=None, cache_seqlens_local=None,
                 gather_output=False, o=None, lse_out=None, ws=None, want_lse=True, scale=None, num_splits=0,
-                stream=None):
+                stream=None, parents=None):
+        """hta_forward_seqpar over this rank's KV slice; the tree as `mask`, or as `parents`
+        (int32 [T] shared or [B, T]: hta_forward_seqpar_tree)."""
+        if (mask is None) == (parents is None):
+            raise ValueError("give exactly one of mask and parents")
         shape = make_shape(q, k_cache=k_cache_local, k_tree=k_tree, scale=scale, num_splits=num_splits)
         B, T, H, d = q.shape
         Hx = H if gather_output else H // self.world_size
@@ -515,6 +521,16 @@ class HtaComm:
         ws_given = ws
         if ws is None or ws.numel() < n:
             ws = torch.empty(n, dtype=torch.uint8, device=q.device)
+        if parents is not None:
+            par = parents if parents.dtype == torch.int32 and parents.is_contiguous() else \
+                parents.to(torch.int32).contiguous()
+            _check("hta_forward_seqpar_tree", lib().hta_forward_seqpar_tree(
+                self.handle, ctypes.byref(shape), _ptr(q), _ptr(k_cache_local), _ptr(v_cache_local),
+                _ptr(cache_seqlens_local), _ptr(k_tree), _ptr(v_tree), _ptr(par), 0 if par.dim() == 1 else par.stride(0),
+                _ptr(o), _ptr(lse_out), 1 if gather_output else 0, _ptr(ws), ws.numel() * ws.element_size(),
+                _stream(stream)))
+            _hold(stream, None if ws is ws_given else ws, None if par is parents else par)
+            return o, lse_out
         mbs = 0 if mask.dim() == 2 else mask.stride(0)
         _check("hta_forward_seqpar", lib().hta_forward_seqpar(
             self.handle, ctypes.byref(shape), _ptr(q), _ptr(k_cache_local), _ptr(v_cache_local),

@@ -426,13 +426,15 @@ def test_fused_tree_pass_edge_cases(cuda_device, case):
     (2, 200, 4, 2, 64, 900, ("random_forest", "star")),   # two tree tiles, forests (several roots)
     (1, 256, 16, 4, 128, 700, ("chain",)),                # T = 256, depth 255
     (3, 30, 10, 2, 128, 500, ("heap_binary", "roots", "random")),  # G = 5
+    (1, 8, 1, 1, 64, 256, ("heap_binary",), "fp32"),      # the toy config (fp32 SIMT prefix)
 ])
 def test_forward_tree_from_parents(cuda_device, case):
     """hta_forward_tree derives each row's visible tree keys from the parent array inside the
     kernels (Z4).  Its result is bit-identical to hta_forward over the mask hta_build_tree_mask
     writes, and matches the oracle over the oracle's tree mask."""
-    B, T, H, Hkv, d, N, kinds = case
-    w = make_workload(B, T, H, Hkv, d, N, "bf16", dist="V1", seed=29, tree="beam")
+    B, T, H, Hkv, d, N, kinds = case[:7]
+    dt = case[7] if len(case) > 7 else "bf16"
+    w = make_workload(B, T, H, Hkv, d, N, dt, dist="V1", seed=29, tree="beam")
     par = torch.stack([tree_parents(kinds[b % len(kinds)], T, seed=b) for b in range(B)])
     shared = len(kinds) == 1
     x = to_dev(w, cuda_device)
@@ -443,7 +445,7 @@ def test_forward_tree_from_parents(cuda_device, case):
     m_dev = torch.stack([hta.hta_build_tree_mask(par[0 if shared else b].to(cuda_device)) for b in range(B)])
     om, lm = hta.hta_forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], m_dev)
     torch.cuda.synchronize()
-    compare(o, l, o_ref, l_ref, "bf16", f"forward_tree {case}")
+    compare(o, l, o_ref, l_ref, dt, f"forward_tree {case}")
     assert torch.equal(o, om) and torch.equal(l, lm), "hta_forward_tree differs from hta_forward over the built mask"
 
 

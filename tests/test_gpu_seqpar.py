@@ -70,3 +70,21 @@ def test_seqpar_step_in_cuda_graph(cuda_device, comm):
     torch.cuda.synchronize()
     assert torch.equal(o, o_e) and torch.equal(lse, l_e)
     assert not comm.async_error()
+
+
+@pytest.mark.parametrize("gather", [False, True])
+def test_seqpar_tree_from_parents(cuda_device, comm, gather):
+    """hta_forward_seqpar_tree (the tree as its parent array; the final merge walks it) is
+    bit-identical to hta_forward_seqpar over the mask hta_build_tree_mask writes, per-batch trees."""
+    w = make_workload(2, 40, 8, 2, 128, 1500, "bf16", dist="V1", seed=12, tree="random")
+    x = to_dev(w, cuda_device)
+    par = torch.stack([w.parents[b] for b in range(2)]).to(torch.int32).to(cuda_device)
+    mask = torch.stack([hta.hta_build_tree_mask(par[b]) for b in range(2)])
+    o_m, l_m = comm.forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], mask, cache_seqlens_local=x["sl"],
+                            gather_output=gather)
+    o_p, l_p = comm.forward(x["q"], x["kc"], x["vc"], x["kt"], x["vt"], cache_seqlens_local=x["sl"],
+                            gather_output=gather, parents=par)
+    torch.cuda.synchronize()
+    assert torch.equal(o_m, o_p) and torch.equal(l_m, l_p)
+    o_ref, l_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, oracle_masks(w), seqlens=w.seqlens)
+    compare(o_p, l_p, o_ref, l_ref, "bf16", "seqpar_tree P=1")
