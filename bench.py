@@ -281,7 +281,7 @@ def main():
 
     side = torch.cuda.Stream(device=dev)
 
-    def step(x, events=None):
+    def step(x, events=None, tree_ready=None):
         """One verification step: a0 (the tree mask, kept for the other layers of the step) and
         a6 (the accepted path: it needs only the tree and the target's argmax) in one launch on a
         forked stream, beside a1-a4 (a5 for N > 1) on the current stream, which derives each
@@ -290,14 +290,18 @@ def main():
         cur = torch.cuda.current_stream()
         side.wait_stream(cur)
         with torch.cuda.stream(side):
+            if tree_ready is not None:
+                side.wait_event(tree_ready)
             hta.hta_tree_step(x["parents"], x["draft"], x["tgt"], root=0, context_argmax=ctx, mask=mask,
                               path=path, path_len=plen, bonus=bonus)                         # a0 + a6
         if seqpar:                                                                          # a1-a5
+            if tree_ready is not None:
+                cur.wait_event(tree_ready)
             comm.forward(x["q"], kc, vc, x["kt"], x["vt"], cache_seqlens_local=sl, o=o, lse_out=lse, ws=wsb,
                          parents=x["parents"])
         else:                                                                               # a1-a4
             hta.hta_forward_tree(x["q"], kc, vc, x["kt"], x["vt"], x["parents"], cache_seqlens=sl, o=o,
-                                 lse_out=lse, ws=wsb, events=events)
+                                 lse_out=lse, ws=wsb, events=events, tree_ready=tree_ready)
         cur.wait_stream(side)
 
     launches_per_step = 4 if seqpar else 3  # tree step; prefix, (local merge, final merge | tree/merge)
@@ -312,10 +316,22 @@ def main():
     torch.cuda.synchronize()
 
     # The step and the end-to-end step (H2D of the step's inputs from pinned memory, the step,
-    # D2H of O and the accepted path) are captured once as CUDA graphs and replayed.
+    # D2H of O and the accepted path) are captured once as CUDA graphs and replayed.  In the
+    # end-to-end step only q gates the prefix pass: the tree K/V, parents and tokens are copied on
+    # another stream beside it, and only the tree step and the kernel after the prefix wait for them.
+    copy_stream = torch.cuda.Stream(device=dev)
+    tree_ev = torch.cuda.Event()
+    q_bytes = d_in["q"].numel() * d_in["q"].element_size()  # (q is the first field of the packed buffer)
+
     def e2e_body():
-        e2e_buf.copy_(host_buf, non_blocking=True)
-        step(e2e_in)
+        cur = torch.cuda.current_stream()
+        e2e_buf[:q_bytes].copy_(host_buf[:q_bytes], non_blocking=True)
+        copy_stream.wait_stream(cur)  # (after q: two H2D copies at once would share the link)
+        with torch.cuda.stream(copy_stream):
+            e2e_buf[q_bytes:].copy_(host_buf[q_bytes:], non_blocking=True)
+            tree_ev.record()
+        step(e2e_in, tree_ready=tree_ev)
+        cur.wait_stream(copy_stream)
         out_host.copy_(out_buf, non_blocking=True)
 
     e2e_buf, e2e_in = packed({k: (v.shape, v.dtype) for k, v in src.items()}, dev)
@@ -470,8 +486,9 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
         "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "t_us": dist_us(e2e_times),
-                "note": ("per-step inputs (q, tree K/V, parents, draft/target tokens) H2D as one copy from a pinned "
-                         "staging buffer, O + accepted path D2H as one copy; KV cache resident; " + graph_note)},
+                "note": ("per-step inputs from a pinned staging buffer: q H2D on the launch stream (it gates the "
+                         "prefix pass), tree K/V + parents + draft/target tokens H2D on another stream beside it; O + "
+                         "accepted path D2H as one copy; KV cache resident; " + graph_note)},
         "roofline": roof,
     }
 

@@ -178,13 +178,16 @@ hta_status_t hta_forward_ex(const hta_shape_t *shape, const void *q, const void 
  *              by the batch), parents[t] in [-1, t)
  *   ev_prefix_begin / ev_prefix_end  optional cudaEvent_t recorded around the prefix kernel,
  *              as in hta_forward_timed (NULL: none)
+ *   tree_inputs_ready  optional cudaEvent_t: k_tree, v_tree and parents may still be in flight
+ *              (e.g. copied from the host on another stream); only the kernel after the prefix
+ *              pass waits for it, as in hta_forward_ex (the tree pass then runs there)
  * Other arguments, layout, ownership and errors as hta_forward. */
 hta_status_t hta_forward_tree(const hta_shape_t *shape, const void *q, const void *k_cache,
                               const void *v_cache, const int32_t *cache_seqlens,
                               const void *k_tree, const void *v_tree, const int32_t *parents,
                               int64_t parents_batch_stride, void *o, float *lse_out, void *ws,
                               size_t ws_bytes, hta_stream_t stream, void *ev_prefix_begin,
-                              void *ev_prefix_end);
+                              void *ev_prefix_end, void *tree_inputs_ready);
 
 /* hybrid_tree_attention over a PAGED KV cache (the block-table layout of
  * flash_attn_with_kvcache, for batched serving): as hta_forward (bf16 only), with

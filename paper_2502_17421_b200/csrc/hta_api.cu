@@ -642,10 +642,11 @@ hta_status_t hta_forward_paged(const hta_shape_t *shape, const void *q, const vo
 hta_status_t hta_forward_tree(const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,
                               const int32_t *cache_seqlens, const void *k_tree, const void *v_tree,
                               const int32_t *parents, int64_t parents_batch_stride, void *o, float *lse_out, void *ws,
-                              size_t ws_bytes, hta_stream_t stream, void *ev_prefix_begin, void *ev_prefix_end) {
+                              size_t ws_bytes, hta_stream_t stream, void *ev_prefix_begin, void *ev_prefix_end,
+                              void *tree_inputs_ready) {
     if (parents == nullptr) return HTA_ERR_INVALID_ARGUMENT;
     return forward_impl(nullptr, shape, q, k_cache, v_cache, cache_seqlens, k_tree, v_tree, nullptr, 0, o, lse_out, ws,
-                        ws_bytes, stream, ev_prefix_begin, ev_prefix_end, nullptr, nullptr, parents,
+                        ws_bytes, stream, ev_prefix_begin, ev_prefix_end, nullptr, tree_inputs_ready, parents,
                         parents_batch_stride);
 }
 

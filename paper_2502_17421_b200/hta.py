@@ -50,7 +50,7 @@ _SIG = {
     "hta_forward_ex": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, _P, _P, _P, ctypes.c_int64, _P, _P,
                                       _P, ctypes.c_size_t, _P, _P]),
     "hta_forward_tree": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, _P, _P, _P, ctypes.c_int64,
-                                        _P, _P, _P, ctypes.c_size_t, _P, _P, _P]),
+                                        _P, _P, _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "hta_forward_paged": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, _P, _P, ctypes.c_int32, ctypes.c_int32, _P,
                                          ctypes.c_int32, _P, _P, _P, _P, ctypes.c_int64, _P, _P, _P, ctypes.c_size_t,
                                          _P]),
@@ -275,10 +275,12 @@ def hta_forward(q, k_cache, v_cache, k_tree, v_tree, mask, cache_seqlens=None, o
 
 def hta_forward_tree(q, k_cache, v_cache, k_tree, v_tree, parents, cache_seqlens=None, o=None, lse_out=None,
                      ws=None, want_lse=True, scale=None, num_splits=0, max_seqlen=0, stream=None,
-                     events=None) -> Tuple[torch.Tensor, Optional[torch.Tensor]]:
+                     events=None, tree_ready=None) -> Tuple[torch.Tensor, Optional[torch.Tensor]]:
     """hta_forward with the tree as its parent array (int32 [T] shared, or [B, T]); each row's
     visible tree keys are derived in the kernels (no mask input).  `events` = optional (begin,
-    end) torch.cuda.Event pair recorded around the prefix kernel."""
+    end) torch.cuda.Event pair recorded around the prefix kernel; `tree_ready` = a
+    torch.cuda.Event the kernel after the prefix pass waits for (k_tree / v_tree / parents may
+    still be in flight)."""
     shape = make_shape(q, k_cache=k_cache, k_tree=k_tree, scale=scale, num_splits=num_splits, max_seqlen=max_seqlen)
     B, T, H, d = q.shape
     par = parents if parents.dtype == torch.int32 and parents.is_contiguous() else parents.to(torch.int32).contiguous()
@@ -291,7 +293,8 @@ def hta_forward_tree(q, k_cache, v_cache, k_tree, v_tree, parents, cache_seqlens
     ev0, ev1 = (None, None) if events is None else (ctypes.c_void_p(e.cuda_event) for e in events)
     _check("hta_forward_tree", lib().hta_forward_tree(
         ctypes.byref(shape), _ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(cache_seqlens), _ptr(k_tree), _ptr(v_tree),
-        _ptr(par), pbs, _ptr(o), _ptr(lse_out), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream), ev0, ev1))
+        _ptr(par), pbs, _ptr(o), _ptr(lse_out), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream), ev0, ev1,
+        None if tree_ready is None else ctypes.c_void_p(tree_ready.cuda_event)))
     _hold(stream, None if ws is ws_given else ws, None if par is parents else par)
     return o, lse_out
 
