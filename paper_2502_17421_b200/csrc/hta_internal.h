@@ -9,9 +9,14 @@
 
 namespace hta {
 
-// Keys per KV tile of the prefix pass: TMEM holds three 128-column S/P buffers and the
-// 128-column O accumulator (512 columns in all).
-constexpr int kBlockN = 128;
+// Keys per KV tile of the prefix pass: TMEM holds 384 / kBlockN S/P buffers of kBlockN columns
+// and the 128-column O accumulator (512 columns in all): three 128-key buffers (96-key tiles with
+// four buffers measured slower: profiles/r02_experiments.md).
+#ifndef HTA_BLOCK_N
+#define HTA_BLOCK_N 128
+#endif
+constexpr int kBlockN = HTA_BLOCK_N;
+static_assert(kBlockN == 96 || kBlockN == 128, "96-key tiles (four S/P buffers) or 128 (three)");
 constexpr int kSimtBlock = 16;   // key block (split granularity) of the fp32 SIMT prefix pass
 constexpr int kRowsPerTile = 128;  // rows of one tcgen05 M=128 tile
 

@@ -188,11 +188,6 @@ __device__ __forceinline__ uint32_t tree_chunk_bits(const uint8_t *mrow, int T, 
     return bits;
 }
 
-// Fused tree pass: set S to -inf in TMEM for the keys of a tree tile the row's mask hides.  The
-// calling thread's 64 S values of the tile (two 32-column chunks, 16x32bx2 shape, half offset 64)
-// start at TMEM address `at`; mrow = the row's mask bytes (nullptr: a padding row, all hidden),
-// k0 = the tree key of the first of the 64 columns.  Not inlined: keeps the softmax loop's
-// schedule independent of this rarely taken path.
 // Visibility bits of tree keys [k0, k0 + 64) for token t derived from the parent array (hta_forward
 // _tree): t and its ancestors, walking parent links (Z4); a chain that meets an invalid link
 // (parents[a] < -1 or >= a) makes the row all-hidden, exactly as hta_build_tree_mask's row.
@@ -210,22 +205,29 @@ __device__ __forceinline__ void ancestor_bits64(const int32_t *par, int t, int k
     }
 }
 
-// mrow: the row's mask bytes; or (mrow == nullptr, par != nullptr) the parent array and the row's
-// token t; neither: a padding row (all hidden).
+// Fused tree pass: set S to -inf in TMEM for the keys of a tree tile the row's mask hides.  The
+// calling thread's HALF S values of the tile (16-column chunks, 16x32bx2 shape, half offset HALF)
+// start at TMEM address `at`; k0 = the tree key of the first of them.  Visibility: mrow = the row's
+// mask bytes; or (mrow == nullptr, par != nullptr) the parent array and the row's token t;
+// neither: a padding row (all hidden).  Not inlined: keeps the softmax loop's schedule
+// independent of this rarely taken path.
+template <int HALF>
 __device__ __noinline__ void mask_tree_tile(uint32_t at, const uint8_t *mrow, const int32_t *par, int t, int T,
                                             int k0) {
+    static_assert(HALF % 16 == 0 && HALF <= 64, "16-column chunks, at most 64 columns");
     uint32_t pw[2] = {0u, 0u};
     if (mrow == nullptr && par != nullptr) ancestor_bits64(par, t, k0, pw);
 #pragma unroll 1
-    for (int ch = 0; ch < 2; ++ch) {
-        float sm[32];
-        tmem_ld_x32_nowait<64>(at + ch * 32, sm);
-        tmem_ld_wait_fence<32>(sm);
-        const uint32_t bits = mrow != nullptr ? tree_chunk_bits(mrow, T, k0 + ch * 32) : pw[ch];
+    for (int c0 = 0; c0 < HALF; c0 += 16) {
+        float sm[16];
+        tmem_ld_x16_nowait<HALF>(at + c0, sm);
+        tmem_ld_wait_fence<16>(sm);
+        const uint32_t bits = mrow != nullptr ? tree_chunk_bits(mrow, T, k0 + c0) : pw[c0 >> 5] >> (c0 & 31);
 #pragma unroll
-        for (int cc = 0; cc < 32; ++cc)
+        for (int cc = 0; cc < 16; ++cc)
             if (!((bits >> cc) & 1u)) sm[cc] = -INFINITY;
-        tmem_st_16x32_split<64>(at + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(sm));
+        tmem_st_16x16_split_nowait<HALF>(at + c0, reinterpret_cast<const uint32_t *>(sm));
+        tmem_st_wait();
     }
 }
 
@@ -271,7 +273,8 @@ static_assert(HTA_MMA_SLOT == 1 || HTA_MMA_SLOT == 3, "MMA slot");
 template <int D, bool PAIR>
 struct TcCfg {
     static_assert(!PAIR || D == 128, "CTA pairs split the 128-column V tile in two 64-column halves");
-    static_assert(kBlockN == 128, "three 128-column S/P buffers + O fill the 512 TMEM columns");
+    static constexpr int kSBufs = (512 - 128) / kBlockN;          // S/P buffers beside the 128-column O
+    static_assert(kSBufs * kBlockN + 128 == 512, "S/P buffers + O fill the 512 TMEM columns");
     static constexpr int kKB = D / 64;                          // 128-byte K-blocks of the head dim
     static constexpr int kRegionBytes = 128 * 128;              // 128 rows x 128 B
     static constexpr int kQBytes = kRowsPerTile * D * 2;        // this CTA's 128 Q rows
@@ -282,7 +285,6 @@ struct TcCfg {
     static constexpr int kRingBytes = 192 * 1024;
     static constexpr int kSlotsK = (kRingBytes / 2) / kKBytes;
     static constexpr int kSlotsV = (kRingBytes / 2) / kVBytes;
-    static constexpr int kSBufs = 3;
     static constexpr int kGroupWarps = 8;                       // softmax warps per group (two per SMSP)
     static constexpr int kThreads = 32 * (4 + 2 * kGroupWarps);
     static constexpr int kVOff = kQBytes + kSlotsK * kKBytes;   // start of the V ring
@@ -295,7 +297,7 @@ struct TcCfg {
     static_assert(8 * 128 * 4 <= kSlotsK * kKBytes, "the epilogue exchange reuses the K ring");
 };
 
-// TMEM column map: S/P buffer b at 128*b (b = 0, 1, 2), O at 384.
+// TMEM column map: S/P buffer b at kBlockN*b, O at 384.
 __device__ __forceinline__ uint32_t s_col(int buf) { return static_cast<uint32_t>(kBlockN * buf); }
 constexpr uint32_t kOCol = 384u;
 
@@ -935,7 +937,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             // S, in a function of its own so that the exponential loop
             // is scheduled exactly as for the cache tiles
             if (tree_tile)
-                mask_tree_tile(tmem + lane_off + s_col(buf), grow < p.M && p.parents == nullptr ? mask_row() : nullptr,
+                mask_tree_tile<kHalf>(tmem + lane_off + s_col(buf), grow < p.M && p.parents == nullptr ? mask_row() : nullptr,
                                grow < p.M ? p.parents + b * p.par_bs : nullptr, grow / p.G, p.T,
                                (j - nc) * kBlockN + chalf * kHalf);
             const bool last = !tree_tile && j == nc - 1;  // the split's last cache tile
@@ -943,10 +945,13 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             // chunk's values are loaded, turned into packed P and dead before the next chunk
             // loads, so the softmax fits its register budget without spills.  Keys past the split
             // end -> -inf (last tile only; the empty asm keeps that a real branch).
-            constexpr int kChunk = 32;
+            constexpr int kChunk = kHalf % 32 == 0 ? 32 : 16;
             float s[kChunk];
             auto load_s = [&](int ch) {
-                tmem_ld_x32_nowait<kHalf>(tmem + lane_off + s_col(buf) + ch * kChunk, s);
+                if constexpr (kChunk == 32)
+                    tmem_ld_x32_nowait<kHalf>(tmem + lane_off + s_col(buf) + ch * kChunk, s);
+                else
+                    tmem_ld_x16_nowait<kHalf>(tmem + lane_off + s_col(buf) + ch * kChunk, s);
                 tmem_ld_wait_fence<kChunk>(s);
                 if (last && tail_valid < kBlockN) {
                     asm volatile("" ::: "memory");
@@ -1054,8 +1059,13 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             }
             // P_j over S_j in TMEM (columns [Ch/2, Ch/2 + 32)), without waiting
             if (!(HTA_DIAG & 1)) {
-                tmem_st_16x16_split_nowait<kHalf / 2>(tmem + lane_off + s_col(buf), pk);
-                tmem_st_16x16_split_nowait<kHalf / 2>(tmem + lane_off + s_col(buf) + 16, pk + 16);
+#pragma unroll
+                for (int w0 = 0; w0 < kHalf / 2; w0 += 16) {  // 16 packed words per store, then the rest
+                    if (kHalf / 2 - w0 >= 16)
+                        tmem_st_16x16_split_nowait<kHalf / 2>(tmem + lane_off + s_col(buf) + w0, pk + w0);
+                    else
+                        tmem_st_16x8_split_nowait<kHalf / 2>(tmem + lane_off + s_col(buf) + w0, pk + w0);
+                }
             }
             // O holds the tiles before j in scale m_prev; raise it to m_fin (after PV_{j-1})
             const bool need = j > 0 && m_fin != m_prev;
@@ -1195,7 +1205,7 @@ cudaError_t launch_prefix_tc(const PrefixParams &p, const CUtensorMap &tq, const
         if (p.d == 64 && p.nt == 1) return launch_tc<64, false, true>(p, tq, tk, tv, tkt, tvt, s);
         return cudaErrorInvalidValue;
     }
-    if (p.tree_tiles < 0 || p.tree_tiles > 2) return cudaErrorInvalidValue;
+    if (p.tree_tiles < 0 || p.tree_tiles > (256 + kBlockN - 1) / kBlockN) return cudaErrorInvalidValue;
     if (p.tree_tiles > 0) {  // the fused tree pass (single-CTA row groups, hta_api.cu forward_impl)
         if (p.nt != 1) return cudaErrorInvalidValue;
         if (p.d == 128) return launch_tc<128, false, false, true>(p, tq, tk, tv, tkt, tvt, s);
