@@ -222,6 +222,8 @@ def main():
     ap.add_argument("--no-all-configs", action="store_true")
     ap.add_argument("--no-scale-config", action="store_true", help="skip the 128k/T=128 step line")
     ap.add_argument("--ref-budget", type=float, default=60.0, help="seconds of oracle work for --impl reference")
+    ap.add_argument("--nccl-exchange", action="store_true", help="sequence parallel: NCCL all-to-all instead of the "
+                    "peer-memory exchange")
     ap.add_argument("--force-seqpar", action="store_true",
                     help="run the sequence-parallel step (NCCL) even on one rank: checks the N > 1 code path "
                          "on a single GPU")
@@ -246,6 +248,22 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=ws)
     comm = hta.HtaComm(rank, ws) if seqpar else None
+    exchange = None
+    if seqpar and not args.nccl_exchange:
+        # the peer-memory exchange (split combine writing into the peers' receive buffers over
+        # NVLink), sized for both workloads this run times; NCCL if any rank cannot set it up
+        shapes = []
+        for nm in {args.workload, SCALE_WORKLOAD}:
+            c = CONFIGS[nm]
+            s_ = hta.hta_shape_t()
+            s_.B, s_.T, s_.H, s_.H_kv, s_.d = c["B"], c["T"], c["H"], c["H_kv"], c["d"]
+            shapes.append(s_)
+        try:
+            exchange = "peer memory (P2P stores over NVLink, IPC-mapped)" if comm.enable_p2p(shapes) else None
+        except Exception as exc:  # (NCCL stays)
+            print(f"peer-memory exchange unavailable: {exc}", file=sys.stderr)
+    if seqpar and exchange is None:
+        exchange = "NCCL all-to-all"
 
     # ---- inputs (seeded, synthetic, BASELINE.json workload shape); KV cache resident in HBM
     w = config_workload(args.workload, seed=0)
@@ -305,6 +323,26 @@ def main():
         cur.wait_stream(side)
 
     launches_per_step = 4 if seqpar else 3  # tree step; prefix, (local merge, final merge | tree/merge)
+
+    if seqpar and exchange.startswith("peer"):
+        # Validate the peer-memory exchange on this run's inputs before timing it: its step must
+        # equal the NCCL-exchange step bit for bit on every rank, with no peer wait given up;
+        # otherwise the NCCL exchange is timed instead.
+        def one(p2p_on):
+            comm.set_p2p(p2p_on)
+            oo, ll = comm.forward(d_in["q"], kc, vc, d_in["kt"], d_in["vt"], cache_seqlens_local=sl, ws=wsb,
+                                  parents=d_in["parents"])
+            torch.cuda.synchronize()
+            return oo.clone(), ll.clone()
+        o_p, l_p = one(True)
+        o_n, l_n = one(False)
+        good = (not comm.p2p_error()) and torch.equal(o_p, o_n) and torch.equal(l_p, l_n)
+        t = torch.tensor([1 if good else 0], dtype=torch.int32, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
+        if int(t.item()) == 1:
+            comm.set_p2p(True)
+        else:
+            exchange = "NCCL all-to-all (the peer-memory exchange failed its check)"
 
     def barrier():
         if seqpar:
@@ -473,7 +511,7 @@ def main():
         "setup": {"parallelism": f"seq{ws}",
                   "l2": "flushed before every timed step (512 MiB write, then two reads of it; untimed)",
                   "step": ("a0 mask + a6 accept (hta_tree_step) on a forked stream | " +
-                           ("hta_forward_seqpar_tree (a1-a5, NCCL exchange" if seqpar else "hta_forward_tree (a1-a4") +
+                           (f"hta_forward_seqpar_tree (a1-a5, {exchange} exchange" if seqpar else "hta_forward_tree (a1-a4") +
                            "; visibility from the parent array); " + graph_note)},
         "t_us": dist_us(times),
         "kernel_us": {"prefix": None if prefix_ms is None else prefix_ms * 1e3,

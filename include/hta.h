@@ -330,6 +330,33 @@ hta_status_t hta_comm_create_loopback(int32_t nranks, hta_comm_t *comm);
  * it before enqueueing.  A loopback communicator always returns HTA_OK. */
 hta_status_t hta_comm_async_error(hta_comm_t comm);
 
+/* Peer-memory exchange for the sequence-parallel step (the fused compute +
+ * collective path over NVLink / NVSwitch).  Instead of the NCCL all-to-all, the split-combine
+ * kernel of rank r writes head block q of its prefix partial straight into rank q's receive
+ * buffer (P2P stores over NVLink to an IPC-mapped allocation), one signal kernel fences at system
+ * scope and raises rank r's flag in every peer's flag array, and the final merge waits for all P
+ * flags of its step.  Receive buffers are double-buffered by a device-side step counter, so the
+ * step can be captured in a CUDA graph and replayed.  Used by hta_forward_seqpar[_tree] (and the
+ * loopback forward) whenever it is enabled, gather_output is 0 and the step's block fits the
+ * capacity; otherwise the NCCL path runs.
+ *   hta_comm_p2p_alloc: allocate this rank's buffers on the current device for blocks of at most
+ *     block_capacity_floats floats (B*T*(H/P)*d + B*(H/P)*T for the shapes to be run), and write
+ *     its two CUDA IPC handles (receive buffer, flags; 64 bytes each) to ipc_handles_128.  For a
+ *     loopback communicator it allocates every virtual rank's buffers, wires them to each other
+ *     and enables the exchange at once (the handles are zeroed).
+ *   hta_comm_p2p_open: ipc_handles_all = the nranks ranks' 128-byte handles in rank order (e.g.
+ *     all-gathered over the process group); opens the peers' buffers and enables the exchange.
+ * At most 8 ranks (one NVSwitch node): HTA_ERR_UNSUPPORTED beyond.  Errors leave the exchange
+ * disabled (HTA_ERR_CUDA: an allocation, IPC export or IPC open failed). */
+hta_status_t hta_comm_p2p_alloc(hta_comm_t comm, size_t block_capacity_floats, void *ipc_handles_128);
+hta_status_t hta_comm_p2p_open(hta_comm_t comm, const void *ipc_handles_all);
+/* Switch an allocated and opened peer-memory exchange off (0: the NCCL exchange runs) or on. */
+hta_status_t hta_comm_p2p_set(hta_comm_t comm, int32_t enabled);
+/* HTA_OK, or HTA_ERR_CUDA once a final merge gave up waiting (100 ms) for a peer's flag (a peer
+ * that never signals must not hang the step; that step's output is garbage).  Synchronous (reads
+ * a device word). */
+hta_status_t hta_comm_p2p_error(hta_comm_t comm);
+
 /* Workspace for hta_forward_seqpar: split partials + send/receive buffers. */
 size_t hta_workspace_size_seqpar(const hta_shape_t *shape_local, int32_t num_sms,
                                  int32_t nranks);

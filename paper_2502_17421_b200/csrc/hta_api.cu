@@ -815,7 +815,7 @@ namespace hta {
 
 hta_status_t seqpar_local_parts(const hta_shape_t *shape, const void *q, const void *k, const void *v,
                                 const int32_t *seqlens, float *parts_ws, size_t parts_bytes, float *sendb, int P,
-                                cudaStream_t st) {
+                                cudaStream_t st, const P2pOut *p2p) {
     Shape sh;
     hta_status_t r = check_shape(shape, &sh);
     if (r != HTA_OK) return r;
@@ -845,13 +845,27 @@ hta_status_t seqpar_local_parts(const hta_shape_t *shape, const void *q, const v
     p.lse = sendb + int64_t(s.B) * s.T * Hp * s.d;
     p.lse_block_stride = blk;
     p.out_hb = Hp;
+    if (p2p != nullptr) {  // straight into the peers' receive buffers
+        if (P > kMaxP2pRanks) return HTA_ERR_INVALID_ARGUMENT;
+        p.p2p_role = 1;
+        p.p2p_epoch = p2p->epoch;
+        p.p2p_parity = p2p->parity;
+        p.p2p_lse_off = int64_t(s.B) * s.T * Hp * s.d;
+        p.p2p_counter = p2p->counter;
+        p.p2p_nranks = P;
+        p.p2p_rank = p2p->rank;
+        for (int i = 0; i < P; ++i) {
+            p.p2p_dst[i] = p2p->dst[i];
+            p.p2p_peer_flags[i] = p2p->peer_flags[i];
+        }
+    }
     return launch_tree_merge(p, s.d, s.dtype, HTA_FP32, true, st) == cudaSuccess ? HTA_OK : HTA_ERR_CUDA;
 }
 
 hta_status_t seqpar_final_merge(const hta_shape_t *shape, int P, int rank, const void *q, const void *kt,
                                 const void *vt, const uint8_t *mask, int64_t mask_bs, const int32_t *parents,
                                 int64_t par_bs, const float *recvb, size_t blk_floats, void *o, float *lse,
-                                cudaStream_t st) {
+                                cudaStream_t st, const P2pIn *p2p) {
     Shape sh;
     hta_status_t r = check_shape(shape, &sh);
     if (r != HTA_OK) return r;
@@ -882,6 +896,12 @@ hta_status_t seqpar_final_merge(const hta_shape_t *shape, int P, int rank, const
     p.os2 = s.d;
     p.lse = lse;
     p.out_hb = Hp;
+    if (p2p != nullptr) {  // this step's half of the double-buffered receive blocks, once flagged
+        p.p2p_role = 2;
+        p.p2p_epoch = p2p->epoch;
+        p.p2p_flags = p2p->flags;
+        p.p2p_parity = p2p->parity;
+    }
     return launch_tree_merge(p, s.d, s.dtype, s.dtype, false, st) == cudaSuccess ? HTA_OK : HTA_ERR_CUDA;
 }
 

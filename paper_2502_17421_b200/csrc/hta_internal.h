@@ -70,6 +70,8 @@ struct PrefixParams {
     int64_t o_split_stride, lse_split_stride;  // elements between splits
 };
 
+constexpr int kMaxP2pRanks = 8;  // ranks of the peer-memory exchange (one NVSwitch node)
+
 struct TreeMergeParams {
     // Row space: (b, t, hl) with hl in [0, Hr); the global query head is h = h0 + hl.
     int B, T, H, H_kv, G, Hr, h0;
@@ -95,6 +97,22 @@ struct TreeMergeParams {
     float *lse;                       // may be nullptr
     int64_t lse_block_stride;
     int out_hb;
+    // Peer-memory exchange of the sequence-parallel step (p2p_role != 0):
+    //  role 1 (split combine): block blk goes to p2p_dst[blk] + ((*p2p_epoch) & 1) * p2p_parity
+    //         (O) and + p2p_lse_off (LSE), i.e. straight into rank blk's receive buffer, followed by
+    //         a system-scope fence;
+    //  role 2 (final merge): the partials are read at o_parts + (((*p2p_epoch) - 1) & 1) *
+    //         p2p_parity after every p2p_flags[q], q < n_parts, has reached *p2p_epoch.
+    //  role 1 also signals: its last block (p2p_counter, a step-long block counter) raises flag
+    //  p2p_rank in every p2p_peer_flags[q], q < p2p_nranks, to the new step and advances *p2p_epoch.
+    int p2p_role;
+    const uint32_t *p2p_epoch;
+    const uint32_t *p2p_flags;
+    int64_t p2p_parity, p2p_lse_off;
+    float *p2p_dst[kMaxP2pRanks];
+    uint32_t *p2p_counter;
+    uint32_t *p2p_peer_flags[kMaxP2pRanks];
+    int p2p_nranks, p2p_rank;
 };
 
 // Launchers (return cudaGetLastError() of the launch).
@@ -105,6 +123,7 @@ int prefix_tc_smem_bytes(int d, int nt);
 cudaError_t launch_prefix_simt(const PrefixParams &p, cudaStream_t s);
 cudaError_t launch_tree_merge(const TreeMergeParams &p, int d, hta_dtype_t in_dtype, hta_dtype_t out_dtype,
                               bool pdl, cudaStream_t s);
+
 // Geometry of hta_commit_kv (element strides; esize bytes per element).
 struct CommitGeom {
     int T, H_kv, row_bytes, esize;
@@ -138,14 +157,31 @@ inline size_t seqpar_block_floats(int B, int T, int Hp, int d) {
 // Sequence-parallel building blocks (implemented in hta_api.cu, used by seqpar.cu).
 // Local prefix pass over this rank's KV slice, combined into one partial per row laid out
 // destination-major: block p (for rank p) = O [B][T][H/P][d] then LSE [B][H/P][T].
+// Peer-memory exchange: the split combine of rank r writes block q into
+// dst[q] + (epoch & 1) * parity (rank r's slot of rank q's double-buffered receive buffer); the
+// final merge reads its receive buffer's half ((epoch - 1) & 1) once flags[q] >= epoch for all q.
+struct P2pOut {
+    float *dst[kMaxP2pRanks];
+    uint32_t *epoch;        // this rank's step counter
+    uint32_t *counter;      // this rank's block counter of the split combine
+    uint32_t *peer_flags[kMaxP2pRanks];
+    int rank;
+    int64_t parity;
+};
+struct P2pIn {
+    const uint32_t *epoch;
+    const uint32_t *flags;
+    int64_t parity;
+};
 hta_status_t seqpar_local_parts(const hta_shape_t *s, const void *q, const void *k, const void *v,
                                 const int32_t *seqlens, float *parts_ws, size_t parts_bytes, float *sendb, int P,
-                                cudaStream_t st);
+                                cudaStream_t st, const P2pOut *p2p = nullptr);
 // Merge the P received partials (blocks of `blk_floats`) with the tree pass of heads
 // [r*H/P, (r+1)*H/P) into o [B,T,H/P,d] (dtype) and lse [B,H/P,T] (optional).
 // The tree's visibility is the mask, or (mask == nullptr) the parent array (ancestor walk).
 hta_status_t seqpar_final_merge(const hta_shape_t *s, int P, int r, const void *q, const void *kt, const void *vt,
                                 const uint8_t *mask, int64_t mask_bs, const int32_t *parents, int64_t par_bs,
-                                const float *recvb, size_t blk_floats, void *o, float *lse, cudaStream_t st);
+                                const float *recvb, size_t blk_floats, void *o, float *lse, cudaStream_t st,
+                                const P2pIn *p2p = nullptr);
 
 }  // namespace hta

@@ -45,6 +45,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar_addr, uint32_t parity
         : "memory");
     return ok != 0;
 }
+// System-scope acquire load / release store of a 32-bit word in global memory (flags written by
+// peer GPUs over NVLink).
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 // Shared-memory word read/written with volatile semantics (flag hand-over between warps).
 __device__ __forceinline__ uint32_t ld_volatile_shared(const uint32_t *p) {
     uint32_t v;

@@ -180,11 +180,75 @@ hta_status_t phase_reassemble(const Geometry &g, const RankWs &w, void *o, float
 
 }  // namespace
 
+// Peer-memory exchange state of one rank (or of every virtual rank of a loopback communicator):
+// a double-buffered receive buffer recv [2][P][cap] floats (block q = source rank q: O then LSE)
+// and P flags + 1 epoch counter (uint32), and the peers' views of theirs (IPC-mapped over NVLink).
+struct P2pRank {
+    float *recv = nullptr;
+    uint32_t *flags = nullptr;  // [P] flags, [P] step counter, [P+1] block counter, [P+2] error word
+    float *peer_recv[kMaxP2pRanks] = {};
+    uint32_t *peer_flags[kMaxP2pRanks] = {};
+    bool owned = true;          // allocated here (else IPC-opened or a loopback alias)
+};
+
 struct hta_comm_s {
     nccl_comm_t comm;  // nullptr for a loopback communicator
     int nranks;
     int rank;          // -1 for a loopback communicator (it holds every rank)
+    // peer-memory exchange (hta_comm_p2p_*): per rank (one for NCCL, nranks for loopback)
+    bool p2p = false;
+    size_t p2p_cap = 0;  // floats per block
+    std::vector<P2pRank> p2p_ranks;
 };
+
+namespace {
+// rank r's phases 1-3 of the sequence-parallel step over the peer-memory exchange
+hta_status_t p2p_combine(const Geometry &g, const RankWs &w, const hta_comm_s &c, int r, const void *q,
+                         const void *k, const void *v, const int32_t *seqlens, cudaStream_t st) {
+    P2pOut out{};
+    const P2pRank &me = c.p2p_ranks[c.rank >= 0 ? 0 : r];
+    for (int p = 0; p < g.P; ++p) {
+        out.dst[p] = me.peer_recv[p] + size_t(r) * c.p2p_cap;
+        out.peer_flags[p] = me.peer_flags[p];
+    }
+    out.epoch = me.flags + g.P;
+    out.counter = me.flags + g.P + 1;
+    out.rank = r;
+    out.parity = int64_t(g.P) * int64_t(c.p2p_cap);
+    return seqpar_local_parts(&g.s, q, k, v, seqlens, w.parts, w.parts_bytes, w.sendb, g.P, st, &out);
+}
+hta_status_t p2p_merge(const Geometry &g, const hta_comm_s &c, int r, const void *q, const void *kt, const void *vt,
+                       const uint8_t *mask, int64_t mbs, const int32_t *parents, int64_t pbs, void *o, float *lse,
+                       cudaStream_t st) {
+    const P2pRank &me = c.p2p_ranks[c.rank >= 0 ? 0 : r];
+    P2pIn in{me.flags + g.P, me.flags, int64_t(g.P) * int64_t(c.p2p_cap)};
+    return seqpar_final_merge(&g.s, g.P, r, q, kt, vt, mask, mbs, parents, pbs, me.recv, c.p2p_cap, o, lse, st,
+                              &in);
+}
+void p2p_release(hta_comm_s &c) {
+    for (size_t i = 0; i < c.p2p_ranks.size(); ++i) {
+        P2pRank &pr = c.p2p_ranks[i];
+        if (c.rank >= 0)  // NCCL communicator: close the peers' IPC mappings
+            for (int q = 0; q < c.nranks; ++q)
+                if (q != c.rank && pr.peer_recv[q] != nullptr) {
+                    cudaIpcCloseMemHandle(pr.peer_recv[q]);
+                    cudaIpcCloseMemHandle(pr.peer_flags[q]);
+                }
+        if (pr.owned) {
+            cudaFree(pr.recv);
+            cudaFree(pr.flags);
+        }
+    }
+    c.p2p_ranks.clear();
+    c.p2p = false;
+}
+hta_status_t p2p_alloc_rank(P2pRank &pr, int P, size_t cap) {
+    if (cudaMalloc(&pr.recv, 2 * size_t(P) * cap * sizeof(float)) != cudaSuccess) return HTA_ERR_CUDA;
+    if (cudaMalloc(&pr.flags, (P + 3) * sizeof(uint32_t)) != cudaSuccess) return HTA_ERR_CUDA;
+    if (cudaMemset(pr.flags, 0, (P + 3) * sizeof(uint32_t)) != cudaSuccess) return HTA_ERR_CUDA;
+    return cudaDeviceSynchronize() == cudaSuccess ? HTA_OK : HTA_ERR_CUDA;
+}
+}  // namespace
 
 extern "C" {
 
@@ -227,12 +291,93 @@ hta_status_t hta_comm_create_loopback(int32_t nranks, hta_comm_t *comm) {
 hta_status_t hta_comm_destroy(hta_comm_t comm) {
     if (comm == nullptr) return HTA_ERR_INVALID_ARGUMENT;
     hta_status_t r = HTA_OK;
+    p2p_release(*comm);
     if (comm->comm != nullptr) {
         NcclApi &api = nccl();
         if (api.ok && api.CommDestroy(comm->comm) != 0) r = HTA_ERR_NCCL;
     }
     delete comm;
     return r;
+}
+
+hta_status_t hta_comm_p2p_alloc(hta_comm_t comm, size_t block_capacity_floats, void *ipc_handles_128) {
+    if (comm == nullptr || ipc_handles_128 == nullptr || block_capacity_floats == 0) return HTA_ERR_INVALID_ARGUMENT;
+    if (comm->nranks > kMaxP2pRanks) return HTA_ERR_UNSUPPORTED;
+    p2p_release(*comm);
+    const int n = comm->rank >= 0 ? 1 : comm->nranks;
+    comm->p2p_ranks.assign(n, P2pRank{});
+    comm->p2p_cap = (block_capacity_floats + 3) & ~size_t(3);  // (16-byte aligned blocks)
+    for (int i = 0; i < n; ++i) {
+        hta_status_t r = p2p_alloc_rank(comm->p2p_ranks[i], comm->nranks, comm->p2p_cap);
+        if (r != HTA_OK) {
+            p2p_release(*comm);
+            return r;
+        }
+    }
+    if (comm->rank < 0) {  // loopback: every virtual rank's peers are the other virtual ranks' buffers
+        for (int i = 0; i < n; ++i)
+            for (int q = 0; q < n; ++q) {
+                comm->p2p_ranks[i].peer_recv[q] = comm->p2p_ranks[q].recv;
+                comm->p2p_ranks[i].peer_flags[q] = comm->p2p_ranks[q].flags;
+            }
+        std::memset(ipc_handles_128, 0, 128);
+        comm->p2p = true;
+        return HTA_OK;
+    }
+    cudaIpcMemHandle_t h[2];
+    if (cudaIpcGetMemHandle(&h[0], comm->p2p_ranks[0].recv) != cudaSuccess ||
+        cudaIpcGetMemHandle(&h[1], comm->p2p_ranks[0].flags) != cudaSuccess) {
+        p2p_release(*comm);
+        return HTA_ERR_CUDA;
+    }
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    std::memcpy(ipc_handles_128, h, 128);
+    return HTA_OK;
+}
+
+hta_status_t hta_comm_p2p_set(hta_comm_t comm, int32_t enabled) {
+    if (comm == nullptr) return HTA_ERR_INVALID_ARGUMENT;
+    if (enabled && comm->p2p_ranks.empty()) return HTA_ERR_INVALID_ARGUMENT;
+    comm->p2p = enabled != 0 && (comm->rank < 0 || comm->p2p_ranks[0].peer_recv[comm->rank] != nullptr);
+    return enabled && !comm->p2p ? HTA_ERR_INVALID_ARGUMENT : HTA_OK;
+}
+
+hta_status_t hta_comm_p2p_error(hta_comm_t comm) {
+    if (comm == nullptr) return HTA_ERR_INVALID_ARGUMENT;
+    for (const P2pRank &pr : comm->p2p_ranks) {
+        uint32_t err = 0;
+        if (cudaMemcpy(&err, pr.flags + comm->nranks + 2, sizeof(err), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return HTA_ERR_CUDA;
+        if (err != 0) return HTA_ERR_CUDA;
+    }
+    return HTA_OK;
+}
+
+hta_status_t hta_comm_p2p_open(hta_comm_t comm, const void *ipc_handles_all) {
+    if (comm == nullptr || ipc_handles_all == nullptr || comm->p2p_ranks.empty()) return HTA_ERR_INVALID_ARGUMENT;
+    if (comm->rank < 0) return HTA_OK;  // loopback: wired by hta_comm_p2p_alloc
+    P2pRank &me = comm->p2p_ranks[0];
+    const uint8_t *all = static_cast<const uint8_t *>(ipc_handles_all);
+    for (int q = 0; q < comm->nranks; ++q) {
+        if (q == comm->rank) {
+            me.peer_recv[q] = me.recv;
+            me.peer_flags[q] = me.flags;
+            continue;
+        }
+        cudaIpcMemHandle_t h[2];
+        std::memcpy(h, all + size_t(q) * 128, 128);
+        void *pr = nullptr, *pf = nullptr;
+        if (cudaIpcOpenMemHandle(&pr, h[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+            cudaIpcOpenMemHandle(&pf, h[1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            p2p_release(*comm);
+            return HTA_ERR_CUDA;
+        }
+        me.peer_recv[q] = static_cast<float *>(pr);
+        me.peer_flags[q] = static_cast<uint32_t *>(pf);
+    }
+    comm->p2p = true;
+    return HTA_OK;
 }
 
 hta_status_t hta_comm_async_error(hta_comm_t comm) {
@@ -282,6 +427,13 @@ static hta_status_t seqpar_forward(hta_comm_t comm, const hta_shape_t *shape_loc
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const RankWs w = carve(g, ws);
 
+    if (comm->p2p && !gather_output && g.blk <= comm->p2p_cap) {
+        // peer-memory exchange: the split combine writes each head block straight into its rank's
+        // receive buffer over NVLink, one signal kernel flags them, the final merge waits for the flags
+        if ((rc = p2p_combine(g, w, *comm, r, q, k_cache_local, v_cache_local, cache_seqlens_local, st)) != HTA_OK)
+            return rc;
+        return p2p_merge(g, *comm, r, q, k_tree, v_tree, mask, mask_batch_stride, parents, parents_bs, o, lse_out, st);
+    }
     // 1) local prefix pass -> one destination-major partial per row
     if ((rc = phase_local(g, w, q, k_cache_local, v_cache_local, cache_seqlens_local, st)) != HTA_OK) return rc;
     // 2) all-to-all of head slices: block p of sendb goes to rank p, block p of recvb comes from p
@@ -367,6 +519,16 @@ hta_status_t hta_forward_seqpar_loopback(hta_comm_t comm, const hta_shape_t *sha
     for (int r = 0; r < P; ++r) w[r] = carve(g, static_cast<uint8_t *>(ws) + per * r);
     auto sl = [&](int r) { return cache_seqlens_local ? cache_seqlens_local[r] : nullptr; };
     auto lse = [&](int r) { return lse_out ? lse_out[r] : nullptr; };
+    if (comm->p2p && !gather_output && g.blk <= comm->p2p_cap) {  // the peer-memory exchange, all ranks
+        for (int r = 0; r < P; ++r)
+            if ((rc = p2p_combine(g, w[r], *comm, r, q, k_cache_local[r], v_cache_local[r], sl(r), st)) != HTA_OK)
+                return rc;
+        for (int r = 0; r < P; ++r)
+            if ((rc = p2p_merge(g, *comm, r, q, k_tree, v_tree, mask, mask_batch_stride, nullptr, 0, o[r], lse(r),
+                                st)) != HTA_OK)
+                return rc;
+        return HTA_OK;
+    }
     for (int r = 0; r < P; ++r)
         if ((rc = phase_local(g, w[r], q, k_cache_local[r], v_cache_local[r], sl(r), st)) != HTA_OK) return rc;
     // the all-to-all: block dst of rank src's send buffer -> block src of rank dst's receive buffer

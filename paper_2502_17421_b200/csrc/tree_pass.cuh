@@ -224,18 +224,20 @@ __device__ __forceinline__ void merge_row(const TreeMergeParams &p, int b, int t
 #pragma unroll
     for (int e = 0; e < E; ++e) out[e] = ot[e];
     if (p.n_parts > 0) {
+        // (peer-memory exchange, role 2: this step's half of the double-buffered receive blocks)
+        const int64_t par_off = p.p2p_role == 2 ? static_cast<int64_t>((*p.p2p_epoch - 1u) & 1u) * p.p2p_parity : 0;
         const int64_t lrow = (static_cast<int64_t>(b) * p.Hr + hl) * p.T + t;
         const int64_t orow = ((static_cast<int64_t>(b) * p.T + t) * p.Hr + hl) * D + lane * E;
         if (p.n_parts <= kFastParts) {
             // every load of the row in flight at once: one round trip (partials are L2-resident)
             float v16[kFastParts][E];
-            const float ls = lane < p.n_parts ? (CG ? __ldcg(p.lse_parts + lane * p.lse_part_stride + lrow)
-                                                    : p.lse_parts[lane * p.lse_part_stride + lrow])
+            const float ls = lane < p.n_parts ? (CG ? __ldcg(p.lse_parts + par_off + lane * p.lse_part_stride + lrow)
+                                                    : (p.lse_parts + par_off)[lane * p.lse_part_stride + lrow])
                                               : -INFINITY;
 #pragma unroll
             for (int j = 0; j < kFastParts; ++j) {
                 if (j < p.n_parts) {
-                    const float *src = p.o_parts + j * p.o_part_stride + orow;
+                    const float *src = p.o_parts + par_off + j * p.o_part_stride + orow;
                     if (CG)
                         load_cg<E>(src, v16[j]);
                     else
@@ -272,8 +274,8 @@ __device__ __forceinline__ void merge_row(const TreeMergeParams &p, int b, int t
         } else {
         float mx = lse_t;
         for (int s = lane; s < p.n_parts; s += 32)
-            mx = fmaxf(mx, CG ? __ldcg(p.lse_parts + s * p.lse_part_stride + lrow)
-                              : p.lse_parts[s * p.lse_part_stride + lrow]);
+            mx = fmaxf(mx, CG ? __ldcg(p.lse_parts + par_off + s * p.lse_part_stride + lrow)
+                              : (p.lse_parts + par_off)[s * p.lse_part_stride + lrow]);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
         if (mx == -INFINITY) {
@@ -288,8 +290,8 @@ __device__ __forceinline__ void merge_row(const TreeMergeParams &p, int b, int t
             for (int e = 0; e < E; ++e) acc[e] = wt * ot[e];
             for (int s0 = 0; s0 < p.n_parts; s0 += 32) {
                 const int s = s0 + lane;
-                const float ls = s < p.n_parts ? (CG ? __ldcg(p.lse_parts + s * p.lse_part_stride + lrow)
-                                                     : p.lse_parts[s * p.lse_part_stride + lrow])
+                const float ls = s < p.n_parts ? (CG ? __ldcg(p.lse_parts + par_off + s * p.lse_part_stride + lrow)
+                                                     : (p.lse_parts + par_off)[s * p.lse_part_stride + lrow])
                                                : -INFINITY;
                 const float ws = expf(ls - mx);
                 const int cnt = min(32, p.n_parts - s0);
@@ -300,7 +302,7 @@ __device__ __forceinline__ void merge_row(const TreeMergeParams &p, int b, int t
                     for (int j = 0; j < 8; ++j) {
                         w8[j] = __shfl_sync(0xffffffffu, ws, (u + j) & 31);
                         if (u + j < cnt) {
-                            const float *src = p.o_parts + (s0 + u + j) * p.o_part_stride + orow;
+                            const float *src = p.o_parts + par_off + (s0 + u + j) * p.o_part_stride + orow;
                             if (CG)
                                 load_cg<E>(src, v8[j]);
                             else
@@ -327,6 +329,13 @@ __device__ __forceinline__ void merge_row(const TreeMergeParams &p, int b, int t
         }
     }
     const int blk = hl / p.out_hb, hh = hl % p.out_hb;
+    if (p.p2p_role == 1) {  // straight into rank blk's receive buffer (fp32 partials), then fenced
+        float *base = p.p2p_dst[blk] + static_cast<int64_t>(*p.p2p_epoch & 1u) * p.p2p_parity;
+        VecIO<float, E>::store(base + b * p.os0 + t * p.os1 + hh * p.os2 + lane * E,
+                               reinterpret_cast<const float(&)[E]>(out));
+        if (lane == 0) base[p.p2p_lse_off + (static_cast<int64_t>(b) * p.out_hb + hh) * p.T + t] = lse_out;
+        return;  // (the kernel's last block fences and signals: tree_merge_kernel)
+    }
     Tout *dst = static_cast<Tout *>(p.o) + blk * p.o_block_stride + b * p.os0 + t * p.os1 + hh * p.os2 + lane * E;
     VecIO<Tout, E>::store(dst, out);
     if (p.lse != nullptr && lane == 0)

@@ -69,6 +69,10 @@ _SIG = {
     "hta_comm_destroy": (ctypes.c_int, [_P]),
     "hta_comm_create_loopback": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]),
     "hta_comm_async_error": (ctypes.c_int, [_P]),
+    "hta_comm_p2p_alloc": (ctypes.c_int, [_P, ctypes.c_size_t, _P]),
+    "hta_comm_p2p_open": (ctypes.c_int, [_P, _P]),
+    "hta_comm_p2p_set": (ctypes.c_int, [_P, ctypes.c_int32]),
+    "hta_comm_p2p_error": (ctypes.c_int, [_P]),
     "hta_workspace_size_seqpar": (ctypes.c_size_t, [ctypes.POINTER(hta_shape_t), ctypes.c_int32, ctypes.c_int32]),
     "hta_forward_seqpar": (ctypes.c_int, [_P, ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, _P, _P, _P,
                                           ctypes.c_int64, _P, _P, ctypes.c_int32, _P, ctypes.c_size_t, _P]),
@@ -542,6 +546,40 @@ class HtaComm:
         _hold(stream, None if ws is ws_given else ws)
         return o, lse_out
 
+    def enable_p2p(self, shapes, group=None) -> bool:
+        """Enable the peer-memory exchange (hta_comm_p2p_*) for steps of the given hta_shape_t's
+        (local shapes): allocate this rank's buffers, all-gather the IPC handles over the process
+        group, open the peers'.  Returns False (the NCCL exchange stays) if any rank failed."""
+        import torch.distributed as dist
+        cap = max(seqpar_block_floats(s, self.world_size) for s in shapes)
+        buf = (ctypes.c_uint8 * 128)()
+        rc = lib().hta_comm_p2p_alloc(self.handle, cap, buf)
+        mine = torch.tensor(list(bytes(buf)) + [1 if rc == 0 else 0], dtype=torch.uint8)
+        if self.world_size > 1:
+            t = mine.cuda() if dist.get_backend(group) == "nccl" else mine
+            out = [torch.empty_like(t) for _ in range(self.world_size)]
+            dist.all_gather(out, t, group=group)
+            every = torch.stack([o.cpu() for o in out])
+        else:
+            every = mine[None]
+        if not bool(every[:, 128].all()):
+            return False
+        raw = (ctypes.c_uint8 * (128 * self.world_size))(*every[:, :128].flatten().tolist())
+        rc = lib().hta_comm_p2p_open(self.handle, raw)
+        ok = torch.tensor([1 if rc == 0 else 0], dtype=torch.uint8)
+        if self.world_size > 1:  # every rank must have opened its peers
+            t = ok.cuda() if dist.get_backend(group) == "nccl" else ok
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+            ok = t.cpu()
+        return bool(ok.item())
+
+    def set_p2p(self, enabled: bool) -> None:
+        _check("hta_comm_p2p_set", lib().hta_comm_p2p_set(self.handle, 1 if enabled else 0))
+
+    def p2p_error(self) -> bool:
+        """True once a final merge gave up waiting for a peer's flag (hta_comm_p2p_error)."""
+        return lib().hta_comm_p2p_error(self.handle) != 0
+
     def async_error(self) -> bool:
         """True if NCCL reported an asynchronous error on this communicator."""
         return lib().hta_comm_async_error(self.handle) != 0
@@ -569,6 +607,13 @@ class LoopbackComm:
             raise HtaError("hta_workspace_size_seqpar", 1)
         return self.world_size * ((n + 15) // 16 * 16)
 
+    def enable_p2p(self, shapes) -> None:
+        """The peer-memory exchange between the virtual ranks (hta_comm_p2p_alloc on a loopback
+        communicator): every rank's combine writes into the others' receive buffers."""
+        cap = max(seqpar_block_floats(s, self.world_size) for s in shapes)
+        buf = (ctypes.c_uint8 * 128)()
+        _check("hta_comm_p2p_alloc", lib().hta_comm_p2p_alloc(self.handle, cap, buf))
+
     def forward(self, q, k_slices, v_slices, k_tree, v_tree, mask, seqlens_slices=None, gather_output=False,
                 want_lse=True, scale=None, num_splits=0, stream=None):
         """k_slices / v_slices: per-rank KV slices [B, N_r, H_kv, d] (same N_r capacity);
@@ -590,6 +635,13 @@ class LoopbackComm:
             ws.numel(), _stream(stream)))
         _hold(stream, ws)
         return os_, ls
+
+
+def seqpar_block_floats(shape: hta_shape_t, world_size: int) -> int:
+    """Floats of one rank's exchange block: O [B,T,H/P,d] + LSE [B,H/P,T], rounded to 4."""
+    hp = shape.H // world_size
+    n = shape.B * shape.T * hp * shape.d + shape.B * hp * shape.T
+    return (n + 3) // 4 * 4
 
 
 def shard_bounds(N: int, world_size: int, rank: int) -> Tuple[int, int]:

@@ -88,3 +88,46 @@ def test_seqpar_tree_from_parents(cuda_device, comm, gather):
     assert torch.equal(o_m, o_p) and torch.equal(l_m, l_p)
     o_ref, l_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, oracle_masks(w), seqlens=w.seqlens)
     compare(o_p, l_p, o_ref, l_ref, "bf16", "seqpar_tree P=1")
+
+
+def test_seqpar_peer_memory_exchange_graph_replays(cuda_device, comm):
+    """The peer-memory exchange on a real (one-rank) communicator, with the IPC export/open of
+    hta_comm_p2p_alloc/open, inside a CUDA graph: the device-side step counter advances on every
+    replay (alternating receive-buffer halves, flags compared with it), and every replay on new
+    inputs equals the NCCL-exchange step of the reference communicator bit for bit."""
+    p2p = hta.HtaComm(0, 1)
+    try:
+        w0 = make_workload(1, 64, 32, 8, 128, 3000, "bf16", dist="V1", seed=60, tree="beam")
+        x = {k: getattr(w0, k).to(cuda_device) for k in ("q", "k_cache", "v_cache", "k_tree", "v_tree")}
+        par = w0.parents[0].to(torch.int32).to(cuda_device)
+        shape = hta.make_shape(x["q"], k_cache=x["k_cache"], k_tree=x["k_tree"])
+        assert p2p.enable_p2p([shape])
+        o = torch.empty_like(x["q"])
+        lse = torch.empty(1, 32, 64, dtype=torch.float32, device=cuda_device)
+        ws = torch.empty(p2p.workspace_size(shape), dtype=torch.uint8, device=cuda_device)
+
+        def fwd():
+            p2p.forward(x["q"], x["k_cache"], x["v_cache"], x["k_tree"], x["v_tree"], o=o, lse_out=lse, ws=ws,
+                        parents=par)
+
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fwd()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fwd()
+        for step in range(4):
+            w = make_workload(1, 64, 32, 8, 128, 3000, "bf16", dist="V1", seed=61 + step, tree="beam")
+            for k in x:
+                x[k].copy_(getattr(w, {"q": "q", "k_cache": "k_cache", "v_cache": "v_cache", "k_tree": "k_tree",
+                                       "v_tree": "v_tree"}[k]))
+            par.copy_(w.parents[0].to(torch.int32))
+            g.replay()
+            o_ref, l_ref = comm.forward(x["q"], x["k_cache"], x["v_cache"], x["k_tree"], x["v_tree"], parents=par)
+            torch.cuda.synchronize()
+            assert torch.equal(o, o_ref) and torch.equal(lse, l_ref), f"replay {step}"
+    finally:
+        p2p.close()

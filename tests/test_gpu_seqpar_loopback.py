@@ -112,3 +112,48 @@ def test_loopback_p1_equals_forward(cuda_device):
         assert (ls[0] - l1).abs().max().item() <= 1e-4
     finally:
         comm.close()
+
+
+P2P_CASES = [
+    # B, T, H, Hkv, d, N, dtype, tree, P
+    (1, 64, 32, 8, 128, 3000, "bf16", "beam", 2),
+    (1, 64, 32, 8, 128, 3000, "bf16", "beam", 8),
+    (2, 13, 8, 2, 128, 1000, "bf16", "random", 4),
+    (1, 128, 32, 8, 128, 4100, "bf16", "beam", 8),
+    (1, 8, 4, 1, 64, 256, "fp32", "heap_binary", 2),
+]
+
+
+@pytest.mark.parametrize("case", P2P_CASES, ids=lambda c: f"B{c[0]}T{c[1]}H{c[2]}/{c[3]}d{c[4]}N{c[5]}{c[6]}P{c[8]}")
+def test_loopback_peer_memory_exchange(cuda_device, case):
+    """The peer-memory exchange (hta_comm_p2p_*): each virtual rank's split combine writes its
+    head blocks straight into the other ranks' receive buffers, a signal kernel raises its flag
+    in every rank's flag array, each final merge waits for all P flags.  Three consecutive steps
+    on different inputs exercise both halves of the double-buffered receive buffers and the step
+    counters; every step's every rank equals the copy-exchange loopback step bit for bit and the
+    oracle within tolerance."""
+    B, T, H, Hkv, d, N, dtype, tree, P = case
+    p2p = hta.LoopbackComm(P)
+    ref = hta.LoopbackComm(P)
+    try:
+        for step in range(3):
+            w = make_workload(B, T, H, Hkv, d, N, dtype, dist="V1", seed=40 + step, tree=tree)
+            mask = torch.from_numpy(oracle_masks(w)).to(cuda_device)
+            ks, vs, sls = _shards(w, P, w.seqlens, cuda_device)
+            shape = hta.make_shape(w.q.to(cuda_device), k_cache=ks[0], k_tree=w.k_tree.to(cuda_device))
+            if step == 0:
+                p2p.enable_p2p([shape])
+            args = (w.q.to(cuda_device), ks, vs, w.k_tree.to(cuda_device), w.v_tree.to(cuda_device), mask)
+            os_p, ls_p = p2p.forward(*args, seqlens_slices=sls)
+            os_c, ls_c = ref.forward(*args, seqlens_slices=sls)
+            torch.cuda.synchronize()
+            o_ref, l_ref = oracle.attention(w.q, w.k_cache, w.v_cache, w.k_tree, w.v_tree, oracle_masks(w),
+                                            seqlens=w.seqlens)
+            Hp = H // P
+            for r in range(P):
+                assert torch.equal(os_p[r], os_c[r]) and torch.equal(ls_p[r], ls_c[r]), f"step {step} rank {r}"
+                hs = slice(r * Hp, (r + 1) * Hp)
+                compare(os_p[r], ls_p[r], o_ref[:, :, hs], l_ref[:, hs], dtype, f"p2p P={P} step {step} rank {r}")
+    finally:
+        p2p.close()
+        ref.close()
