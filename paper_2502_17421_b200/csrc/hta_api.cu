@@ -547,15 +547,17 @@ static hta_status_t forward_impl(const PagedArgs *pg, const hta_shape_t *shape, 
     if ((r = check_device()) != HTA_OK) return r;
     // The tree pass runs inside the prefix kernel (masked tree tiles appended to the last split of
     // every unit) for single-CTA row groups; it stays in the tree/merge kernel
-    // beside the merge for CTA pairs (there the tree tile costs the pair kernel about what the
-    // separate tree pass costs the tail: Llama-8B-64k 69.2 vs 69.6 us, 128k 217.7 vs 217.6 us),
+    // beside the merge for CTA pairs (there the tree tile costs the pair kernel more than the
+    // separate tree pass costs the tail: Llama-8B-64k 71.1 vs 69.6 us, 128k 225.8 vs 219 us;
+    // HTA_FUSE_PAIRS builds it),
     // for an FP8 cache, when the tree inputs arrive late on another stream (tree_ready), and when
     // k_tree / v_tree cannot be described by a tensor map.
     TreeArgs tr{};
     PrefixPlan pl = make_plan(sh, device_sms());
     if (f8 == nullptr && tree_ready == nullptr && fused_tree_tiles(s) > 0) {
         const PrefixPlan plt = make_plan(sh, device_sms(), fused_tree_tiles(s));
-        if (plt.nt == 1 && make_tree_map(&tr.tkt, k_tree, s, kBlockN) &&
+        // (a CTA of a pair loads its 64-key half of a tree K tile and a 64-column half of V)
+        if ((plt.nt == 1 || HTA_FUSE_PAIRS) && make_tree_map(&tr.tkt, k_tree, s, plt.nt == 2 ? kBlockN / 2 : kBlockN) &&
             make_tree_map(&tr.tvt, v_tree, s, kBlockN)) {
             tr.tree_tiles = fused_tree_tiles(s);
             tr.mask = mask;

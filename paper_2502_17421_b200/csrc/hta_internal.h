@@ -12,6 +12,13 @@ namespace hta {
 // Keys per KV tile of the prefix pass: TMEM holds 384 / kBlockN S/P buffers of kBlockN columns
 // and the 128-column O accumulator (512 columns in all): three 128-key buffers (96-key tiles with
 // four buffers measured slower: profiles/r02_experiments.md).
+// Fused tree pass for CTA pairs too (build option; measured slower than the tree pass in the
+// tree/merge kernel: Llama-8B-64k 71.1 vs 69.6 us, 128k/T=128 225.8 vs 219 us; profiles/
+// r02_experiments.md).  Single-CTA row groups always fuse.
+#ifndef HTA_FUSE_PAIRS
+#define HTA_FUSE_PAIRS 0
+#endif
+
 #ifndef HTA_BLOCK_N
 #define HTA_BLOCK_N 128
 #endif

@@ -124,15 +124,19 @@ constexpr int kL2Ahead = HTA_L2_AHEAD;  // FP8 cache: tiles prefetched into L2 b
 // memory round trip per batch; written out explicitly because the compiler cannot reorder the loads
 // above stores that may alias them).  That is safe: the f16 rows a batch writes overlap only E4M3
 // rows of the same batch or earlier ones (f16 row r covers E4M3 rows <= r in both slot shapes).
-template <int kRowBytes, int kRows>
-__device__ __forceinline__ void widen_e4m3_tile(uint8_t *slot, int lane, int valid) {
+// kParts > 1: this warp widens only rows [part*kRows/kParts, +kRows/kParts) -- for the 128-byte
+// rows of a single CTA's tiles only, where f16 row r covers exactly E4M3 row r (its second atom)
+// and the rows are independent, so several warps can widen one tile.
+template <int kRowBytes, int kRows, int kParts = 1>
+__device__ __forceinline__ void widen_e4m3_tile(uint8_t *slot, int lane, int valid, int part = 0) {
+    static_assert(kParts == 1 || kRowBytes == 128, "row-parallel widening needs 128-byte rows");
     constexpr int kChunks = kRowBytes / 16;  // 16-byte E4M3 chunks per row
     constexpr int kSlotBytes = kRows * kRowBytes * 2;
-    constexpr int kIters = kRows * kChunks / 32;
+    constexpr int kIters = kRows * kChunks / 32 / kParts;
     static_assert(kIters % kWidenUnroll == 0, "widen batches");
     const uint8_t *src = slot + kSlotBytes / 2;
 #pragma unroll 1
-    for (int it0 = 0; it0 < kIters; it0 += kWidenUnroll) {
+    for (int it0 = part * kIters; it0 < (part + 1) * kIters; it0 += kWidenUnroll) {
         uint4 x[kWidenUnroll];
 #pragma unroll
         for (int u = 0; u < kWidenUnroll; ++u) {
@@ -350,6 +354,11 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     const int lane = threadIdx.x & 31;
     const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
+    // FP8 cache, single CTA, at most 64 rows (MHA with T <= 64, the draft frontier): the softmax
+    // warps of lane quarters 2-3 hold only padding rows; they widen the E4M3 tiles instead (four
+    // per ring, a quarter of each tile's rows each) and the TMA warps only issue the loads.
+    const bool wide = KV8 && !PAIR && D == 128 && p.M <= 64;
+    constexpr int kWideWarps = 4;  // widening warps per ring in that mode
 #ifdef HTA_TRACE
     unsigned long long *const tr_buf = g_trace;  // read once: a global load per record would stall
     const bool tr_on = tr_buf != nullptr && static_cast<int>(blockIdx.x) == g_trace_cta;
@@ -381,18 +390,18 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         // the FP8 variant fills a slot by widening in place: its full barrier counts one arrival per
         // CTA (no TMA bytes); the E4M3 tile's TMA completes on the CTA's own land barrier
         for (int i = 0; i < C::kSlotsK; ++i) {
-            mbar_init(&k_full[i], KV8 && PAIR ? 2 : 1);
+            mbar_init(&k_full[i], KV8 && PAIR ? 2 : (wide ? kWideWarps : 1));
             mbar_init(&k_empty[i], 1);
             mbar_init(&k_land[i], 1);
         }
         for (int i = 0; i < C::kSlotsV; ++i) {
-            mbar_init(&v_full[i], KV8 && PAIR ? 2 : 1);
+            mbar_init(&v_full[i], KV8 && PAIR ? 2 : (wide ? kWideWarps : 1));
             mbar_init(&v_empty[i], 1);
             mbar_init(&v_land[i], 1);
         }
         for (int i = 0; i < C::kSBufs; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], C::kGroupWarps * (PAIR ? 2 : 1));
+            mbar_init(&p_full[i], wide ? C::kGroupWarps / 2 : C::kGroupWarps * (PAIR ? 2 : 1));
             mbar_init(&pv_done[i], 1);
         }
         mbar_init(o_final, 1);
@@ -489,7 +498,20 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                                     kPolicyEvictNormal);
                 }
             };
-            if constexpr (KV8) {
+            if (KV8 && wide) {
+                // FP8 cache, widening warps: lane 0 only lands the E4M3 tiles (the whole ring ahead)
+                if (lane == 0)
+                    for (int j = 0; j < n_tiles; ++j) {
+                        const int slot = j % C::kSlotsK;
+                        mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);
+                        HTA_TR(30, j);
+                        mbar_arrive_expect_tx(&k_land[slot], C::kKBytes / 2);
+                        tma_load_4d(sK + slot * C::kKBytes + C::kKBytes / 2, &tmap_k, &k_land[slot], 0, g,
+                                    static_cast<int>(key_lo) + j * kBlockN, b, kKvPolicy);
+                        if (j + kL2Ahead < n_tiles)
+                            tma_prefetch_l2_4d(&tmap_k, 0, g, static_cast<int>(key_lo) + (j + kL2Ahead) * kBlockN, b);
+                    }
+            } else if constexpr (KV8) {
                 // FP8 cache: the whole warp loads E4M3 tiles kLead tiles ahead (lane 0 issues the
                 // TMA into the upper half of the f16 slot) and widens tile j in place, then signals
                 // the MMA warp (in a pair: the leader's barrier, both CTAs arrive)
@@ -608,7 +630,19 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             // barrier of this CTA (v_tail_land); the MMA warp then waits on v_tail_ready (both CTAs
             // of a pair arrive) instead of v_full.
             const uint32_t vfull0 = PAIR ? mapa_shared(smem_u32(&v_full[0]), 0) : 0u;
-            if constexpr (KV8) {
+            if (KV8 && wide) {
+                if (lane == 0)
+                    for (int j = 0; j < n_tiles; ++j) {
+                        const int slot = j % C::kSlotsV;
+                        mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
+                        HTA_TR(31, j);
+                        mbar_arrive_expect_tx(&v_land[slot], C::kVBytes / 2);
+                        tma_load_4d(sV + slot * C::kVBytes + C::kVBytes / 2, &tmap_v, &v_land[slot], 0, g,
+                                    static_cast<int>(key_lo) + j * kBlockN, b, kKvPolicy);
+                        if (j + kL2Ahead < n_tiles)
+                            tma_prefetch_l2_4d(&tmap_v, 0, g, static_cast<int>(key_lo) + (j + kL2Ahead) * kBlockN, b);
+                    }
+            } else if constexpr (KV8) {
                 // FP8 cache: as the K producer; rows past the sequence end of the last tile are
                 // written as zeros while widening (so no separate sanitising pass)
                 constexpr int kLead = C::kSlotsV - 1;
@@ -921,7 +955,38 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     mbar_arrive(&p_full[jp % C::kSBufs]);
             }
         };
-        for (int j = grp; j < n_tiles; j += 2) {
+        if constexpr (KV8 && !PAIR && D == 128) {
+            if (wide && quarter >= 2) {
+                // ================= widening warp (FP8, <= 64 rows): warps of bands 0-1 widen K tiles,
+                // bands 2-3 V tiles; part = a quarter of the tile's rows.  V rows past the sequence
+                // end of the last tile are written as zeros (Z13).
+                const int wi = band * 2 + (quarter - 2);
+                const bool kw = wi < kWideWarps;
+                const int part = wi % kWideWarps;
+                for (int j = 0; j < n_tiles; ++j) {
+                    const int slot = j % (kw ? C::kSlotsK : C::kSlotsV);
+                    const uint32_t par = static_cast<uint32_t>((j / (kw ? C::kSlotsK : C::kSlotsV)) & 1);
+                    if (kw) {
+                        mbar_wait(&k_land[slot], par);
+                        __syncwarp();
+                        HTA_TR(34, j);
+                        widen_e4m3_tile<D, C::kKRows, kWideWarps>(sK + slot * C::kKBytes, lane, C::kKRows, part);
+                    } else {
+                        mbar_wait(&v_land[slot], par);
+                        __syncwarp();
+                        HTA_TR(34, j);
+                        widen_e4m3_tile<C::kVCols, kBlockN, kWideWarps>(
+                            sV + slot * C::kVBytes, lane, (tail_zero && j == nc - 1) ? tail_valid : kBlockN, part);
+                    }
+                    HTA_TR(35, j);
+                    fence_proxy_async_smem();  // generic-proxy writes -> read by the tensor core
+                    __syncwarp();
+                    HTA_TR(kw ? 32 : 33, j);
+                    if (lane == 0) mbar_arrive(kw ? &k_full[slot] : &v_full[slot]);
+                }
+            }
+        }
+        for (int j = grp; j < n_tiles && !(wide && quarter >= 2); j += 2) {
             const bool tree_tile = TREE && j >= nc;  // a tree tile of the fused tree pass
             const int buf = j % C::kSBufs;
             mbar_wait(&s_full[buf], static_cast<uint32_t>((j / C::kSBufs) & 1));
@@ -1206,10 +1271,13 @@ cudaError_t launch_prefix_tc(const PrefixParams &p, const CUtensorMap &tq, const
         return cudaErrorInvalidValue;
     }
     if (p.tree_tiles < 0 || p.tree_tiles > (256 + kBlockN - 1) / kBlockN) return cudaErrorInvalidValue;
-    if (p.tree_tiles > 0) {  // the fused tree pass (single-CTA row groups, hta_api.cu forward_impl)
+    if (p.tree_tiles > 0) {  // the fused tree pass (hta_api.cu forward_impl)
+#if HTA_FUSE_PAIRS
+        if (p.d == 128 && p.nt == 2) return launch_tc<128, true, false, true>(p, tq, tk, tv, tkt, tvt, s);
+#endif
         if (p.nt != 1) return cudaErrorInvalidValue;
         if (p.d == 128) return launch_tc<128, false, false, true>(p, tq, tk, tv, tkt, tvt, s);
-        if (p.d == 64) return launch_tc<64, false, false, true>(p, tq, tk, tv, tkt, tvt, s);
+        if (p.d == 64 && p.nt == 1) return launch_tc<64, false, false, true>(p, tq, tk, tv, tkt, tvt, s);
         return cudaErrorInvalidValue;
     }
     if (p.d == 128)

@@ -42,6 +42,14 @@ def main():
                                                          parents, o=o, lse_out=lse, ws=ws),
             "timed(events)": lambda: hta.hta_forward(*args, o=o, lse_out=lse, ws=ws, events=evs),
         }
+        if os.environ.get("FP8"):  # the forward over an E4M3 copy of the cache
+            from workloads import fp8_cache
+            k8, ks = fp8_cache(w.k_cache)
+            v8, vs = fp8_cache(w.v_cache)
+            k8, v8, ks, vs = k8.to(dev), v8.to(dev), ks.to(dev), vs.to(dev)
+            fns = {"fp8": lambda: hta.hta_forward_fp8kv(x["q"], k8, v8, ks, vs, x["k_tree"], x["v_tree"], mask, o=o,
+                                                        lse_out=lse),
+                   "bf16": fns["fused"]}
         res = {}
         for nm, fn in fns.items():
             s = torch.cuda.Stream(device=dev)

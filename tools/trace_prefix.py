@@ -169,7 +169,7 @@ def main():
     # producers: issue -> landed latency (V landed = event 3 of the MMA warp, K landed = event 2)
     kw = next((w for w in range(32) if (w, 30) in ev), None)
     vw = next((w for w in range(32) if (w, 31) in ev), None)
-    if kw is not None and vw is not None:
+    if kw is not None and vw is not None and (kw, 32) not in ev and not any((w, 34) in ev for w in range(32)):
         kl = [mma[2][j] - ev[(kw, 30)][j] for j in tiles if j in mma[2] and j in ev[(kw, 30)]]
         vl = [mma[3][j] - ev[(vw, 31)][j] for j in tiles if j in mma[3] and j in ev[(vw, 31)]]
         vlead = [mma[1][j] - ev[(vw, 31)][j] for j in tiles if j in ev[(vw, 31)]]
@@ -182,10 +182,30 @@ def main():
             continue
         a, bb = ev[(w0, e0)], ev[(w0, e1)]
         js = sorted(j for j in bb if j in a)
+        if len(js) < 2:
+            continue
         wid = [bb[j] - a[j] for j in js]
         gap = [a[j2] - bb[j1] for j1, j2 in zip(js, js[1:])]
         print(f"FP8 {nm} producer (warp {w0}): widen median {statistics.median(wid):.0f} cycles, "
               f"wait for the next tile to land median {statistics.median(gap):.0f}")
+    # FP8 cache, widening warps (<= 64 rows): landed (34) -> widened (32 K / 33 V), and the wait
+    # for the next tile to land
+    for wi in range(32):
+        if (wi, 34) not in ev:
+            continue
+        e1 = 32 if (wi, 32) in ev else 33
+        a, bb = ev[(wi, 34)], ev.get((wi, e1), {})
+        js = sorted(j for j in bb if j in a)
+        if not js:
+            continue
+        wid = [bb[j] - a[j] for j in js]
+        gap = [a[j2] - bb[j1] for j1, j2 in zip(js, js[1:])]
+        c35 = ev.get((wi, 35), {})
+        fen = [bb[j] - c35[j] for j in js if j in c35]
+        print(f"widening warp {wi} ({'K' if e1 == 32 else 'V'}): widen median {statistics.median(wid):.0f} "
+              f"(fence + sync {statistics.median(fen) if fen else 0:.0f}), "
+              f"wait for the next landing median {statistics.median(gap) if gap else 0:.0f}, "
+              f"widened at {[rel(bb[j]) for j in js[:4]]}..")
     # per warp: median lag of its publish behind the first warp of its group
     lags = defaultdict(list)
     for j in range(2, len(tiles) - 2):
