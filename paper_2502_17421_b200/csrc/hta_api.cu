@@ -267,7 +267,8 @@ hta_status_t make_pool_map(CUtensorMap *map, const void *base, const hta_shape_t
 
 // FP8 (E4M3) cache [B, N, H_kv, d] as bytes: box = box_cols x 1 x box_rows x 1, no swizzle (the
 // kernel widens the landed tile into the 128B-swizzled f16 layout itself).
-hta_status_t make_kv_map_fp8(CUtensorMap *map, const void *base, const hta_shape_t &s, int box_cols, int box_rows) {
+hta_status_t make_kv_map_fp8(CUtensorMap *map, const void *base, const hta_shape_t &s, int box_cols, int box_rows,
+                             bool swizzle = false) {
     EncodeTiledFn enc = encode_fn();
     if (enc == nullptr) return HTA_ERR_CUDA;
     cuuint64_t dims[4] = {cuuint64_t(s.d), cuuint64_t(s.H_kv), cuuint64_t(std::max<int64_t>(s.N_max, 1)),
@@ -276,8 +277,8 @@ hta_status_t make_kv_map_fp8(CUtensorMap *map, const void *base, const hta_shape
     cuuint32_t box[4] = {cuuint32_t(box_cols), 1, cuuint32_t(box_rows), 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? HTA_OK : HTA_ERR_INVALID_ARGUMENT;
 }
 
@@ -297,6 +298,12 @@ struct TreeArgs {
 };
 
 // Enqueue the prefix pass writing `splits` partials at (o_out, lse_out) with the given strides.
+// FP8 cache: the transposed kernel (build option HTA_T8) takes single-CTA units of at most 64
+// rows at d = 128
+bool t8_eligible(const hta_shape_t &s, const PrefixPlan &pl) {
+    return HTA_T8 && s.d == 128 && pl.nt == 1 && pl.n_mgroups == 1 && pl.M <= 64 && kBlockN == 128;
+}
+
 hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, const void *k, const void *v,
                         const int32_t *seqlens, float *o_out, float *lse_out, int64_t o_split_stride,
                         int64_t lse_split_stride, cudaStream_t st, const PagedArgs *pg = nullptr,
@@ -346,6 +353,14 @@ hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, co
     if (s.dtype == HTA_BF16) {
         CUtensorMap tk, tv;
         hta_status_t r;
+        if (f8 != nullptr && t8_eligible(s, pl)) {
+            // units of at most 64 rows: the transposed kernel (K tiles 128-byte swizzled)
+            if ((r = make_kv_map_fp8(&tk, k, s, 128, kBlockN, true)) != HTA_OK) return r;
+            if ((r = make_kv_map_fp8(&tv, v, s, 128, kBlockN, false)) != HTA_OK) return r;  // (widened in place)
+#if HTA_T8
+            return launch_prefix_t8(p, tk, tv, st) == cudaSuccess ? HTA_OK : HTA_ERR_CUDA;
+#endif
+        }
         if (f8 != nullptr) {
             // a CTA of a pair loads half of each K tile (64 keys, all d) and half of each V tile
             // (64 columns, all 128 keys) -- the same halves as the bf16 cache

@@ -127,6 +127,14 @@ cudaError_t launch_prefix_tc(const PrefixParams &p, const CUtensorMap &tmap_q, c
                              const CUtensorMap &tmap_v, const CUtensorMap &tmap_kt, const CUtensorMap &tmap_vt,
                              int smem_bytes, cudaStream_t s);
 int prefix_tc_smem_bytes(int d, int nt);
+// FP8 cache, units of at most 64 rows, d = 128: the transposed kernel (prefix_t8.cu); tk / tv are
+// E4M3 maps with 128 x 128-byte boxes, tk with 128-byte swizzle, tv without.  A build option
+// (-DHTA_T8=1): correct, but not faster than prefix_tc.cu's widening warps on LongChat-16k
+// (63.5 vs 61.5 us; profiles/r02_experiments.md), so the default library does not contain it.
+#ifndef HTA_T8
+#define HTA_T8 0
+#endif
+cudaError_t launch_prefix_t8(const PrefixParams &p, const CUtensorMap &tk, const CUtensorMap &tv, cudaStream_t s);
 cudaError_t launch_prefix_simt(const PrefixParams &p, cudaStream_t s);
 cudaError_t launch_tree_merge(const TreeMergeParams &p, int d, hta_dtype_t in_dtype, hta_dtype_t out_dtype,
                               bool pdl, cudaStream_t s);

@@ -283,5 +283,12 @@ int main() {
     run<true, true, 128, true, 8>("WARP pair TS M256, 8 TMEM warps", 8, 1);
     run<true, true, 128, true, 4>("WARP pair TS M256, 4 TMEM warps", 8, 1);
     run<false, true, 128, true, 8>("WARP single TS M128, 8 TMEM warps", 8, 1);
+    // the transposed FP8 kernel's shapes (prefix_t8.cu): N = 64 query rows
+    run<false, false, 64, true, 0>("WARP single SS M128 N64", 8, 0);
+    run<false, false, 64, true, 0>("WARP single SS M128 N64 B MN-major", 8, 1);
+    run<false, true, 64, true, 0>("WARP single TS M128 N64", 8, 0);
+    run<false, false, 128, true, 0>("WARP single SS M128 N128", 8, 0);
+    run<false, true, 128, true, 0>("WARP single TS M128 N128", 8, 0);
+    run<false, false, 256, true, 0>("WARP single SS M128 N256", 8, 0);
     return 0;
 }

@@ -28,6 +28,64 @@ from workloads.generators import config_workload  # noqa: E402
 RECS = 1024
 
 
+def analyze_t8(ev, rel, name, cta):
+    """prefix_t8.cu events: TMA 40/41 (K/V slot free, issue); K widening 42 landed, 43 TMEM buffer
+    free, 44 done; V 45/46/47; MMA 48 S_j issue, 49 PV_j issue; softmax 50 S ready, 51 pass 1
+    done, 52 vote done, 53 published."""
+    med = lambda xs: statistics.median(xs) if xs else 0  # noqa: E731
+    exit_t = max(rel(v[0]) for (wi, e), v in ev.items() if e == 0)
+    print(f"{name} CTA {cta} (transposed FP8 kernel): last warp entry at {exit_t}")
+    mma = next((w for w in range(32) if (w, 49) in ev), None)
+    if mma is None:
+        print("no MMA records")
+        return
+    pv, sis = ev[(mma, 49)], ev[(mma, 48)]
+    js = sorted(pv)
+    per = [pv[b] - pv[a] for a, b in zip(js, js[1:])]
+    print(f"MMA warp {mma}: {len(js)} PV; first PV at {rel(pv[js[0]])}, last at {rel(pv[js[-1]])}; "
+          f"period median {med(per):.0f} (p10 {sorted(per)[len(per) // 10] if per else 0}, "
+          f"p90 {sorted(per)[9 * len(per) // 10] if per else 0})")
+    tw = next((w for w in range(32) if (w, 40) in ev), None)
+    if tw is not None:
+        kw_ = next((w for w in range(32) if (w, 42) in ev), None)
+        vw_ = next((w for w in range(32) if (w, 45) in ev), None)
+        for nm, ei, wl, el in (("K", 40, kw_, 42), ("V", 41, vw_, 45)):
+            if wl is None or (tw, ei) not in ev:
+                continue
+            a, b_ = ev[(tw, ei)], ev[(wl, el)]
+            jj = sorted(j for j in a if j in b_)
+            print(f"{nm} TMA issue -> landed (seen by its widening warp) median {med([b_[j] - a[j] for j in jj]):.0f}; "
+                  f"issue lead over PV_j {med([pv[j] - a[j] for j in jj if j in pv]):.0f}")
+    s_iss = [ev[(mma, 55)][j] - sis[j] for j in sorted(ev.get((mma, 55), {})) if j in sis]
+    pv_iss = [ev[(mma, 56)][j] - pv[j] for j in sorted(ev.get((mma, 56), {})) if j in pv]
+    print(f"MMA issue durations: S batch {med(s_iss):.0f}, PV batch {med(pv_iss):.0f} cycles (median)")
+    for nm, evs in (("K", (42, 43, 44)), ("V", (45, 45, 47))):
+        for w in (w for w in range(32) if (w, evs[2]) in ev):
+            a, b_, c_ = (ev.get((w, e), {}) for e in evs)
+            jj = sorted(j for j in c_ if j in a and j in b_)
+            print(f"{nm} warp {w}: landed->buffer free {med([b_[j] - a[j] for j in jj]):.0f}, "
+                  f"widen {med([c_[j] - b_[j] for j in jj]):.0f}, done->next landed "
+                  f"{med([a[j2] - c_[j1] for j1, j2 in zip(jj, jj[1:])]):.0f}")
+    sm = [w for w in range(32) if (w, 53) in ev]
+    for w in sm:
+        e0, e1, e2, e3 = (ev.get((w, e), {}) for e in (50, 51, 52, 53))
+        jj = sorted(j for j in e3 if j in e0 and j in e1 and j in e2)
+        idle = [e0[j2] - e3[j1] for j1, j2 in zip(jj, jj[1:])]
+        print(f"softmax warp {w}: pass1 {med([e1[j] - e0[j] for j in jj]):.0f}, vote {med([e2[j] - e1[j] for j in jj]):.0f}, "
+              f"->published {med([e3[j] - e2[j] for j in jj]):.0f}, idle waiting for S {med(idle):.0f}")
+    print("tile: S_j issued | S_j ready (w0) | published (all softmax warps) | PV_j issued | K_j done | V_j done  (cycles)")
+    for j in js[max(0, len(js) // 2 - 5):len(js) // 2 + 5]:
+        pubs = [ev.get((w, 53), {}).get(j) for w in sm]
+        pubs = [rel(x) for x in pubs if x is not None]
+        kd = [ev.get((w, 44), {}).get(j) for w in range(32)]
+        vd = [ev.get((w, 47), {}).get(j) for w in range(32)]
+        kd = max(rel(x) for x in kd if x is not None) if any(x is not None for x in kd) else "-"
+        vd = max(rel(x) for x in vd if x is not None) if any(x is not None for x in vd) else "-"
+        sr = ev.get((0, 50), {}).get(j)
+        print(f"{j:4d}: {rel(sis[j]) if j in sis else '-'} | {rel(sr) if sr else '-'} | "
+              f"{min(pubs) if pubs else '-'}..{max(pubs) if pubs else '-'} | {rel(pv[j])} | {kd} | {vd}")
+
+
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "llama8b_64k"
     cta = int(sys.argv[2]) if len(sys.argv) > 2 else 0
@@ -50,6 +108,9 @@ def main():
         bt = torch.arange(w.B * maxp, dtype=torch.int32, device=dev).view(w.B, maxp)
         fwd = lambda: hta.hta_forward_paged(x[0], kp, vp, bt, x[3], x[4], mask)  # noqa: E731
     L = hta.lib()
+    t8 = bool(os.environ.get("T8"))  # the transposed FP8 kernel (prefix_t8.cu) instead
+    if t8:
+        L.hta_debug_set_trace = L.hta_debug_set_trace_t8
     L.hta_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
     buf = torch.zeros(32 * RECS, dtype=torch.int64, device=dev)
     fwd()
@@ -86,6 +147,8 @@ def main():
         print("no trace records")
         return
     rel = lambda c: c - t0  # noqa: E731
+    if t8:
+        return analyze_t8(ev, rel, name, cta)
     exit_t = max(rel(v[0]) for (wi, e), v in ev.items() if e == 63)
     print(f"{name} CTA {cta}: exit at {exit_t} cycles after the first entry")
     # roles from the records: the MMA warp logs events 1-3, softmax warps event 10 (group = tile parity)
