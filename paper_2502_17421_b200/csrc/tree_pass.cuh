@@ -76,51 +76,54 @@ struct VecIO<__nv_bfloat16, 2> {
     }
 };
 
-// Tree pass of one output row: normalised tree partial in ot[] and its natural-log LSE.
-template <typename Tin, int D>
-__device__ __forceinline__ float tree_row(const TreeMergeParams &p, int b, int t, int h, int lane,
-                                          float (&ot)[D / 32]) {
+// Tree pass of one output row: normalised tree partial in ot[] and its natural-log LSE.  W = 64-bit
+// words of the row's visibility (1 for T <= 64, 4 for T <= 256): the set is built and walked with
+// 64-bit ballots / find-first-set, so a small tree costs no per-word selects.
+template <typename Tin, int D, int W>
+__device__ __forceinline__ float tree_row_w(const TreeMergeParams &p, int b, int t, int h, int lane,
+                                            float (&ot)[D / 32]) {
     constexpr int E = D / 32;
     constexpr int kKeys = 8;  // visible keys whose K and V rows are in flight at once
     const int g = h / p.G;
 #pragma unroll
     for (int e = 0; e < E; ++e) ot[e] = 0.f;
-    // one round trip for q and the whole mask row (T <= 256: up to 8 bytes per lane)
+    // one round trip for q and the whole mask row (T <= 64 W: up to 2 W bytes per lane)
     float qv[E];
     VecIO<Tin, E>::load(static_cast<const Tin *>(p.q) + b * p.qs0 + t * p.qs1 + h * p.qs2 + lane * E, qv);
-    uint32_t vis[8];
+    uint64_t vis[W];
     if (p.mask != nullptr) {
         const uint8_t *mrow = p.mask + b * p.mask_bs + static_cast<int64_t>(t) * p.T;
-        uint8_t mb[8];
+        uint8_t mb[2 * W];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) mb[c] = (c * 32 < p.T && c * 32 + lane < p.T) ? mrow[c * 32 + lane] : 0;
+        for (int c = 0; c < 2 * W; ++c) mb[c] = c * 32 + lane < p.T ? mrow[c * 32 + lane] : 0;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) vis[c] = __ballot_sync(0xffffffffu, mb[c] != 0);
+        for (int c = 0; c < W; ++c)
+            vis[c] = static_cast<uint64_t>(__ballot_sync(0xffffffffu, mb[2 * c] != 0)) |
+                     (static_cast<uint64_t>(__ballot_sync(0xffffffffu, mb[2 * c + 1] != 0)) << 32);
     } else {
         // hta_forward_tree: the row's visible keys are t and its ancestors (Z4), found by walking
         // the parent links held in registers (lane l: parents[32c + l]); a chain through an
         // invalid link (parents[a] < -1 or >= a) hides the whole row, as hta_build_tree_mask does
         const int32_t *prow = p.parents + b * p.par_bs;
-        int par[8];
+        int par[2 * W];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) par[c] = c * 32 + lane < p.T ? prow[c * 32 + lane] : -1;
+        for (int c = 0; c < 2 * W; ++c) par[c] = c * 32 + lane < p.T ? prow[c * 32 + lane] : -1;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) vis[c] = 0u;
-        int a = t;
+        for (int c = 0; c < W; ++c) vis[c] = 0ull;
+        int a = t;  // (warp-uniform)
         while (a >= 0) {
             int pa = -1;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                if (c * 32 >= p.T) break;
+            for (int c = 0; c < 2 * W; ++c) {
                 const int x = __shfl_sync(0xffffffffu, par[c], a & 31);
-                if (c == (a >> 5)) {
-                    pa = x;
-                    vis[c] |= 1u << (a & 31);
-                }
+                if (c == (a >> 5)) pa = x;
             }
+#pragma unroll
+            for (int c = 0; c < W; ++c)
+                if (c == (a >> 6)) vis[c] |= 1ull << (a & 63);
             if (pa < -1 || pa >= a) {
 #pragma unroll
-                for (int c = 0; c < 8; ++c) vis[c] = 0u;
+                for (int c = 0; c < W; ++c) vis[c] = 0ull;
                 break;
             }
             a = pa;
@@ -131,21 +134,21 @@ __device__ __forceinline__ float tree_row(const TreeMergeParams &p, int b, int t
     using Acc = typename std::conditional<std::is_same<Tin, float>::value, double, float>::type;
     float l = 0.f;
     Acc m_acc = static_cast<Acc>(-INFINITY);  // running max kept at accumulation precision
-    int c = 0;
     while (true) {
         // next (up to) kKeys visible keys in index order
         int idx[kKeys];
         int n = 0;
 #pragma unroll
         for (int u = 0; u < kKeys; ++u) {
-            while (c < 8 && vis[c] == 0u) ++c;
-            if (c < 8) {
-                idx[u] = c * 32 + __ffs(vis[c]) - 1;
-                vis[c] &= vis[c] - 1u;
-                ++n;
-            } else {
-                idx[u] = -1;
+            idx[u] = -1;
+#pragma unroll
+            for (int c = 0; c < W; ++c) {
+                if (idx[u] < 0 && vis[c] != 0ull) {
+                    idx[u] = c * 64 + __ffsll(static_cast<long long>(vis[c])) - 1;
+                    vis[c] &= vis[c] - 1ull;
+                }
             }
+            n += idx[u] >= 0 ? 1 : 0;
         }
         if (n == 0) break;
         Acc z[kKeys];
@@ -193,6 +196,11 @@ __device__ __forceinline__ float tree_row(const TreeMergeParams &p, int b, int t
 #pragma unroll
     for (int e = 0; e < E; ++e) ot[e] *= inv;
     return static_cast<float>(m_acc + static_cast<Acc>(logf(l)));
+}
+
+template <typename Tin, int D>
+__device__ __forceinline__ float tree_row(const TreeMergeParams &p, int b, int t, int h, int lane, float (&ot)[D / 32]) {
+    return p.T <= 64 ? tree_row_w<Tin, D, 1>(p, b, t, h, lane, ot) : tree_row_w<Tin, D, 4>(p, b, t, h, lane, ot);
 }
 
 // Loads of partials written during the same kernel by other CTAs: L2 only (ld.global.cg).
