@@ -110,9 +110,11 @@ __device__ __forceinline__ float fold_max(float m, float rho) { return rho > m +
 #endif
 constexpr int kWidenUnroll = HTA_WIDEN_UNROLL;  // (4 with the 48-register producers)
 #ifndef HTA_L2_AHEAD
-#define HTA_L2_AHEAD 4
+#define HTA_L2_AHEAD 0
 #endif
-constexpr int kL2Ahead = HTA_L2_AHEAD;  // FP8 cache: tiles prefetched into L2 beyond the smem ring
+// FP8 cache: tiles prefetched into L2 beyond the smem ring (0 = none: measured faster, LongChat-16k
+// 59.4 vs 61.5 us at 4; the same prefetch on the bf16 cache cost 53.4 -> 61.5 us)
+constexpr int kL2Ahead = HTA_L2_AHEAD;
 
 // FP8 KV cache: an E4M3 tile (kRows rows of kRowBytes bytes) landed by TMA in
 // the upper half of its f16 ring slot is widened IN PLACE into the slot's f16 K-major SWIZZLE_128B
@@ -508,7 +510,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                         mbar_arrive_expect_tx(&k_land[slot], C::kKBytes / 2);
                         tma_load_4d(sK + slot * C::kKBytes + C::kKBytes / 2, &tmap_k, &k_land[slot], 0, g,
                                     static_cast<int>(key_lo) + j * kBlockN, b, kKvPolicy);
-                        if (j + kL2Ahead < n_tiles)
+                        if (kL2Ahead > 0 && j + kL2Ahead < n_tiles)
                             tma_prefetch_l2_4d(&tmap_k, 0, g, static_cast<int>(key_lo) + (j + kL2Ahead) * kBlockN, b);
                     }
             } else if constexpr (KV8) {
@@ -527,7 +529,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                                     r0 + jj * kBlockN, b, kKvPolicy);
                         // the ring is shallow (each in-flight tile holds a whole f16 slot): stage the
                         // tiles further ahead in L2
-                        if (jj + kL2Ahead < n_tiles) tma_prefetch_l2_4d(&tmap_k, 0, g, r0 + (jj + kL2Ahead) * kBlockN, b);
+                        if (kL2Ahead > 0 && jj + kL2Ahead < n_tiles) tma_prefetch_l2_4d(&tmap_k, 0, g, r0 + (jj + kL2Ahead) * kBlockN, b);
                     }
                 };
                 for (int jj = 0; jj < kLead && jj < n_tiles; ++jj) issue(jj);
@@ -639,7 +641,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                         mbar_arrive_expect_tx(&v_land[slot], C::kVBytes / 2);
                         tma_load_4d(sV + slot * C::kVBytes + C::kVBytes / 2, &tmap_v, &v_land[slot], 0, g,
                                     static_cast<int>(key_lo) + j * kBlockN, b, kKvPolicy);
-                        if (j + kL2Ahead < n_tiles)
+                        if (kL2Ahead > 0 && j + kL2Ahead < n_tiles)
                             tma_prefetch_l2_4d(&tmap_v, 0, g, static_cast<int>(key_lo) + (j + kL2Ahead) * kBlockN, b);
                     }
             } else if constexpr (KV8) {
@@ -655,7 +657,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                         mbar_arrive_expect_tx(&v_land[slot], C::kVBytes / 2);
                         tma_load_4d(sV + slot * C::kVBytes + C::kVBytes / 2, &tmap_v, &v_land[slot], c0, g,
                                     static_cast<int>(key_lo) + jj * kBlockN, b, kKvPolicy);
-                        if (jj + kL2Ahead < n_tiles)
+                        if (kL2Ahead > 0 && jj + kL2Ahead < n_tiles)
                             tma_prefetch_l2_4d(&tmap_v, c0, g, static_cast<int>(key_lo) + (jj + kL2Ahead) * kBlockN, b);
                     }
                 };
