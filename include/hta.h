@@ -93,18 +93,8 @@ int32_t hta_version(void);
 /* Bytes of device workspace hta_prefix_attn / hta_forward need for `shape` on a device with
  * `num_sms` SMs (pass the device's multiProcessorCount; <= 0 means 148, one B200).  The
  * workspace holds the split-KV partials: num_splits x (B*T*H*d + B*H*T) floats (at least one
- * split), and for bf16 a block of unit counters at its END (2 x B x H_kv x ceil(T*G/128) + 1
- * words, rounded to 16 bytes) used by hta_forward / hta_forward_tree / hta_forward_paged for the
- * fused split combine: that block must be ZERO before the workspace is first
- * used (cudaMemset once; every call leaves it zero) and must not be written by anything else.
- * A workspace without room for it (the partials only) still works: the split combine then runs
- * as a second kernel.  Returns (size_t)-1 for an invalid shape.  Host-only; never touches the GPU. */
+ * split).  Returns (size_t)-1 for an invalid shape.  Host-only; never touches the GPU. */
 size_t hta_workspace_size(const hta_shape_t *shape, int32_t num_sms);
-
-/* Fused split combine on (enable != 0, the default) or off (the split combine and the tree pass of
- * CTA-pair units then run as a second kernel, tree_merge_kernel).  Process-wide; returns the
- * previous setting.  For A/B measurements and tests; results agree to rounding either way. */
-int32_t hta_set_fused_merge(int32_t enable);
 
 /* attend_cache: UNMASKED attention of every tree query over the KV cache -- the
  * paper's FlashAttention/FlashDecoding prefix call.

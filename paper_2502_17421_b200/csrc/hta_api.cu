@@ -17,8 +17,6 @@ namespace {
 constexpr int kDefaultSms = 148;
 
 bool is_aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
-// hta_set_fused_merge(0): the split combine runs as its own kernel (A/B and tests)
-std::atomic<int> g_no_fused_merge{0};
 
 // Normalised copy of a shape with default strides filled in.
 struct Shape {
@@ -166,18 +164,6 @@ size_t part_floats(const hta_shape_t &s) {
     return size_t(s.B) * s.T * s.H * s.d + size_t(s.B) * s.H * s.T;
 }
 
-// Fused split combine: two arrival counters per unit (b, kv head, 128-row group)
-// plus an error word, in the last fm_ctr_bytes(s) bytes of the workspace (16-byte aligned).
-int fm_units(const hta_shape_t &s) {
-    const int G = s.H_kv > 0 ? s.H / s.H_kv : 1;
-    return s.B * s.H_kv * ((s.T * G + kRowsPerTile - 1) / kRowsPerTile);
-}
-size_t fm_ctr_bytes(const hta_shape_t &s) { return (size_t(2 * fm_units(s) + 1) * 4 + 15) / 16 * 16; }
-uint32_t *fm_ctr_ptr(void *ws, size_t ws_bytes, const hta_shape_t &s) {
-    const size_t off = (ws_bytes - fm_ctr_bytes(s)) / 16 * 16;
-    return reinterpret_cast<uint32_t *>(static_cast<uint8_t *>(ws) + off);
-}
-
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -321,15 +307,9 @@ bool t8_eligible(const hta_shape_t &s, const PrefixPlan &pl) {
 hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, const void *k, const void *v,
                         const int32_t *seqlens, float *o_out, float *lse_out, int64_t o_split_stride,
                         int64_t lse_split_stride, cudaStream_t st, const PagedArgs *pg = nullptr,
-                        const Fp8Args *f8 = nullptr, const TreeArgs *tr = nullptr,
-                        const TreeMergeParams *fm = nullptr, uint32_t *fm_ctr = nullptr) {
+                        const Fp8Args *f8 = nullptr, const TreeArgs *tr = nullptr) {
     const hta_shape_t &s = sh.s;
     PrefixParams p{};
-    if (fm != nullptr) {  // fused split combine (bf16 cache, tensor-core kernel)
-        p.fm = *fm;
-        p.fm_ctr = fm_ctr;
-        p.fm_err = fm_ctr + 2 * fm_units(s);
-    }
     if (f8 != nullptr) {
         p.kv8 = 1;
         p.k_scale = f8->k_scale;
@@ -466,16 +446,13 @@ const char *hta_status_string(hta_status_t st) {
 
 int32_t hta_version(void) { return 100; }
 
-int32_t hta_set_fused_merge(int32_t enable) { return g_no_fused_merge.exchange(enable ? 0 : 1) ? 0 : 1; }
-
 size_t hta_workspace_size(const hta_shape_t *shape, int32_t num_sms) {
     Shape sh;
     if (check_shape(shape, &sh) != HTA_OK) return size_t(-1);
     const int sms = num_sms > 0 ? num_sms : kDefaultSms;
     // the larger of the plans with and without the fused tree tiles (hta_forward uses the latter)
     const int splits = std::max(make_plan(sh, sms).splits, make_plan(sh, sms, fused_tree_tiles(sh.s)).splits);
-    const size_t parts = size_t(splits) * part_floats(sh.s) * sizeof(float);
-    return (parts + 15) / 16 * 16 + (sh.s.dtype == HTA_BF16 ? fm_ctr_bytes(sh.s) : 0);
+    return size_t(splits) * part_floats(sh.s) * sizeof(float);
 }
 
 hta_status_t hta_prefix_attn(const hta_shape_t *shape, const void *q, const void *k_cache, const void *v_cache,
@@ -612,6 +589,16 @@ static hta_status_t forward_impl(const PagedArgs *pg, const hta_shape_t *shape, 
     const int64_t ostride = int64_t(s.B) * s.T * s.H * s.d;
     float *lse_ws = o_ws + size_t(pl.splits) * ostride;
     const int64_t lstride = int64_t(s.B) * s.H * s.T;
+    if (ev_begin != nullptr && cudaEventRecord(static_cast<cudaEvent_t>(ev_begin), st) != cudaSuccess)
+        return HTA_ERR_CUDA;
+    r = run_prefix(sh, pl, q, k_cache, v_cache, cache_seqlens, o_ws, lse_ws, ostride, lstride, st, pg, f8, &tr);
+    if (r != HTA_OK) return r;
+    if (ev_end != nullptr && cudaEventRecord(static_cast<cudaEvent_t>(ev_end), st) != cudaSuccess)
+        return HTA_ERR_CUDA;
+    // the tree inputs (k_tree, v_tree, mask) may still be in flight on another stream: only the
+    // tree/merge kernel waits for them, the prefix kernel above does not
+    if (tree_ready != nullptr && cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(tree_ready), 0) != cudaSuccess)
+        return HTA_ERR_CUDA;
     TreeMergeParams p = base_tm(sh);
     p.q = q;
     p.kt = k_tree;
@@ -631,25 +618,6 @@ static hta_status_t forward_impl(const PagedArgs *pg, const hta_shape_t *shape, 
     p.os1 = s.q_strides[1];
     p.os2 = s.q_strides[2];
     p.lse = lse_out;
-    // Fused split combine: the prefix kernel's CTAs merge their unit's rows themselves (no second
-    // kernel) when the bf16 tensor-core kernel runs, the tree inputs are ready on this stream, a
-    // unit's CTAs fit on the SMs at once, and the workspace has room for the unit counters
-    // (hta_workspace_size includes them).
-    const bool fuse_merge = s.dtype == HTA_BF16 && f8 == nullptr && tree_ready == nullptr && !g_no_fused_merge &&
-                            pl.splits * pl.nt <= device_sms() && ws_bytes >= need + fm_ctr_bytes(s);
-    uint32_t *fm_ctr = fuse_merge ? fm_ctr_ptr(ws, ws_bytes, s) : nullptr;
-    if (ev_begin != nullptr && cudaEventRecord(static_cast<cudaEvent_t>(ev_begin), st) != cudaSuccess)
-        return HTA_ERR_CUDA;
-    r = run_prefix(sh, pl, q, k_cache, v_cache, cache_seqlens, o_ws, lse_ws, ostride, lstride, st, pg, f8, &tr,
-                   fuse_merge ? &p : nullptr, fm_ctr);
-    if (r != HTA_OK) return r;
-    if (ev_end != nullptr && cudaEventRecord(static_cast<cudaEvent_t>(ev_end), st) != cudaSuccess)
-        return HTA_ERR_CUDA;
-    if (fuse_merge) return HTA_OK;
-    // the tree inputs (k_tree, v_tree, mask) may still be in flight on another stream: only the
-    // tree/merge kernel waits for them, the prefix kernel above does not
-    if (tree_ready != nullptr && cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(tree_ready), 0) != cudaSuccess)
-        return HTA_ERR_CUDA;
     return launch_tree_merge(p, s.d, s.dtype, s.dtype, ev_end == nullptr, st) == cudaSuccess ? HTA_OK
                                                                                               : HTA_ERR_CUDA;
 }

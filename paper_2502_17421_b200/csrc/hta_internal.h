@@ -39,6 +39,44 @@ struct PrefixPlan {
     int splits;       // S
 };
 
+struct PrefixParams {
+    const void *q;                    // [B,T,H,d] dtype
+    int64_t qs0, qs1, qs2;            // element strides of q
+    const void *k, *v;                // SIMT path only (the tcgen05 path reads via TMA)
+    int64_t ks0, ks1, ks2;
+    const int32_t *seqlens;           // [B] or nullptr
+    int B, T, H, H_kv, d, G, M;
+    int64_t N_max;
+    float scale;                      // softmax scale
+    float scale_log2;                 // scale * log2(e)
+    int nt, n_mgroups, splits, tiles_per_split;
+    int q_tma;                                  // Q rows of a tile come from tmap_q (G divides 128)
+    // Paged KV (page_size > 0, SURVEY.md §8(f) f3): the K/V maps cover a pool of pages seen as
+    // one [rows, H_kv, d] tensor; logical key k of batch b sits at pool row
+    // block_table[b * bt_stride + k / page_size] * page_size + k % page_size.  TMA boxes are 16
+    // rows (page_size % 16 == 0).
+    const int32_t *block_table;
+    int64_t bt_stride;
+    int page_size;
+    int max_pages;                              // entries per block-table row (clamp)
+    // FP8 cache (kv8 = 1, SURVEY.md §8(f) f4): k/v are E4M3 bytes, K = k_scale[g] * E4M3 and
+    // V = v_scale[g] * E4M3 per KV head g (device float [H_kv]); the maps load E4M3 tiles.
+    int kv8;
+    const float *k_scale, *v_scale;
+    // Fused tree pass (hta_forward, bf16 cache): the last split of every unit appends tree_tiles
+    // (= ceil(T / 128)) masked tiles of the tree keys (tmap_kt / tmap_vt over k_tree / v_tree) to
+    // its cache tiles, so its partial already holds the tree part (the Appendix C merge applied
+    // inside the online softmax).  Row r of token t sees tree key s iff mask[b*mask_bs + t*T + s].
+    int tree_tiles;
+    const uint8_t *mask;
+    int64_t mask_bs;
+    const int32_t *parents;           // hta_forward_tree: visibility from parents [b*par_bs + t] instead of mask
+    int64_t par_bs;
+    float *o_out;                     // [S][B][T][H][d] fp32, normalised partials
+    float *lse_out;                   // [S][B][H][T] natural-log LSE
+    int64_t o_split_stride, lse_split_stride;  // elements between splits
+};
+
 constexpr int kMaxP2pRanks = 8;  // ranks of the peer-memory exchange (one NVSwitch node)
 
 struct TreeMergeParams {
@@ -82,53 +120,6 @@ struct TreeMergeParams {
     uint32_t *p2p_counter;
     uint32_t *p2p_peer_flags[kMaxP2pRanks];
     int p2p_nranks, p2p_rank;
-};
-
-struct PrefixParams {
-    const void *q;                    // [B,T,H,d] dtype
-    int64_t qs0, qs1, qs2;            // element strides of q
-    const void *k, *v;                // SIMT path only (the tcgen05 path reads via TMA)
-    int64_t ks0, ks1, ks2;
-    const int32_t *seqlens;           // [B] or nullptr
-    int B, T, H, H_kv, d, G, M;
-    int64_t N_max;
-    float scale;                      // softmax scale
-    float scale_log2;                 // scale * log2(e)
-    int nt, n_mgroups, splits, tiles_per_split;
-    int q_tma;                                  // Q rows of a tile come from tmap_q (G divides 128)
-    // Paged KV (page_size > 0, SURVEY.md §8(f) f3): the K/V maps cover a pool of pages seen as
-    // one [rows, H_kv, d] tensor; logical key k of batch b sits at pool row
-    // block_table[b * bt_stride + k / page_size] * page_size + k % page_size.  TMA boxes are 16
-    // rows (page_size % 16 == 0).
-    const int32_t *block_table;
-    int64_t bt_stride;
-    int page_size;
-    int max_pages;                              // entries per block-table row (clamp)
-    // FP8 cache (kv8 = 1, SURVEY.md §8(f) f4): k/v are E4M3 bytes, K = k_scale[g] * E4M3 and
-    // V = v_scale[g] * E4M3 per KV head g (device float [H_kv]); the maps load E4M3 tiles.
-    int kv8;
-    const float *k_scale, *v_scale;
-    // Fused tree pass (hta_forward, bf16 cache): the last split of every unit appends tree_tiles
-    // (= ceil(T / 128)) masked tiles of the tree keys (tmap_kt / tmap_vt over k_tree / v_tree) to
-    // its cache tiles, so its partial already holds the tree part (the Appendix C merge applied
-    // inside the online softmax).  Row r of token t sees tree key s iff mask[b*mask_bs + t*T + s].
-    int tree_tiles;
-    const uint8_t *mask;
-    int64_t mask_bs;
-    const int32_t *parents;           // hta_forward_tree: visibility from parents [b*par_bs + t] instead of mask
-    int64_t par_bs;
-    float *o_out;                     // [S][B][T][H][d] fp32, normalised partials
-    float *lse_out;                   // [S][B][H][T] natural-log LSE
-    int64_t o_split_stride, lse_split_stride;  // elements between splits
-    // Fused split combine (hta_forward family, bf16 cache; fm_ctr != nullptr): after its partial is
-    // stored every CTA of a unit (b, g, mg) arrives on the unit's counter pair fm_ctr[2*unit..+1]
-    // (zero between calls: the last CTA to leave re-arms it); the unit's softmax warps then run the
-    // tree pass (fm.do_tree) and the merge of fm's row (b, t, h) -- the tree/merge kernel's work --
-    // spread over all the unit's CTAs.  fm_err: set to 1 if a unit waited > 200 ms (a CTA of the
-    // unit never ran; the result is then garbage).
-    uint32_t *fm_ctr;
-    uint32_t *fm_err;
-    TreeMergeParams fm;
 };
 
 // Launchers (return cudaGetLastError() of the launch).

@@ -40,7 +40,6 @@
 
 #include "hta_internal.h"
 #include "ptx_sm100.cuh"
-#include "tree_pass.cuh"
 
 namespace hta {
 
@@ -318,186 +317,13 @@ __device__ __forceinline__ int paged_row(const PrefixParams &p, int b, int k) {
     return e * p.page_size + k % p.page_size;
 }
 
-// ---- Fused split combine (p.fm_ctr != nullptr).  The CTAs of one unit (b, g,
-// row group mg) -- its splits, and both CTAs of a pair -- are co-resident (the host only fuses
-// when splits x CTAs per unit fits on the SMs, and a unit's CTAs are adjacent in launch order),
-// so they can wait for each other: each CTA arrives on the unit's counter once its partial is
-// stored, and its 16 softmax warps (one output row each, round robin over the unit's warps) run
-// the tree pass of their row (overlapping the wait) and, once every CTA of the unit has arrived,
-// the merge of the row's split partials -- the work of tree_merge_kernel, on the SMs that just
-// produced the partials instead of after a second launch.  The last CTA to leave re-arms the
-// counters (they are zero between calls).
-#ifndef HTA_FM_KEYS
-#define HTA_FM_KEYS 4
-#endif
-constexpr uint64_t kFmTimeoutNs = 200000000ull;  // 200 ms: a step takes well under 1 ms
-
-__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-
-// Merge of one row for the fused split combine: the same arithmetic as merge_row (tree_pass.cuh)
-// in compact code -- it runs once per SM after the main loop, from a cold instruction cache, so
-// its size matters more than its instruction count: the partial rows are prefetched into L1 first
-// and then combined by a rolled loop.
-#ifndef HTA_FM_WARM
-#define HTA_FM_WARM 1
-#endif
-#ifndef HTA_FM_COMPACT
-#define HTA_FM_COMPACT 1
-#endif
-template <int D>
-__device__ __forceinline__ void merge_row_compact(const TreeMergeParams &p, int b, int t, int h, int lane,
-                                                  const float (&ot)[D / 32], float lse_t, bool dry) {
-    constexpr int E = D / 32;
-    const int n = dry ? 1 : p.n_parts;  // (dry: the code is walked once, no memory touched)
-    const int64_t lrow = (static_cast<int64_t>(b) * p.Hr + h) * p.T + t;
-    const int64_t orow = ((static_cast<int64_t>(b) * p.T + t) * p.Hr + h) * D + lane * E;
-#pragma unroll 1
-    for (int j = 0; j < n; ++j)
-        if (!dry) prefetch_l1(p.o_parts + j * p.o_part_stride + orow);
-    float mx = lse_t;
-#pragma unroll 1
-    for (int j = lane; j < n; j += 32)
-        mx = fmaxf(mx, dry ? 0.f : __ldcg(p.lse_parts + j * p.lse_part_stride + lrow));
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    float out[E];
-    float lse_out = -INFINITY;
-    if (mx == -INFINITY) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) out[e] = 0.f;
-    } else {
-        const float wt = expf(lse_t - mx);  // 0 when the tree part is a sentinel
-        float W = wt;
-#pragma unroll
-        for (int e = 0; e < E; ++e) out[e] = wt * ot[e];
-#pragma unroll 1
-        for (int j = 0; j < n; ++j) {
-            const float w = expf((dry ? 0.f : p.lse_parts[j * p.lse_part_stride + lrow]) - mx);  // (L1 hits)
-            float v[E];
-            if (dry) {
-#pragma unroll
-                for (int e = 0; e < E; ++e) v[e] = 0.f;
-            } else {
-                VecIO<float, E>::load(p.o_parts + j * p.o_part_stride + orow, v);
-            }
-            W += w;
-#pragma unroll
-            for (int e = 0; e < E; ++e) out[e] = fmaf(w, v[e], out[e]);
-        }
-        const float inv = 1.0f / W;
-#pragma unroll
-        for (int e = 0; e < E; ++e) out[e] *= inv;
-        lse_out = mx + logf(W);
-    }
-    __nv_bfloat16 *dst = static_cast<__nv_bfloat16 *>(p.o) + b * p.os0 + t * p.os1 + h * p.os2 + lane * E;
-    if (dry) return;
-    VecIO<__nv_bfloat16, E>::store(dst, out);
-    if (p.lse != nullptr && lane == 0) p.lse[(static_cast<int64_t>(b) * p.Hr + h) * p.T + t] = lse_out;
-}
-
-#ifndef HTA_FM_DIAG
-#define HTA_FM_DIAG 0  // timing diagnostics only (results wrong): 1 no wait, 2 no row work, 4 nothing
-#endif
-template <int D, bool PAIR>
-__device__ __forceinline__ void fused_merge(const PrefixParams &p, bool dry) {
-    if (HTA_FM_DIAG & 4) return;
-    // (special registers read with volatile moves, so that the compiler cannot keep the main
-    // loop's copies of these values live across it)
-    uint32_t tid, cta;
-    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
-    asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(cta));
-    const int sw = static_cast<int>(tid >> 5), lane = static_cast<int>(tid & 31);
-    constexpr int n_cta_pair = PAIR ? 2 : 1;
-    const int rank = PAIR ? static_cast<int>(cluster_ctarank()) : 0;
-    int rest = static_cast<int>(PAIR ? (cta >> 1) : cta);
-    const int mg = rest % p.n_mgroups;
-    rest /= p.n_mgroups;
-    const int split = rest % p.splits;
-    rest /= p.splits;
-    const int g = rest % p.H_kv;
-    const int b = rest / p.H_kv;
-    const int unit = (b * p.H_kv + g) * p.n_mgroups + mg;
-    uint32_t *arrive = p.fm_ctr + 2 * unit;
-    uint32_t *depart = arrive + 1;
-    const uint32_t n_cta = static_cast<uint32_t>(p.splits * n_cta_pair);
-    // arrival (the grid-barrier pattern): the 16 softmax warps meet on named barrier 2 once their
-    // partial stores are issued; one thread fences at gpu scope (cumulative over the CTA's stores
-    // ordered before it by the barrier) and arrives
-    if (!dry) named_bar_sync(2, 32 * 16);
-    if (tid == 0 && !dry) {
-        fence_acq_rel_gpu();
-        atomicAdd(arrive, 1u);
-    }
-    const TreeMergeParams &f = p.fm;
-    const int rows0 = mg * kRowsPerTile * n_cta_pair;
-    const int rows_u = min(kRowsPerTile * n_cta_pair, p.M - rows0);
-    const int n_w = static_cast<int>(n_cta) * 16;
-    int lr = dry ? 0 : (split * n_cta_pair + rank) * 16 + sw;
-    // the tree pass of this warp's first row overlaps the wait for the unit's other CTAs
-    float ot[D / 32];
-    float lse_t = -INFINITY;
-#pragma unroll
-    for (int e = 0; e < D / 32; ++e) ot[e] = 0.f;
-    if (f.do_tree && lr < rows_u && !(HTA_FM_DIAG & 2) && !dry) {
-        const int grow = rows0 + lr;
-        lse_t = tree_row<__nv_bfloat16, D, HTA_FM_KEYS>(f, b, grow / p.G, g * p.G + grow % p.G, lane, ot);
-    }
-    // one thread polls the unit's counter (relaxed loads, backing off), then fences (acquire side)
-    // and releases the other warps
-    if (tid == 0 && !(HTA_FM_DIAG & 1) && !dry) {
-        const uint64_t t0 = global_ns();
-        while (ld_relaxed_gpu(arrive) < n_cta) {
-            __nanosleep(64);
-            if (global_ns() - t0 > kFmTimeoutNs) {
-                atomicExch(p.fm_err, 1u);
-                break;
-            }
-        }
-        fence_acq_rel_gpu();
-    }
-    if (!dry) named_bar_sync(2, 32 * 16);
-    for (; lr < rows_u && !(HTA_FM_DIAG & 2); lr += n_w) {
-        const int grow = rows0 + lr;
-        const int t = grow / p.G, h = g * p.G + grow % p.G;
-        if (HTA_FM_COMPACT)
-            merge_row_compact<D>(f, b, t, h, lane, ot, lse_t, dry);
-        else
-            merge_row<__nv_bfloat16, D, true>(f, b, t, h, lane, ot, lse_t);
-        if (dry) break;
-        if (f.do_tree && lr + n_w < rows_u) {  // (T > 64 with few splits: more rows per warp)
-            const int gn = rows0 + lr + n_w;
-            lse_t = tree_row<__nv_bfloat16, D, HTA_FM_KEYS>(f, b, gn / p.G, g * p.G + gn % p.G, lane, ot);
-        }
-    }
-    // departure: the last CTA of the unit to leave re-arms both counters (every CTA has passed its
-    // wait by then)
-    if (dry) return;
-    named_bar_sync(2, 32 * 16);
-    if (tid == 0 && atomicAdd(depart, 1u) + 1u == n_cta) {
-        atomicExch(arrive, 0u);
-        atomicExch(depart, 0u);
-    }
-}
-
-// (the copy for empty splits, out of line: inlined there it would raise the register pressure of
-// the whole kernel)
-template <int D, bool PAIR>
-__device__ __noinline__ void fused_merge_ool(const PrefixParams &p, bool dry) {
-    fused_merge<D, PAIR>(p, dry);
-}
-
 // TREE: the fused tree pass (tree tiles appended to the last split); the kernels without it carry
 // none of its code, so their schedule is exactly that of the plain prefix pass.
 template <int D, bool PAIR, bool KV8, bool TREE>
 __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     prefix_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
                      const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ CUtensorMap tmap_kt,
-                     const __grid_constant__ CUtensorMap tmap_vt, const __grid_constant__ PrefixParams p) {
+                     const __grid_constant__ CUtensorMap tmap_vt, const PrefixParams p) {
     using C = TcCfg<D, PAIR>;
     using Spec = SpecCfg<KV8>;
     extern __shared__ __align__(1024) uint8_t smem[];  // 128B-swizzled tiles need 1024B alignment
@@ -636,12 +462,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);
             lse_base[(static_cast<int64_t>(b) * p.H + h) * p.T + t] = -INFINITY;
         }
-        if (!KV8 && p.fm_ctr != nullptr && warp < kOtherBase) fused_merge_ool<D, PAIR>(p, false);
     } else if (warp >= kOtherBase && warp < kOtherBase + 4) {
-        // fused split combine: the spare warp walks its code once now (no memory touched), so that
-        // the softmax warps do not run it from a cold instruction cache after the main loop
-        if (HTA_FM_WARM && !KV8 && p.fm_ctr != nullptr && warp == kOtherBase + (HTA_MMA_SLOT == 1 ? 3 : 1))
-            fused_merge_ool<D, PAIR>(p, true);
         setmaxnreg_dec<KV8>();
         if (warp == kWarpK) {
             // ================= TMA producer of Q and the K ring (K_j is consumed by S_j).  K and V
@@ -1386,7 +1207,6 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         }
         if (row_ok && chalf == 0 && grp == 0)
             lse_base[(static_cast<int64_t>(b) * p.H + h) * p.T + t] = (m_tot + log2f(l_tot)) * 0.69314718055994530942f;
-        if (!KV8 && p.fm_ctr != nullptr) fused_merge_ool<D, PAIR>(p, false);
     }
 
     HTA_TR(63, 0);

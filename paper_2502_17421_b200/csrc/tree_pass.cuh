@@ -79,11 +79,11 @@ struct VecIO<__nv_bfloat16, 2> {
 // Tree pass of one output row: normalised tree partial in ot[] and its natural-log LSE.  W = 64-bit
 // words of the row's visibility (1 for T <= 64, 4 for T <= 256): the set is built and walked with
 // 64-bit ballots / find-first-set, so a small tree costs no per-word selects.
-template <typename Tin, int D, int W, int kKeys = 8>
+template <typename Tin, int D, int W>
 __device__ __forceinline__ float tree_row_w(const TreeMergeParams &p, int b, int t, int h, int lane,
                                             float (&ot)[D / 32]) {
     constexpr int E = D / 32;
-    // kKeys: visible keys whose K and V rows are in flight at once
+    constexpr int kKeys = 8;  // visible keys whose K and V rows are in flight at once
     const int g = h / p.G;
 #pragma unroll
     for (int e = 0; e < E; ++e) ot[e] = 0.f;
@@ -198,10 +198,9 @@ __device__ __forceinline__ float tree_row_w(const TreeMergeParams &p, int b, int
     return static_cast<float>(m_acc + static_cast<Acc>(logf(l)));
 }
 
-template <typename Tin, int D, int kKeys = 8>
+template <typename Tin, int D>
 __device__ __forceinline__ float tree_row(const TreeMergeParams &p, int b, int t, int h, int lane, float (&ot)[D / 32]) {
-    return p.T <= 64 ? tree_row_w<Tin, D, 1, kKeys>(p, b, t, h, lane, ot)
-                     : tree_row_w<Tin, D, 4, kKeys>(p, b, t, h, lane, ot);
+    return p.T <= 64 ? tree_row_w<Tin, D, 1>(p, b, t, h, lane, ot) : tree_row_w<Tin, D, 4>(p, b, t, h, lane, ot);
 }
 
 // Loads of partials written during the same kernel by other CTAs: L2 only (ld.global.cg).

@@ -40,7 +40,6 @@ _SIG = {
     "hta_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "hta_version": (ctypes.c_int32, []),
     "hta_workspace_size": (ctypes.c_size_t, [ctypes.POINTER(hta_shape_t), ctypes.c_int32]),
-    "hta_set_fused_merge": (ctypes.c_int32, [ctypes.c_int32]),
     "hta_prefix_attn": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
     "hta_tree_attn": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), _P, _P, _P, _P, ctypes.c_int64, _P, _P, _P]),
     "hta_merge_lse": (ctypes.c_int, [ctypes.POINTER(hta_shape_t), ctypes.c_int32, _P, _P, _P, _P, _P]),
@@ -158,12 +157,6 @@ def workspace_size(shape: hta_shape_t, num_sms: int = 0) -> int:
     if n == ctypes.c_size_t(-1).value:
         raise HtaError("hta_workspace_size", 1)
     return n
-
-
-def set_fused_merge(enable: bool) -> bool:
-    """hta_set_fused_merge: the split combine inside the prefix kernel (default) or as its own
-    kernel; returns the previous setting."""
-    return bool(lib().hta_set_fused_merge(1 if enable else 0))
 
 
 def _num_sms(dev) -> int:

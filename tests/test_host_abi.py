@@ -54,35 +54,26 @@ def _shape(B=1, T=64, H=32, H_kv=8, d=128, N=65536, dtype=hta.HTA_BF16, splits=0
 
 
 def test_workspace_size_matches_split_plan(L):
-    # split partials, then (bf16) the fused split combine's unit counters: two words per
-    # (b, kv head, 128-row group) and an error word, rounded to 16 bytes (include/hta.h)
-    def ctr(s):
-        G = s.H // s.H_kv
-        return ((2 * s.B * s.H_kv * ((s.T * G + 127) // 128) + 1) * 4 + 15) // 16 * 16
-    part1 = lambda s: (s.B * s.T * s.H * s.d + s.B * s.H * s.T) * 4
-    part = lambda s: part1(s)  # (multiples of 16 bytes in the shapes below)
-
-    def size(k, s):
-        return k * part(s) + ctr(s)
+    part = lambda s: (s.B * s.T * s.H * s.d + s.B * s.H * s.T) * 4
     # Llama-8B-64k: M = 256 rows per kv head -> one CTA pair per kv head, 8 pairs = 16 CTAs per
     # split, 9 splits = 144 CTAs
     s = _shape()
-    assert L.hta_workspace_size(ctypes.byref(s), 148) == size(9, s)
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == 9 * part(s)
     # forced splits are capped by the number of 128-key tiles (and rounded to whole tiles per
     # split); the size covers the larger of the plans without and with the fused tree pass's
     # tree tile (hta_forward): N=300: 3 tiles -> 3 splits, 3 + 1 tree tile -> 4 splits;
     # N=1000: 8 tiles in 7 splits = 2 per split = 4 splits, 8 + 1 -> 2 per split = 5 splits
     s = _shape(N=300, splits=7)
-    assert L.hta_workspace_size(ctypes.byref(s), 148) == size(4, s)
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == 4 * part(s)
     s = _shape(N=1000, splits=7)
-    assert L.hta_workspace_size(ctypes.byref(s), 148) == size(5, s)
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == 5 * part(s)
     s = _shape(N=0)
-    assert L.hta_workspace_size(ctypes.byref(s), 148) == size(1, s)
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == 1 * part(s)
     # QwQ-like: M = 320 rows.  Pairs: 2 row groups x 8 kv heads x B=4 = 128 CTAs per split, best
     # 1 split (one wave of 256 tiles).  Single CTAs: 3 row groups = 96 CTAs per split, 3 splits =
     # 288 CTAs = 2 waves of 86 tiles -> the planner takes single CTAs with 3 splits
     s = _shape(B=4, H=40, N=32768)
-    assert L.hta_workspace_size(ctypes.byref(s), 148) == size(3, s)
+    assert L.hta_workspace_size(ctypes.byref(s), 148) == 3 * part(s)
 
 
 @pytest.mark.parametrize("field,value", [("T", 0), ("T", 257), ("H", 30), ("d", 96), ("N_max", -1),
@@ -224,5 +215,4 @@ def test_max_seqlen_hint_shrinks_the_plan(L):
     small = _shape(N=8192)
     assert L.hta_workspace_size(ctypes.byref(hinted), 148) == L.hta_workspace_size(ctypes.byref(small), 148)
     assert L.hta_workspace_size(ctypes.byref(full), 148) >= L.hta_workspace_size(ctypes.byref(hinted), 148)
-    ctr = ((2 * 1 * 8 * 2 + 1) * 4 + 15) // 16 * 16  # the fused merge's unit counters (16 units)
-    assert (L.hta_workspace_size(ctypes.byref(hinted), 148) - ctr) % part(hinted) == 0
+    assert L.hta_workspace_size(ctypes.byref(hinted), 148) % part(hinted) == 0
