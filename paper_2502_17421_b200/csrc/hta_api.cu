@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 
 #include "hta_internal.h"
@@ -364,7 +365,11 @@ hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, co
         if (f8 != nullptr) {
             // a CTA of a pair loads half of each K tile (64 keys, all d) and half of each V tile
             // (64 columns, all 128 keys) -- the same halves as the bf16 cache
-            if ((r = make_kv_map_fp8(&tk, k, s, s.d, pl.nt == 2 ? kBlockN / 2 : kBlockN)) != HTA_OK) return r;
+            // (d = 128, single CTAs: the E4M3 K tile is the MMA operand itself, landed 128-byte swizzled)
+            if ((r = make_kv_map_fp8(&tk, k, s, s.d, pl.nt == 2 ? kBlockN / 2 : kBlockN,
+                                     s.d == 128 && pl.nt == 1 && HTA_F8S)) !=
+                HTA_OK)
+                return r;
             if ((r = make_kv_map_fp8(&tv, v, s, pl.nt == 2 ? 64 : s.d, kBlockN)) != HTA_OK) return r;
         } else if (pg != nullptr) {
             if ((r = make_pool_map(&tk, k, s, *pg)) != HTA_OK) return r;

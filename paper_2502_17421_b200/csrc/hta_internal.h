@@ -19,6 +19,12 @@ namespace hta {
 #define HTA_FUSE_PAIRS 0
 #endif
 
+// FP8 cache, d = 128: S = Q K^T on kind::f8f6f4 over the E4M3 K tile (q as two E4M3 terms); 0 =
+// the K tile widened to f16 like V
+#ifndef HTA_F8S
+#define HTA_F8S 1
+#endif
+
 #ifndef HTA_BLOCK_N
 #define HTA_BLOCK_N 128
 #endif

@@ -35,7 +35,9 @@
 //  * epilogue (both groups: half of the head dim each): O / row sum -> fp32 partial + LSE.
 // A split with no visible key writes the sentinel (O = 0, LSE = -inf).
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "hta_internal.h"
@@ -109,6 +111,9 @@ __device__ __forceinline__ float fold_max(float m, float rho) { return rho > m +
 #define HTA_WIDEN_UNROLL 4
 #endif
 constexpr int kWidenUnroll = HTA_WIDEN_UNROLL;  // (4 with the 48-register producers)
+#ifndef HTA_F8S
+#define HTA_F8S 1  // FP8 cache, d = 128: S on kind::f8f6f4 over the E4M3 K tile (0: K widened to f16)
+#endif
 #ifndef HTA_L2_AHEAD
 #define HTA_L2_AHEAD 0
 #endif
@@ -297,7 +302,8 @@ struct TcCfg {
     static constexpr int kBarOff = kVOff + kSlotsV * kVBytes;
     static constexpr int kNumBars = 3 * kSlotsK + 3 * kSlotsV + 3 * kSBufs + 4;
     static constexpr int kMaxOff = kBarOff + 8 * kNumBars + 8;  // row-max hand-over rho[3][128]
-    static constexpr int kSmemBytes = kMaxOff + 3 * 128 * 4;    // base is 1024-aligned (__align__ below)
+    static constexpr int kQScaleOff = kMaxOff + 3 * 128 * 4;   // FP8 S path: the q scale exponent of each row
+    static constexpr int kSmemBytes = kQScaleOff + 128 * 4;     // base is 1024-aligned (__align__ below)
     static_assert(kSlotsK >= 2 && kSlotsV >= 2, "need at least 2 slots per ring");
     static_assert(kSmemBytes <= 232448, "shared memory budget");
     static_assert(8 * 128 * 4 <= kSlotsK * kKBytes, "the epilogue exchange reuses the K ring");
@@ -326,6 +332,11 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                      const __grid_constant__ CUtensorMap tmap_vt, const PrefixParams p) {
     using C = TcCfg<D, PAIR>;
     using Spec = SpecCfg<KV8>;
+    // FP8 cache, d = 128, single CTAs: S = Q K^T runs on kind::f8f6f4 with the E4M3 K tile as landed
+    // by TMA (no widening) and q as the sum of two E4M3 terms (q_hi + q_lo, per-CTA power-of-two
+    // scale), so only V is widened to f16.  CTA pairs keep the widened K (their
+    // one V producer warp per CTA sets the pace: the E4M3 S path measured 124.8 vs 115.5 us there).
+    constexpr bool F8S = KV8 && D == 128 && !PAIR && HTA_F8S;
     extern __shared__ __align__(1024) uint8_t smem[];  // 128B-swizzled tiles need 1024B alignment
     uint8_t *sQ = smem;
     uint8_t *sK = smem + C::kQBytes;
@@ -392,7 +403,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         // the FP8 variant fills a slot by widening in place: its full barrier counts one arrival per
         // CTA (no TMA bytes); the E4M3 tile's TMA completes on the CTA's own land barrier
         for (int i = 0; i < C::kSlotsK; ++i) {
-            mbar_init(&k_full[i], KV8 && PAIR ? 2 : (wide ? kWideWarps : 1));
+            mbar_init(&k_full[i], F8S ? 1 : (KV8 && PAIR ? 2 : (wide ? kWideWarps : 1)));
             mbar_init(&k_empty[i], 1);
             mbar_init(&k_land[i], 1);
         }
@@ -507,11 +518,35 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                         const int slot = j % C::kSlotsK;
                         mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);
                         HTA_TR(30, j);
-                        mbar_arrive_expect_tx(&k_land[slot], C::kKBytes / 2);
-                        tma_load_4d(sK + slot * C::kKBytes + C::kKBytes / 2, &tmap_k, &k_land[slot], 0, g,
-                                    static_cast<int>(key_lo) + j * kBlockN, b, kKvPolicy);
+                        if (F8S) {  // the E4M3 tile is the MMA operand: lands on k_full at the slot base
+                            mbar_arrive_expect_tx(&k_full[slot], C::kKBytes / 2);
+                            tma_load_4d(sK + slot * C::kKBytes, &tmap_k, &k_full[slot], 0, g,
+                                        static_cast<int>(key_lo) + j * kBlockN, b, kKvPolicy);
+                        } else {
+                            mbar_arrive_expect_tx(&k_land[slot], C::kKBytes / 2);
+                            tma_load_4d(sK + slot * C::kKBytes + C::kKBytes / 2, &tmap_k, &k_land[slot], 0, g,
+                                        static_cast<int>(key_lo) + j * kBlockN, b, kKvPolicy);
+                        }
                         if (kL2Ahead > 0 && j + kL2Ahead < n_tiles)
                             tma_prefetch_l2_4d(&tmap_k, 0, g, static_cast<int>(key_lo) + (j + kL2Ahead) * kBlockN, b);
+                    }
+            } else if (F8S) {
+                // FP8 cache, E4M3 S operand: lane 0 lands each tile at its slot base on k_full (a pair
+                // on the leader's barrier, both halves)
+                if (lane == 0)
+                    for (int j = 0; j < n_tiles; ++j) {
+                        const int slot = j % C::kSlotsK;
+                        mbar_wait(&k_empty[slot], ((j / C::kSlotsK) & 1) ^ 1u);
+                        HTA_TR(30, j);
+                        const int n0 = static_cast<int>(key_lo) + j * kBlockN;
+                        if (PAIR) {
+                            if (leader) mbar_arrive_expect_tx(&k_full[slot], C::kKBytes);
+                            tma_load_4d_pair(sK + slot * C::kKBytes, &tmap_k, kfull0 + 8u * slot, 0, g,
+                                             n0 + static_cast<int>(rank) * C::kKRows, b, kKvPolicy);
+                        } else {
+                            mbar_arrive_expect_tx(&k_full[slot], C::kKBytes / 2);
+                            tma_load_4d(sK + slot * C::kKBytes, &tmap_k, &k_full[slot], 0, g, n0, b, kKvPolicy);
+                        }
                     }
             } else if constexpr (KV8) {
                 // FP8 cache: the whole warp loads E4M3 tiles kLead tiles ahead (lane 0 issues the
@@ -787,7 +822,8 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             // (needs K_{j+3}; its buffer was last read by PV_j, issued just before).
             constexpr int kM = PAIR ? 256 : 128;
             // FP8 cache: Q, the widened K/V and P are f16 (E4M3 and bf16 Q convert exactly)
-            const uint32_t idesc_qk = KV8 ? idesc_f16_f32(kM, kBlockN, 0) : idesc_bf16_f32(kM, kBlockN, 0);
+            const uint32_t idesc_qk = F8S ? idesc_e4m3_f32(kM, kBlockN)
+                                          : (KV8 ? idesc_f16_f32(kM, kBlockN, 0) : idesc_bf16_f32(kM, kBlockN, 0));
             const uint32_t idesc_pv = KV8 ? idesc_f16_f32(kM, D, 1) : idesc_bf16_f32(kM, D, 1);
             const uint64_t qd0 = sdesc_sw128(smem_u32(sQ), 16, 1024);
             const uint64_t kd0 = sdesc_sw128(smem_u32(sK), 16, 1024);
@@ -807,15 +843,29 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 if (issuer) {
                     const uint32_t d_t = tmem + s_col(jj % C::kSBufs);
                     const uint64_t kd = kd0 + static_cast<uint32_t>(((jj % C::kSlotsK) * C::kKBytes) >> 4);
+                    if constexpr (F8S) {
+                        // E4M3 K-major SW128: one 128-byte atom per row (d = 128), +32 B per K step
+                        // of 32; q_hi at sQ, q_lo 16 KB further
 #pragma unroll
-                    for (int k = 0; k < D / 16; ++k) {
-                        // K-major SW128: +32 B per K step inside a 128-B atom, next atom = next region
-                        const uint32_t qo = ((k / 4) * C::kRegionBytes + (k % 4) * 32) >> 4;
-                        const uint32_t ko = ((k / 4) * (C::kKRows * 128) + (k % 4) * 32) >> 4;
-                        if (PAIR)
-                            mma2_bf16_ss(d_t, qd0 + qo, kd + ko, idesc_qk, k > 0 ? 1u : 0u);
-                        else
-                            mma_bf16_ss(d_t, qd0 + qo, kd + ko, idesc_qk, k > 0 ? 1u : 0u);
+                        for (int k = 0; k < 8; ++k) {
+                            const uint32_t qo = (((k / 4) * 16384) + (k % 4) * 32) >> 4;
+                            const uint32_t ko = ((k % 4) * 32) >> 4;
+                            if (PAIR)
+                                mma2_e4m3_ss(d_t, qd0 + qo, kd + ko, idesc_qk, k > 0 ? 1u : 0u);
+                            else
+                                mma_e4m3_ss(d_t, qd0 + qo, kd + ko, idesc_qk, k > 0 ? 1u : 0u);
+                        }
+                    } else {  // (braced: a pragma between `else` and its loop detaches what follows)
+#pragma unroll
+                        for (int k = 0; k < D / 16; ++k) {
+                            // K-major SW128: +32 B per K step inside a 128-B atom, next atom = next region
+                            const uint32_t qo = ((k / 4) * C::kRegionBytes + (k % 4) * 32) >> 4;
+                            const uint32_t ko = ((k / 4) * (C::kKRows * 128) + (k % 4) * 32) >> 4;
+                            if (PAIR)
+                                mma2_bf16_ss(d_t, qd0 + qo, kd + ko, idesc_qk, k > 0 ? 1u : 0u);
+                            else
+                                mma_bf16_ss(d_t, qd0 + qo, kd + ko, idesc_qk, k > 0 ? 1u : 0u);
+                        }
                     }
                     commit(&s_full[jj % C::kSBufs]);
                     commit(&k_empty[jj % C::kSlotsK]);
@@ -893,19 +943,72 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     val[i] = __ldg(reinterpret_cast<const uint4 *>(q + b * p.qs0 + t * p.qs1 + h * p.qs2 + ch * 8));
                 }
             }
+            if constexpr (F8S) {
+                // q -> q_hi + q_lo (two E4M3 tiles, K-major SW128, 128-byte rows) at a power-of-two
+                // scale 2^e per row (max |q_row| 2^e < 256): q_hi = E4M3(q 2^e), q_lo = E4M3(q 2^e -
+                // q_hi) hold each bf16 element to within 2^-17 of its row's maximum (exactly when
+                // the element is within 2^-10 of it); the softmax folds 2^-e into its row's scale.
+                // A row's 16 chunks are 16 consecutive lanes of one warp (two rows per warp per i).
+                int32_t *qsc = reinterpret_cast<int32_t *>(smem + C::kQScaleOff);
+                int esr[kPer];
 #pragma unroll
-            for (int i = 0; i < kPer; ++i) {
-                const int idx = qt + i * kQThreads;
-                const int r = idx / kChunks, ch = idx % kChunks;
-                if constexpr (KV8) {  // bf16 -> f16 (exact for |q| in the f16 range)
-                    uint32_t *w = reinterpret_cast<uint32_t *>(&val[i]);
+                for (int i = 0; i < kPer; ++i) {
+                    const uint32_t *w = reinterpret_cast<const uint32_t *>(&val[i]);
+                    float mx = 0.f;
 #pragma unroll
                     for (int e = 0; e < 4; ++e)
-                        w[e] = pack_f16x2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xFFFF0000u));
+                        mx = fmaxf(mx, fmaxf(fabsf(__uint_as_float(w[e] << 16)), fabsf(__uint_as_float(w[e] & 0xFFFF0000u))));
+#pragma unroll
+                    for (int off = 8; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+                    int ex = 0;
+                    frexpf(mx, &ex);  // mx < 2^ex
+                    esr[i] = mx > 0.f ? 8 - ex : 0;
+                    const int idx = qt + i * kQThreads;
+                    if ((lane & 15) == 0 && idx < kRowsPerTile * kChunks) qsc[idx / kChunks] = esr[i];
                 }
-                if (idx < kRowsPerTile * kChunks)
-                    *reinterpret_cast<uint4 *>(sQ + (ch / 8) * C::kRegionBytes + r * 128 + (((ch & 7) ^ (r & 7)) << 4)) =
-                        val[i];
+#pragma unroll
+                for (int i = 0; i < kPer; ++i) {
+                    const int idx = qt + i * kQThreads;
+                    const int r = idx / kChunks, ch = idx % kChunks;  // 8 elements: bytes [ch*8, +8) of row r
+                    const uint32_t *w = reinterpret_cast<const uint32_t *>(&val[i]);
+                    const int es = esr[i];
+                    uint32_t hi[2], lo[2];
+#pragma unroll
+                    for (int e = 0; e < 4; e += 2) {
+                        const float x0 = ldexpf(__uint_as_float(w[e] << 16), es);
+                        const float x1 = ldexpf(__uint_as_float(w[e] & 0xFFFF0000u), es);
+                        const float x2 = ldexpf(__uint_as_float(w[e + 1] << 16), es);
+                        const float x3 = ldexpf(__uint_as_float(w[e + 1] & 0xFFFF0000u), es);
+                        const uint16_t h01 = f32x2_to_e4m3x2(x0, x1), h23 = f32x2_to_e4m3x2(x2, x3);
+                        const uint32_t u01 = e4m3x2_to_f16x2(h01), u23 = e4m3x2_to_f16x2(h23);
+                        const __half2 f01 = *reinterpret_cast<const __half2 *>(&u01);
+                        const __half2 f23 = *reinterpret_cast<const __half2 *>(&u23);
+                        const uint16_t l01 = f32x2_to_e4m3x2(x0 - __low2float(f01), x1 - __high2float(f01));
+                        const uint16_t l23 = f32x2_to_e4m3x2(x2 - __low2float(f23), x3 - __high2float(f23));
+                        hi[e / 2] = static_cast<uint32_t>(h01) | (static_cast<uint32_t>(h23) << 16);
+                        lo[e / 2] = static_cast<uint32_t>(l01) | (static_cast<uint32_t>(l23) << 16);
+                    }
+                    if (idx < kRowsPerTile * kChunks) {
+                        const int off = r * 128 + ((((ch >> 1) ^ (r & 7))) << 4) + (ch & 1) * 8;
+                        *reinterpret_cast<uint2 *>(sQ + off) = make_uint2(hi[0], hi[1]);
+                        *reinterpret_cast<uint2 *>(sQ + 16384 + off) = make_uint2(lo[0], lo[1]);
+                    }
+                }
+            } else {  // (braced: a pragma between `else` and its loop detaches what follows)
+#pragma unroll
+                for (int i = 0; i < kPer; ++i) {
+                    const int idx = qt + i * kQThreads;
+                    const int r = idx / kChunks, ch = idx % kChunks;
+                    if constexpr (KV8) {  // bf16 -> f16 (exact for |q| in the f16 range)
+                        uint32_t *w = reinterpret_cast<uint32_t *>(&val[i]);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            w[e] = pack_f16x2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xFFFF0000u));
+                    }
+                    if (idx < kRowsPerTile * kChunks)
+                        *reinterpret_cast<uint4 *>(sQ + (ch / 8) * C::kRegionBytes + r * 128 +
+                                                   (((ch & 7) ^ (r & 7)) << 4)) = val[i];
+                }
             }
             fence_proxy_async_smem();  // generic-proxy stores -> read by the tensor core
             __syncwarp();
@@ -923,7 +1026,11 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
         const int grow = row0 + r;
         const bool pad_warp = row0 + quarter * 32 + rh * 16 >= p.M;  // warp-uniform
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32 + rh * 16) << 16;
-        const float c = KV8 ? p.scale_log2 * p.k_scale[g] : p.scale_log2;  // K = k_scale[g] * E4M3
+        float c = KV8 ? p.scale_log2 * p.k_scale[g] : p.scale_log2;  // K = k_scale[g] * E4M3
+        if constexpr (F8S) {  // S holds (q 2^e) K: undo the row's q scale (group 0 wrote e)
+            named_bar_sync(1, 32 * 2 * C::kGroupWarps);
+            c = ldexpf(c, -reinterpret_cast<const int32_t *>(smem + C::kQScaleOff)[r]);
+        }
         const uint32_t pfull0 = PAIR ? mapa_shared(smem_u32(&p_full[0]), 0) : 0u;
         constexpr int kHalf = kBlockN / 2;  // S columns per thread
         // m_run: the row's running max (log2 units) as last known to this group; the group's row
@@ -965,7 +1072,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 const int wi = band * 2 + (quarter - 2);
                 const bool kw = wi < kWideWarps;
                 const int part = wi % kWideWarps;
-                for (int j = 0; j < n_tiles; ++j) {
+                for (int j = 0; j < n_tiles && !(F8S && kw); ++j) {
                     const int slot = j % (kw ? C::kSlotsK : C::kSlotsV);
                     const uint32_t par = static_cast<uint32_t>((j / (kw ? C::kSlotsK : C::kSlotsV)) & 1);
                     if (kw) {
@@ -992,6 +1099,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             const bool tree_tile = TREE && j >= nc;  // a tree tile of the fused tree pass
             const int buf = j % C::kSBufs;
             mbar_wait(&s_full[buf], static_cast<uint32_t>((j / C::kSBufs) & 1));
+
             tc_fence_after();
             HTA_TRS(0);
             if (pad_warp) {
@@ -1235,7 +1343,12 @@ static cudaError_t launch_tc(const PrefixParams &p, const CUtensorMap &tq, const
     using C = TcCfg<D, PAIR>;
     auto kern = prefix_tc_kernel<D, PAIR, KV8, TREE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {
+        if (std::getenv("HTA_DEBUG") != nullptr)
+            std::fprintf(stderr, "prefix_tc_kernel<%d,%d,%d,%d>: set smem %d: %s\n", D, PAIR, KV8, TREE, C::kSmemBytes,
+                         cudaGetErrorString(e));
+        return e;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.n_mgroups * p.splits * p.H_kv * p.B * (PAIR ? 2 : 1));
     cfg.blockDim = dim3(C::kThreads);
@@ -1253,8 +1366,10 @@ static cudaError_t launch_tc(const PrefixParams &p, const CUtensorMap &tq, const
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tkt, tvt, p);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess && std::getenv("HTA_DEBUG") != nullptr)
+        std::fprintf(stderr, "prefix_tc_kernel<%d,%d,%d,%d>: launch: %s\n", D, PAIR, KV8, TREE, cudaGetErrorString(e));
+    return e;
 }
 
 int prefix_tc_smem_bytes(int d, int nt) {

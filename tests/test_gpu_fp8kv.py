@@ -92,3 +92,28 @@ def test_fp8kv_logit_jump_past_f16_range(cuda_device, key):
     oc, lc = hta.hta_prefix_attn_fp8kv(q.to(dev), k8.to(dev), v8.to(dev), ks.to(dev), vs.to(dev))
     torch.cuda.synchronize()
     compare(oc, lc, oc_ref, lc_ref, "bf16", "fp8 jump")
+
+
+@pytest.mark.parametrize("spread", ["rows", "elements"])
+def test_fp8kv_q_dynamic_range(cuda_device, spread):
+    """Single-CTA units with d = 128 compute S on kind::f8f6f4 with q split into two E4M3 terms at
+    one power-of-two scale per CTA.  q rows (or elements within a row) spanning
+    ~2^14 in magnitude, and values large enough to need the scale (|q| up to 300), must still meet
+    the bf16 tolerances against the oracle over the exact bf16 q."""
+    w = make_workload(2, 64, 8, 8, 128, 1500, "bf16", dist="V1", seed=31, tree="beam")
+    g = torch.Generator().manual_seed(5)
+    if spread == "rows":  # row scales 2^-7 .. 2^7 (per token, all heads)
+        f = torch.pow(2.0, torch.randint(-7, 8, (2, 64, 1, 1), generator=g).float())
+    else:  # element scales 2^-7 .. 2^7 within every row
+        f = torch.pow(2.0, torch.randint(-7, 8, (2, 64, 8, 128), generator=g).float())
+    q = (w.q.float() * f * 0.05).to(torch.bfloat16)
+    q[0, 0, 0, 0] = 300.0  # one large element: the CTA scale must keep it in E4M3 range
+    w.q = q
+    mask = oracle_masks(w)
+    k8, ks, v8, vs, x = _fp8(w, cuda_device)
+    o_ref, l_ref = oracle.attention_fp8kv(w.q, k8, v8, ks, vs, w.k_tree, w.v_tree, mask)
+    o, l = hta.hta_forward_fp8kv(w.q.to(cuda_device), x["k8"], x["v8"], x["ks"], x["vs"],
+                                 w.k_tree.to(cuda_device), w.v_tree.to(cuda_device),
+                                 torch.from_numpy(mask).to(cuda_device))
+    torch.cuda.synchronize()
+    compare(o, l, o_ref, l_ref, "bf16", f"fp8 q spread {spread}")
