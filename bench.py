@@ -769,8 +769,9 @@ def bench_fp8(dev, flush, k=10, name="longchat7b_16k"):
     torch.cuda.empty_cache()
     return {"workload": name, "us": res["fp8"], "bf16_us": res["bf16"], "roofline_us": t_roof * 1e6,
             "frac_of_roofline": t_roof * 1e6 / res["fp8"], "bound": "hbm",
-            "note": "hta_forward_fp8kv (E4M3 cache, per-KV-head scales; tiles widened to f16 in shared memory by the "
-                    "padding-row softmax warps, <= 64 rows per KV head) vs hta_forward on the bf16 cache; roofline on the E4M3 bytes + Q/O"}
+            "note": "hta_forward_fp8kv (E4M3 cache, per-KV-head scales; S on kind::f8f6f4 straight from the E4M3 K "
+                    "tile with q as two E4M3 terms, V widened to f16 in shared memory by the padding-row softmax warps, "
+                    "<= 64 rows per KV head) vs hta_forward on the bf16 cache; roofline on the E4M3 bytes + Q/O"}
 
 
 def bench_config(name, dev, flush, k=10):
