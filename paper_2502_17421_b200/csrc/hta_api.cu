@@ -370,7 +370,11 @@ hta_status_t run_prefix(const Shape &sh, const PrefixPlan &pl, const void *q, co
                                      s.d == 128 && pl.nt == 1 && HTA_F8S)) !=
                 HTA_OK)
                 return r;
-            if ((r = make_kv_map_fp8(&tv, v, s, pl.nt == 2 ? 64 : s.d, kBlockN)) != HTA_OK) return r;
+            // (d = 128, single CTAs of more than 64 rows, HTA_F8P: V is the MMA operand as landed,
+            // 128-byte swizzled -- prefix_tc.cu launches the KV8 = 2 kernel for exactly these)
+            if ((r = make_kv_map_fp8(&tv, v, s, pl.nt == 2 ? 64 : s.d, kBlockN,
+                                     s.d == 128 && pl.nt == 1 && pl.M > 64 && HTA_F8S && HTA_F8P)) != HTA_OK)
+                return r;
         } else if (pg != nullptr) {
             if ((r = make_pool_map(&tk, k, s, *pg)) != HTA_OK) return r;
             if ((r = make_pool_map(&tv, v, s, *pg)) != HTA_OK) return r;

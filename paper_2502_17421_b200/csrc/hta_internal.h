@@ -25,6 +25,12 @@ namespace hta {
 #define HTA_F8S 1
 #endif
 
+// ... and with it PV on kind::f8f6f4 (P as E4M3 + E5M2 terms in TMEM, V read as landed); 0 = V
+// widened to f16, f16 P
+#ifndef HTA_F8P
+#define HTA_F8P 1
+#endif
+
 #ifndef HTA_BLOCK_N
 #define HTA_BLOCK_N 128
 #endif

@@ -96,16 +96,20 @@ constexpr uint64_t kKvPolicy = kPolicyEvictFirst;  // L2 policy of the streamed 
 constexpr int kPolyPairs = HTA_POLY;               // pairs of every 8 whose exp2 runs on the FMA pipe
 // Largest P the speculative pass may produce (log2: kSpecArg): 2^60 for bf16 P; 2^15 for the f16 P
 // of the FP8-cache variant (f16 overflows at 65504).
-template <bool KV8>
+// F8P (FP8 cache, P as two 8-bit terms): P is formed as P' = P * 2^kPS and must stay below E4M3's
+// 448, so the speculative margin is kArg = 2.75 (P' <= 2^8.75) and is checked on every exponent
+// argument (kLimit unused); kPS = 6 keeps P down to 2^-22 above E5M2's 2^-16 floor.
+template <bool KV8, bool F8P = false>
 struct SpecCfg {
-    static constexpr float kLimit = KV8 ? 0x1p15f : 0x1p60f;
-    static constexpr float kArg = KV8 ? 15.f : 60.f;
+    static constexpr float kLimit = F8P ? INFINITY : (KV8 ? 0x1p15f : 0x1p60f);
+    static constexpr float kArg = F8P ? 2.75f : (KV8 ? 15.f : 60.f);
+    static constexpr float kPS = F8P ? 6.f : 0.f;
 };
 
 // The running max after a tile whose requirement is rho (its row max, or -inf when the tile
 // fits under m): raised only when some exponent argument would exceed kArg (P > 2^kArg).
-template <bool KV8>
-__device__ __forceinline__ float fold_max(float m, float rho) { return rho > m + SpecCfg<KV8>::kArg ? rho : m; }
+template <class Spec>
+__device__ __forceinline__ float fold_max(float m, float rho) { return rho > m + Spec::kArg ? rho : m; }
 
 #ifndef HTA_WIDEN_UNROLL
 #define HTA_WIDEN_UNROLL 4
@@ -325,18 +329,27 @@ __device__ __forceinline__ int paged_row(const PrefixParams &p, int b, int k) {
 
 // TREE: the fused tree pass (tree tiles appended to the last split); the kernels without it carry
 // none of its code, so their schedule is exactly that of the plain prefix pass.
-template <int D, bool PAIR, bool KV8, bool TREE>
+// KV8: 0 = bf16 cache; 1 = FP8 cache, V widened to f16; 2 = FP8 cache, PV on kind::f8f6f4 too
+// (single CTAs with d = 128 and more than 64 rows: F8P below)
+template <int D, bool PAIR, int KV8, bool TREE>
 __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
     prefix_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
                      const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ CUtensorMap tmap_kt,
                      const __grid_constant__ CUtensorMap tmap_vt, const PrefixParams p) {
     using C = TcCfg<D, PAIR>;
-    using Spec = SpecCfg<KV8>;
+    using Spec = SpecCfg<KV8 != 0, KV8 == 2>;
     // FP8 cache, d = 128, single CTAs: S = Q K^T runs on kind::f8f6f4 with the E4M3 K tile as landed
     // by TMA (no widening) and q as the sum of two E4M3 terms (q_hi + q_lo, per-CTA power-of-two
     // scale), so only V is widened to f16.  CTA pairs keep the widened K (their
     // one V producer warp per CTA sets the pace: the E4M3 S path measured 124.8 vs 115.5 us there).
-    constexpr bool F8S = KV8 && D == 128 && !PAIR && HTA_F8S;
+    constexpr bool F8S = KV8 != 0 && D == 128 && !PAIR && HTA_F8S;
+    // KV8 == 2: PV too -- P as an E4M3 term plus an E5M2 remainder (P' = P 2^kPS = P_hi + P_lo, ~7
+    // significant bits, down to 2^-16) in TMEM, V read by kind::f8f6f4 as TMA lands it (MN-major
+    // E4M3), so nothing is widened at all.  Not for units of at most 64 rows:
+    // there the softmax runs on two sub-partitions only and the split P costs more than the
+    // widening it saves (the idle warps of the other two widen V instead).
+    constexpr bool F8P = KV8 == 2 && F8S;
+    static_assert(KV8 != 2 || F8S, "KV8 == 2 needs the E4M3 S path (single CTAs, d = 128)");
     extern __shared__ __align__(1024) uint8_t smem[];  // 128B-swizzled tiles need 1024B alignment
     uint8_t *sQ = smem;
     uint8_t *sK = smem + C::kQBytes;
@@ -408,7 +421,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             mbar_init(&k_land[i], 1);
         }
         for (int i = 0; i < C::kSlotsV; ++i) {
-            mbar_init(&v_full[i], KV8 && PAIR ? 2 : (wide ? kWideWarps : 1));
+            mbar_init(&v_full[i], F8P ? 1 : (KV8 && PAIR ? 2 : (wide ? kWideWarps : 1)));
             mbar_init(&v_empty[i], 1);
             mbar_init(&v_land[i], 1);
         }
@@ -667,7 +680,34 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             // barrier of this CTA (v_tail_land); the MMA warp then waits on v_tail_ready (both CTAs
             // of a pair arrive) instead of v_full.
             const uint32_t vfull0 = PAIR ? mapa_shared(smem_u32(&v_full[0]), 0) : 0u;
-            if (KV8 && wide) {
+            if (F8P) {
+                // E4M3 V read by the MMA as landed: lane 0 lands every tile at its slot base on
+                // v_full, except the sequence-end tail tile, which lands on v_land and is
+                // sanitised here (E4M3 rows past the length zeroed) before v_full
+                const bool tail = tail_zero;
+                if (lane == 0)
+                    for (int j = 0; j < n_tiles; ++j) {
+                        const int slot = j % C::kSlotsV;
+                        mbar_wait(&v_empty[slot], ((j / C::kSlotsV) & 1) ^ 1u);
+                        HTA_TR(31, j);
+                        uint64_t *bar = tail && j == nc - 1 ? &v_land[slot] : &v_full[slot];
+                        mbar_arrive_expect_tx(bar, C::kVBytes / 2);
+                        tma_load_4d(sV + slot * C::kVBytes, &tmap_v, bar, 0, g, static_cast<int>(key_lo) + j * kBlockN,
+                                    b, kKvPolicy);
+                    }
+                __syncwarp();
+                if (tail) {
+                    const int slot = (nc - 1) % C::kSlotsV;
+                    mbar_wait(&v_land[slot], ((nc - 1) / C::kSlotsV) & 1);
+                    uint8_t *vt = sV + slot * C::kVBytes;
+                    for (int i = lane; i < (kBlockN - tail_valid) * 8; i += 32)
+                        *reinterpret_cast<uint4 *>(vt + (tail_valid + i / 8) * 128 + (i % 8) * 16) =
+                            make_uint4(0u, 0u, 0u, 0u);
+                    fence_proxy_async_smem();  // generic-proxy zeros -> read by the tensor core
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&v_full[slot]);
+                }
+            } else if (KV8 && wide) {
                 if (lane == 0)
                     for (int j = 0; j < n_tiles; ++j) {
                         const int slot = j % C::kSlotsV;
@@ -827,7 +867,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             const uint32_t idesc_pv = KV8 ? idesc_f16_f32(kM, D, 1) : idesc_bf16_f32(kM, D, 1);
             const uint64_t qd0 = sdesc_sw128(smem_u32(sQ), 16, 1024);
             const uint64_t kd0 = sdesc_sw128(smem_u32(sK), 16, 1024);
-            const uint64_t vd0 = sdesc_sw128(smem_u32(sV), kBlockN * 128, 1024);
+            const uint64_t vd0 = sdesc_sw128(smem_u32(sV), F8P ? 16384 : kBlockN * 128, 1024);
             auto commit = [](uint64_t *bar) {
                 if (PAIR)
                     tc_commit2_mc(bar);
@@ -896,15 +936,26 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 if (issuer) {
                     const uint32_t a_t = tmem + s_col(j % C::kSBufs);
                     const uint64_t vd = vd0 + static_cast<uint32_t>(((j % C::kSlotsV) * C::kVBytes) >> 4);
+                    if constexpr (F8P) {
+                        // E4M3 V MN-major SW128 (128-byte rows): 32 keys = +4096 B per K step; P_hi
+                        // (E4M3) in columns [0, 32) of the buffer, P_lo (E5M2) in [32, 64)
 #pragma unroll
-                    for (int k = 0; k < kBlockN / 16; ++k) {
-                        // MN-major SW128: 16 keys = two 8-row groups = +2048 B per K step
-                        if (PAIR)
-                            mma2_bf16_ts(tmem + kOCol, a_t + k * 8, vd + static_cast<uint32_t>(k * 128), idesc_pv,
-                                         (j > 0 || k > 0) ? 1u : 0u);
-                        else
-                            mma_bf16_ts(tmem + kOCol, a_t + k * 8, vd + static_cast<uint32_t>(k * 128), idesc_pv,
-                                        (j > 0 || k > 0) ? 1u : 0u);
+                        for (int k = 0; k < kBlockN / 32; ++k) {
+                            const uint64_t vk = vd + static_cast<uint32_t>((k * 4096) >> 4);
+                            mma_f8_ts(tmem + kOCol, a_t + k * 8, vk, idesc_f8_pv(128, D, 0), (j > 0 || k > 0) ? 1u : 0u);
+                            mma_f8_ts(tmem + kOCol, a_t + 32 + k * 8, vk, idesc_f8_pv(128, D, 1), 1u);
+                        }
+                    } else {  // (braced: see the S loop)
+#pragma unroll
+                        for (int k = 0; k < kBlockN / 16; ++k) {
+                            // MN-major SW128: 16 keys = two 8-row groups = +2048 B per K step
+                            if (PAIR)
+                                mma2_bf16_ts(tmem + kOCol, a_t + k * 8, vd + static_cast<uint32_t>(k * 128), idesc_pv,
+                                             (j > 0 || k > 0) ? 1u : 0u);
+                            else
+                                mma_bf16_ts(tmem + kOCol, a_t + k * 8, vd + static_cast<uint32_t>(k * 128), idesc_pv,
+                                            (j > 0 || k > 0) ? 1u : 0u);
+                        }
                     }
                     commit(&pv_done[j % C::kSBufs]);
                     commit(&v_empty[j % C::kSlotsV]);
@@ -1065,7 +1116,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             }
         };
         if constexpr (KV8 && !PAIR && D == 128) {
-            if (wide && quarter >= 2) {
+            if (wide && quarter >= 2 && !F8P) {
                 // ================= widening warp (FP8, <= 64 rows): warps of bands 0-1 widen K tiles,
                 // bands 2-3 V tiles; part = a quarter of the tile's rows.  V rows past the sequence
                 // end of the last tile are written as zeros (Z13).
@@ -1148,7 +1199,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             uint32_t pk[kHalf / 2];
             auto exp_pack = [&](float m_use, auto spec) {
                 constexpr bool kSpec = decltype(spec)::value;
-                const float2 c2 = make_float2(c, c), neg2 = make_float2(-m_use, -m_use);
+                const float2 c2 = make_float2(c, c), neg2 = make_float2(Spec::kPS - m_use, Spec::kPS - m_use);
                 float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int ch = 0; ch < kHalf / kChunk; ++ch) {
@@ -1164,6 +1215,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                             if (kSpec) xmax_poly = max3f(xmax_poly, x.x, x.y);
                             pp = exp2_poly2<!kSpec>(x);
                         } else {
+                            if (F8P && kSpec) xmax_poly = max3f(xmax_poly, x.x, x.y);  // (all slots: E4M3's range)
                             pp.x = fast_exp2(x.x);
                             pp.y = fast_exp2(x.y);
                         }
@@ -1171,7 +1223,24 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                             acc1 = __fadd2_rn(acc1, pp);
                         else
                             acc0 = __fadd2_rn(acc0, pp);
-                        pk[ch * (kChunk / 2) + i] = KV8 ? pack_f16x2(pp.x, pp.y) : pack_bf16x2(pp.x, pp.y);
+                        if constexpr (F8P) {
+                            // P' = P_hi (E4M3) + P_lo (E5M2 of the remainder); 4 keys per word,
+                            // P_hi words in pk[0, 16), P_lo words in pk[16, 32)
+                            const uint16_t h = f32x2_to_e4m3x2(pp.x, pp.y);
+                            const uint32_t hf = e4m3x2_to_f16x2(h);
+                            const __half2 hh = *reinterpret_cast<const __half2 *>(&hf);
+                            const uint16_t l = f32x2_to_e5m2x2(pp.x - __low2float(hh), pp.y - __high2float(hh));
+                            const int wi = (ch * (kChunk / 2) + i) >> 1;
+                            if ((i & 1) == 0) {
+                                pk[wi] = h;
+                                pk[16 + wi] = l;
+                            } else {
+                                pk[wi] |= static_cast<uint32_t>(h) << 16;
+                                pk[16 + wi] |= static_cast<uint32_t>(l) << 16;
+                            }
+                        } else {
+                            pk[ch * (kChunk / 2) + i] = KV8 ? pack_f16x2(pp.x, pp.y) : pack_bf16x2(pp.x, pp.y);
+                        }
                     }
                 }
                 return (acc0.x + acc1.x) + (acc0.y + acc1.y);
@@ -1190,7 +1259,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             // group's last fold; tile j-1 is folded in below).
             const float m_spec = m_run;
             float lsum = exp_pack(m_spec, std::true_type{});
-            const bool ovf = __any_sync(0xffffffffu, !(lsum <= Spec::kLimit) || xmax_poly > Spec::kArg);
+            const bool ovf = __any_sync(0xffffffffu, !(lsum <= Spec::kLimit) || xmax_poly > Spec::kArg + Spec::kPS);
             // rho_j: this tile's row max if the speculative pass overflowed, else -inf (the tile
             // needs no larger running max than the row already has).  Handed to the group of tile
             // j+1 at once: no group waits on the other before its own hand-over.
@@ -1218,10 +1287,10 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 }
                 // (TREE: a row may have seen no key at all yet, m = -inf, which the "no
                 // requirement" word -FLT_MAX would otherwise raise)
-                if (!TREE || (wv | 1u) != 0xFF7FFFFFu) m_prev = fold_max<KV8>(m_prev, __uint_as_float(wv));
+                if (!TREE || (wv | 1u) != 0xFF7FFFFFu) m_prev = fold_max<Spec>(m_prev, __uint_as_float(wv));
             }
             HTA_TRS(3);
-            const float m_fin = fold_max<KV8>(m_prev, rho);
+            const float m_fin = fold_max<Spec>(m_prev, rho);
             if (!TREE) {
                 if (__any_sync(0xffffffffu, ovf || m_fin != m_spec)) lsum = exp_pack(m_fin, std::false_type{});
             } else if (__any_sync(0xffffffffu, ovf || m_fin != m_spec)) {
@@ -1233,7 +1302,10 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                 }
             }
             // P_j over S_j in TMEM (columns [Ch/2, Ch/2 + 32)), without waiting
-            if (!(HTA_DIAG & 1)) {
+            if constexpr (F8P) {  // P_hi in columns [16 chalf, +16), P_lo 32 columns further
+                tmem_st_16x16_split_nowait<16>(tmem + lane_off + s_col(buf), pk);
+                tmem_st_16x16_split_nowait<16>(tmem + lane_off + s_col(buf) + 32, pk + 16);
+            } else if (!(HTA_DIAG & 1)) {
 #pragma unroll
                 for (int w0 = 0; w0 < kHalf / 2; w0 += 16) {  // 16 packed words per store, then the rest
                     if (kHalf / 2 - w0 >= 16)
@@ -1314,7 +1386,8 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             }
         }
         if (row_ok && chalf == 0 && grp == 0)
-            lse_base[(static_cast<int64_t>(b) * p.H + h) * p.T + t] = (m_tot + log2f(l_tot)) * 0.69314718055994530942f;
+            lse_base[(static_cast<int64_t>(b) * p.H + h) * p.T + t] =
+                (m_tot + log2f(l_tot) - Spec::kPS) * 0.69314718055994530942f;  // (l_tot holds P' = P 2^kPS)
     }
 
     HTA_TR(63, 0);
@@ -1337,7 +1410,7 @@ extern "C" __attribute__((visibility("default"))) int hta_debug_set_trace(void *
 }
 #endif
 
-template <int D, bool PAIR, bool KV8, bool TREE = false>
+template <int D, bool PAIR, int KV8, bool TREE = false>
 static cudaError_t launch_tc(const PrefixParams &p, const CUtensorMap &tq, const CUtensorMap &tk, const CUtensorMap &tv,
                              const CUtensorMap &tkt, const CUtensorMap &tvt, cudaStream_t s) {
     using C = TcCfg<D, PAIR>;
@@ -1382,9 +1455,10 @@ cudaError_t launch_prefix_tc(const PrefixParams &p, const CUtensorMap &tq, const
     if (p.kv8) {
         if (p.tree_tiles != 0) return cudaErrorInvalidValue;  // (the FP8 variant has no fused tree pass)
         if (p.d == 128)
-            return p.nt == 2 ? launch_tc<128, true, true>(p, tq, tk, tv, tkt, tvt, s)
-                             : launch_tc<128, false, true>(p, tq, tk, tv, tkt, tvt, s);
-        if (p.d == 64 && p.nt == 1) return launch_tc<64, false, true>(p, tq, tk, tv, tkt, tvt, s);
+            return p.nt == 2 ? launch_tc<128, true, 1>(p, tq, tk, tv, tkt, tvt, s)
+                   : (p.M > 64 && HTA_F8S && HTA_F8P) ? launch_tc<128, false, 2>(p, tq, tk, tv, tkt, tvt, s)
+                                                       : launch_tc<128, false, 1>(p, tq, tk, tv, tkt, tvt, s);
+        if (p.d == 64 && p.nt == 1) return launch_tc<64, false, 1>(p, tq, tk, tv, tkt, tvt, s);
         return cudaErrorInvalidValue;
     }
     if (p.tree_tiles < 0 || p.tree_tiles > (256 + kBlockN - 1) / kBlockN) return cudaErrorInvalidValue;

@@ -310,6 +310,29 @@ __device__ __forceinline__ void mma2_e4m3_ss(uint32_t d_tmem, uint64_t a_desc, u
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem], 8-bit operands (kind::f8f6f4, K = 32 per instruction; A holds four
+// elements per 32-bit TMEM column)
+__device__ __forceinline__ void mma_f8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Instruction descriptor for kind::f8f6f4 with A of format a_fmt (0 = E4M3, 1 = E5M2) K-major and
+// E4M3 B MN-major, fp32 accumulate.
+__host__ __device__ constexpr uint32_t idesc_f8_pv(int M, int N, int a_fmt) {
+    return (1u << 4) | (static_cast<uint32_t>(a_fmt) << 7) | (1u << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(M >> 4) << 24);
+}
+// Two floats -> E5M2x2 (round to nearest even, saturating; low byte = lo).
+__device__ __forceinline__ uint16_t f32x2_to_e5m2x2(float lo, float hi) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+    return r;
+}
 // Two floats -> E4M3x2 (round to nearest even, saturating to +-448; low byte = lo).
 __device__ __forceinline__ uint16_t f32x2_to_e4m3x2(float lo, float hi) {
     uint16_t r;

@@ -117,3 +117,19 @@ def test_fp8kv_q_dynamic_range(cuda_device, spread):
                                  torch.from_numpy(mask).to(cuda_device))
     torch.cuda.synchronize()
     compare(o, l, o_ref, l_ref, "bf16", f"fp8 q spread {spread}")
+
+
+@pytest.mark.parametrize("dist", ["V0", "V1"])
+def test_fp8kv_long_context_split_p(cuda_device, dist):
+    """Single-CTA units of more than 64 rows run PV on kind::f8f6f4 with P as an E4M3 term plus an
+    E5M2 remainder.  A 16k-key context spreads the softmax over many small P
+    values (down to E5M2's floor); the bf16 tolerances must still hold against the oracle."""
+    w = make_workload(1, 64, 16, 8, 128, 16384, "bf16", dist=dist, seed=37, tree="beam")
+    mask = oracle_masks(w)
+    k8, ks, v8, vs, x = _fp8(w, cuda_device)
+    o_ref, l_ref = oracle.attention_fp8kv(w.q, k8, v8, ks, vs, w.k_tree, w.v_tree, mask)
+    o, l = hta.hta_forward_fp8kv(w.q.to(cuda_device), x["k8"], x["v8"], x["ks"], x["vs"],
+                                 w.k_tree.to(cuda_device), w.v_tree.to(cuda_device),
+                                 torch.from_numpy(mask).to(cuda_device))
+    torch.cuda.synchronize()
+    compare(o, l, o_ref, l_ref, "bf16", f"fp8 split-P {dist}")
