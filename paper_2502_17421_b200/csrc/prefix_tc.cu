@@ -82,13 +82,6 @@ constexpr int kTraceRecs = 1024;  // per warp
     } while (0)
 #endif
 
-// Timing diagnostics only (tools/lib_variants.sh; results are wrong): HTA_DIAG bit 1 = no P
-// stores to TMEM, bit 2 = no exponentials (P = x), bit 4 = no wait for the row-max hand-over,
-// bit 8 = FP8 pair widening signalled with a CTA-scope (not cluster-scope) release.
-#ifndef HTA_DIAG
-#define HTA_DIAG 0
-#endif
-
 constexpr uint64_t kKvPolicy = kPolicyEvictFirst;  // L2 policy of the streamed K/V tiles (read once)
 #ifndef HTA_POLY
 #define HTA_POLY 2
@@ -591,9 +584,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     __syncwarp();
                     HTA_TR(32, j);
                     if (lane == 0) {
-                        if (PAIR && (HTA_DIAG & 8))
-                            mbar_arrive_remote(kfull0 + 8u * slot);
-                        else if (PAIR)
+                        if (PAIR)
                             mbar_arrive_remote_release_cluster(kfull0 + 8u * slot);
                         else
                             mbar_arrive(&k_full[slot]);
@@ -748,9 +739,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     __syncwarp();
                     HTA_TR(33, j);
                     if (lane == 0) {
-                        if (PAIR && (HTA_DIAG & 8))
-                            mbar_arrive_remote(vfull0 + 8u * slot);
-                        else if (PAIR)
+                        if (PAIR)
                             mbar_arrive_remote_release_cluster(vfull0 + 8u * slot);
                         else
                             mbar_arrive(&v_full[slot]);
@@ -1209,9 +1198,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
                     for (int i = 0; i < kChunk / 2; ++i) {
                         const float2 x = __ffma2_rn(s2[i], c2, neg2);
                         float2 pp;
-                        if (HTA_DIAG & 2) {
-                            pp = x;
-                        } else if ((i & 7) < kPolyPairs) {
+                        if ((i & 7) < kPolyPairs) {
                             if (kSpec) xmax_poly = max3f(xmax_poly, x.x, x.y);
                             pp = exp2_poly2<!kSpec>(x);
                         } else {
@@ -1276,7 +1263,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             // the running max after tile j-1 (fold of rho_{j-1}), then after tile j; both groups
             // fold the same sequence rho_0, rho_1, ... and agree on every tile's max
             float m_prev = m_run;
-            if (j > 0 && !(HTA_DIAG & 4)) {
+            if (j > 0) {
                 const uint32_t *src = &m_sh[((j - 1) % 3) * 128 + r];
                 const uint32_t want = static_cast<uint32_t>(((j - 1) / 3) & 1);
                 uint32_t wv = ld_volatile_shared(src);
@@ -1305,7 +1292,7 @@ __global__ void __launch_bounds__(TcCfg<D, PAIR>::kThreads, 1)
             if constexpr (F8P) {  // P_hi in columns [16 chalf, +16), P_lo 32 columns further
                 tmem_st_16x16_split_nowait<16>(tmem + lane_off + s_col(buf), pk);
                 tmem_st_16x16_split_nowait<16>(tmem + lane_off + s_col(buf) + 32, pk + 16);
-            } else if (!(HTA_DIAG & 1)) {
+            } else {
 #pragma unroll
                 for (int w0 = 0; w0 < kHalf / 2; w0 += 16) {  // 16 packed words per store, then the rest
                     if (kHalf / 2 - w0 >= 16)
