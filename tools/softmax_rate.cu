@@ -21,7 +21,9 @@ __device__ __forceinline__ uint32_t ex2_f16x2(uint32_t x) {
     return y;
 }
 // (pack_f16x2: from ptx_sm100.cuh)
-template <int EMU8, bool SPREAD = false>
+// PACK: 0 = cvt.rn.bf16x2.f32 (the kernel's), 1 = truncation by one byte permute (the row sum then
+// adds the truncated values: one AND per element)
+template <int EMU8, bool SPREAD = false, int PACK = 0>
 __global__ void __launch_bounds__(256, 1) softmax_loop(int iters, float c, float *out) {
     float s[64];
 #pragma unroll
@@ -62,11 +64,16 @@ __global__ void __launch_bounds__(256, 1) softmax_loop(int iters, float c, float
                 pp.x = fast_exp2(x.x);
                 pp.y = fast_exp2(x.y);
             }
+            if (PACK == 1) {
+                const uint32_t ux = __float_as_uint(pp.x) & 0xFFFF0000u, uy = __float_as_uint(pp.y) & 0xFFFF0000u;
+                pp = make_float2(__uint_as_float(ux), __uint_as_float(uy));
+                sink ^= __byte_perm(ux, uy, 0x7632);
+            }
             if (i & 1)
                 acc1 = __fadd2_rn(acc1, pp);
             else
                 acc0 = __fadd2_rn(acc0, pp);
-            sink ^= pack_bf16x2(pp.x, pp.y);
+            if (PACK == 0) sink ^= pack_bf16x2(pp.x, pp.y);
         }
         acc_all += (acc0.x + acc1.x) + (acc0.y + acc1.y);
         m += 1e-7f;  // loop-carried so the compiler cannot hoist the exps
@@ -74,7 +81,7 @@ __global__ void __launch_bounds__(256, 1) softmax_loop(int iters, float c, float
     if (sink == 0x12345 || acc_all == 1.2345f) out[threadIdx.x] = acc_all;
 }
 
-template <int EMU8, bool SPREAD = false>
+template <int EMU8, bool SPREAD = false, int PACK = 0>
 void run(int threads = 256) {
     float *out;
     cudaMalloc(&out, 4096);
@@ -85,7 +92,7 @@ void run(int threads = 256) {
     float best = 1e9;
     for (int r = 0; r < 4; ++r) {
         cudaEventRecord(e0);
-        softmax_loop<EMU8, SPREAD><<<148, threads>>>(iters, 0.12f, out);
+        softmax_loop<EMU8, SPREAD, PACK><<<148, threads>>>(iters, 0.12f, out);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
@@ -94,8 +101,9 @@ void run(int threads = 256) {
     }
     // per SMSP: threads/128 warps x 64 elements x iters
     const double elems_per_smsp = threads / 128.0 * 64 * iters;
-    printf("mode %d/8%s, %d warps/SMSP: %8.1f us  -> %.2f cycles per 32-wide element slot per SMSP @1.9GHz\n", EMU8,
-           SPREAD ? " spread" : "", threads / 128, best * 1e3, best * 1e-3 * 1.9e9 / elems_per_smsp);
+    printf("mode %d/8%s%s, %d warps/SMSP: %8.1f us  -> %.2f cycles per 32-wide element slot per SMSP @1.9GHz\n",
+           EMU8, SPREAD ? " spread" : "", PACK ? " trunc-pack" : "", threads / 128, best * 1e3,
+           best * 1e-3 * 1.9e9 / elems_per_smsp);
 }
 
 int main() {
@@ -108,6 +116,9 @@ int main() {
         run<3, true>(t);
         run<4>(t);
         run<8>(t);
+        run<2, false, 1>(t);
+        run<3, false, 1>(t);
+        run<0, false, 1>(t);
     }
     return 0;
 }
