@@ -213,11 +213,15 @@ hta_status_t hta_forward_paged(const hta_shape_t *shape, const void *q, const vo
  *                     K = k_scale[g] * K8,  V = v_scale[g] * V8  for KV head g
  *   k_scale, v_scale  device float32 [H_kv]
  *   q, k_tree, v_tree, o   bf16 (shape->dtype must be HTA_BF16; d 64 or 128)
- * The E4M3 tiles are widened to f16 in shared memory (exact) and q is converted to f16 (exact in
- * the f16 range), so the prefix contraction runs on the tensor cores in f16 with fp32
- * accumulation and P rounded to f16; the HBM traffic of the cache is halved.  The result matches
- * hybrid tree attention over the decoded cache within the bf16 tolerances (DESIGN.md "FP8 KV
- * cache").  Workspace and errors as hta_forward; HTA_ERR_UNSUPPORTED for dtype fp32. */
+ * The HBM traffic of the cache is halved.  The prefix contraction runs on the tensor cores with
+ * fp32 accumulation: for one-CTA row groups with d = 128, S = q K^T on the FP8
+ * tensor path straight from the E4M3 K tile with q split into two E4M3 terms at a power-of-two
+ * scale per row (bf16 q reproduced to within 2^-17 of its row maximum), and, when a group has
+ * more than 64 rows, P V on the FP8 path too with P as an E4M3 + E5M2 pair (about bf16's
+ * precision; P below 2^-22 of the running maximum dropped); otherwise the E4M3 tiles are widened
+ * to f16 in shared memory (exact), q is converted to f16 and P rounded to f16.  The result
+ * matches hybrid tree attention over the decoded cache within the bf16 tolerances.  Workspace and
+ * errors as hta_forward; HTA_ERR_UNSUPPORTED for dtype fp32. */
 hta_status_t hta_forward_fp8kv(const hta_shape_t *shape, const void *q, const void *k_cache,
                                const void *v_cache, const float *k_scale, const float *v_scale,
                                const int32_t *cache_seqlens, const void *k_tree,
