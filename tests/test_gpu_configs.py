@@ -67,3 +67,25 @@ def test_draft_cross_attention_full_size(cuda_device, T):
                               rows=rows)
     idx = torch.tensor(rows)
     compare(o[idx[:, 0], idx[:, 1], idx[:, 2]], l[idx[:, 0], idx[:, 2], idx[:, 1]], ro, rl, "bf16", f"xattn T={T}")
+
+
+@pytest.mark.parametrize("name", ["qwq32b_32k_b4", "longchat7b_16k", "llama8b_64k"])
+def test_fp8kv_full_size_sampled(cuda_device, name):
+    """SURVEY.md §8(f) f4 at full size: hta_forward_fp8kv over an E4M3 copy of the config's cache
+    (per-KV-head power-of-two scales), sampled rows against the oracle over the decoded cache.
+    QwQ runs the split-P PV variant (single CTAs of more than 64 rows), LongChat the E4M3 S path
+    with V widened (64-row units), Llama the CTA-pair path with K and V widened."""
+    from workloads import fp8_cache
+    w = config_workload(name, dist="V1", seed=0)
+    mask = oracle_masks(w)
+    k8, ks = fp8_cache(w.k_cache)
+    v8, vs = fp8_cache(w.v_cache)
+    dev = cuda_device
+    o, l = hta.hta_forward_fp8kv(w.q.to(dev), k8.to(dev), v8.to(dev), ks.to(dev), vs.to(dev), w.k_tree.to(dev),
+                                 w.v_tree.to(dev), torch.from_numpy(mask).to(dev), cache_seqlens=w.seqlens.to(dev))
+    torch.cuda.synchronize()
+    rows = sample_rows(w.B, w.T, w.H, 256, seed=2)
+    ro, rl = oracle.attention_fp8kv(w.q, k8, v8, ks, vs, w.k_tree, w.v_tree, mask, seqlens=w.seqlens, rows=rows)
+    idx = torch.tensor(rows)
+    compare(o[idx[:, 0], idx[:, 1], idx[:, 2]], l[idx[:, 0], idx[:, 2], idx[:, 1]], ro, rl, "bf16", f"fp8 {name}")
+    assert torch.isfinite(o.float()).all() and torch.isfinite(l).all()
